@@ -1,0 +1,113 @@
+"""The preconditioner P_α⁻¹: the paper's three steps (ORACLE — test infrastructure only).
+
+Linear problems, P:158-165 (eq. pintiter1):
+  Step-(1)  S1 = (F ⊗ I)(Γ_α ⊗ I) r
+  Step-(2)  S2_l = (λ_{1,l} I + λ_{2,l} A)⁻¹ S1_l,  l = 0..N_t-1   (λ_1 = d_l, λ_2 = e_l, R#1)
+  Step-(3)  δ = (Γ_α⁻¹ ⊗ I)(F* ⊗ I) S2 / N_t
+Cahn-Hilliard PinT-I, P:491-499 (eq. pintiter_CH): Step-(2) matrix
+  λ_{1,l} I - Δ_h J̃ + Δ_h + ε²Δ_h²  with J̃ = J̄₃·I (scalar space-time mean of 3u², R#7/R#8),
+  i.e. d_l I - J̄ Δ_h + ε² Δ_h² with J̄ = mean(3u² - 1).
+
+Step-(2) solvers (a library primitive may serve as a step):
+  1D: banded LU with partial pivoting (LAPACK gbsv via scipy.linalg.solve_banded) of the assembled
+      pentadiagonal, then iterative refinement whose residual is evaluated in nested form (R#15)
+      until the correction is below 1e-15 relative (SURVEY §8(c) oracle step 3.3).
+  2D: eigenbasis of the separable Δ_h: unnormalised DST-I / DCT-I matrices (direct sums, one
+      matmul per axis), divide by the mode eigenvalue, inverse transform (T² = 2m·I).
+"""
+import numpy as np
+from scipy.linalg import solve_banded
+
+from . import spatial, circulant
+
+
+def _step2_operator_nested(prob, jbar):
+    """x ↦ A_eff x in nested form, where Step-(2) solves (d_l I + e_l A_eff) x = s."""
+    if prob.kind == "cahn_hilliard":
+        _, e2 = spatial.coeffs(prob)
+
+        def op(x):
+            l1 = spatial.lap(x, prob.m, prob.bc, prob.dim)
+            return -jbar * l1 + e2 * spatial.lap(l1, prob.m, prob.bc, prob.dim)
+        return op
+    return lambda x: spatial.apply_A(x, prob)
+
+
+def _step2_mu(prob, jbar):
+    """Eigenvalue of A_eff on the mode grid."""
+    Lam = spatial.Lam_grid(prob)
+    if prob.kind == "cahn_hilliard":
+        _, e2 = spatial.coeffs(prob)
+        return -jbar * Lam + e2 * (Lam * Lam)
+    return spatial.mu(Lam, prob)
+
+
+def _A_eff_matrix_1d(prob, jbar):
+    D = spatial.lap_matrix_1d(prob.m, prob.bc)
+    if prob.kind == "cahn_hilliard":
+        _, e2 = spatial.coeffs(prob)
+        return -jbar * D + e2 * (D @ D)
+    return spatial.A_matrix_1d(prob)
+
+
+def _to_banded(M: np.ndarray, kl: int, ku: int) -> np.ndarray:
+    """LAPACK band storage: ab[ku + i - j, j] = M[i, j]."""
+    n = M.shape[0]
+    ab = np.zeros((kl + ku + 1, n), dtype=M.dtype)
+    for k in range(-ku, kl + 1):                 # k = i - j
+        diag = np.diagonal(M, -k)
+        if k >= 0:
+            ab[ku + k, :n - k] = diag
+        else:
+            ab[ku + k, -k:] = diag
+    return ab
+
+
+def step2_1d(prob, S1: np.ndarray, jbar: float = 0.0, max_refine: int = 6) -> np.ndarray:
+    """Step-(2) in 1D: per bin, banded LU (partial pivoting) + nested-residual refinement."""
+    nt, n = S1.shape
+    d = circulant.eig_d(nt, prob.alpha, circulant.inv_dt(prob))
+    e = circulant.eig_e(nt, prob.alpha, prob.theta)
+    A_band = _to_banded(_A_eff_matrix_1d(prob, jbar), 2, 2)      # assembled pentadiagonal
+    I_band = _to_banded(np.eye(n), 2, 2)
+    op = _step2_operator_nested(prob, jbar)
+    out = np.empty_like(S1)
+    for l in range(nt):
+        ab = d[l] * I_band + e[l] * A_band                          # d_l I + e_l A, banded
+        s = S1[l]
+        x = solve_banded((2, 2), ab, s)
+        for _ in range(max_refine):
+            Ax = op(x.real) + 1j * op(x.imag)
+            rho = s - (d[l] * x + e[l] * Ax)
+            c = solve_banded((2, 2), ab, rho)
+            x = x + c
+            if np.abs(c).max() <= 1e-15 * np.abs(x).max():
+                break
+        out[l] = x
+    return out
+
+
+def step2_2d(prob, S1: np.ndarray, jbar: float = 0.0) -> np.ndarray:
+    """Step-(2) in 2D: separable eigenbasis solve per bin."""
+    nt = S1.shape[0]
+    d = circulant.eig_d(nt, prob.alpha, circulant.inv_dt(prob))
+    e = circulant.eig_e(nt, prob.alpha, prob.theta)
+    T = spatial.transform_matrix(prob.m, prob.bc)
+    mu = _step2_mu(prob, jbar)                        # [q, p]
+    hat = T @ S1 @ T.T                                 # Ty S Txᵀ for every bin
+    denom = d[:, None, None] + e[:, None, None] * mu[None, :, :]
+    hat = hat / denom
+    return (T @ hat @ T.T) / (2.0 * prob.m) ** 2
+
+
+def apply_precond(prob, r: np.ndarray, jbar: float = 0.0):
+    """δ = P_α⁻¹ r, r shaped [N_t, N_x] (1D) or [N_t, N_y, N_x] (2D).
+
+    Returns (δ, max|Im|/max|Re| after Step-(3)) — the imaginary residue of S:336.
+    """
+    S1 = circulant.step1(r, prob.alpha)
+    if prob.dim == 1:
+        S2 = step2_1d(prob, S1, jbar)
+    else:
+        S2 = step2_2d(prob, S1, jbar)
+    return circulant.step3(S2, prob.alpha)
