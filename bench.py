@@ -1,0 +1,270 @@
+#!/usr/bin/env python
+"""bench.py — ParaDiag iteration throughput on B200 (BASELINE.json metric).
+
+metric: space-time dof/s per ParaDiag iteration (fp64) and % of HBM roofline.
+workload: BASELINE.json configs[4] (c5): 2D linearised Cahn-Hilliard, Neumann, 2049² nodes,
+N_t = 512, T = 0.5, α = 1e-4, β = 0.4, ε = 0.01, U⁰ = 0.  A step is one ParaDiag
+iteration through the public C ABI (paradiag_iterate): residual + P_α⁻¹ (5 passes) + update and
+the 4-scalar read-back.  Inputs (17.2 GB per array) are far larger than L2 (126 MB), so no L2
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
+
+Multi-GPU (torchrun): round 1 runs independent replicas per rank (weak scaling); the sharded
+all-to-all path is DESIGN.md §8 "next".
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_DOF = {  # algorithmic HBM bytes per space-time dof per launch
+    "residual": 16.0, "dtt_x_fwd": 16.0, "dtt_y_fwd": 16.0, "time_solve_2d": 16.0,
+    "dtt_y_inv": 16.0, "dtt_x_inv": 16.0, "update": 24.0,
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+            "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+            "clocks_event_reasons.sw_power_cap"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.samples if len(r) >= 7 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def oracle_sample_problem(name):
+    """Bounded sample of the workload for the CPU oracle: same physics and N_t, 65² nodes."""
+    from workloads import twin
+    return twin(name, m=64)
+
+
+def time_oracle(name, steps, warmup):
+    """Time the oracle (as it stands) on the bounded sample; returns (dof/s, cores, desc, s/step)."""
+    import numpy as np
+    from oracle import iterate
+    from workloads import make_u0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        cores = os.cpu_count()
+    p = oracle_sample_problem(name)
+    u0 = make_u0(p)
+    U = iterate.initial_iterate(p, u0)
+    for _ in range(warmup):
+        U, _ = iterate.iterate_once(p, u0, U)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        U, _ = iterate.iterate_once(p, u0, U)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    desc = (f"oracle iterate_once (numpy fp64, naive O(N_t^2) DFT, dense DCT-I matmuls) on a "
+            f"{p.ny}x{p.nx} x N_t={p.nt} twin of {name} ({p.dofs} dofs), {steps} iteration(s)")
+    return p.dofs / dt, cores, desc, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="per-kernel event timing (on by default)")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from workloads import config, make_u0
+    p = config(args.config)
+    metric = "space-time dof/s per ParaDiag iteration (fp64)"
+    cfg = {"workload": f"BASELINE.json configs[4] ({args.config}): 2D linearised Cahn-Hilliard, Neumann, "
+                       f"{p.ny}x{p.nx} nodes, N_t={p.nt}, T={p.t_window}, alpha={p.alpha}, beta={p.beta}, "
+                       f"eps={p.eps}, U0=0" if args.config == "c5" else args.config,
+           "dofs_per_iteration": p.dofs, "l2": "inputs 17.2 GB/array >> 126 MB L2 (no flush needed)"
+           if args.config == "c5" else "see dofs"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        v, cores, desc, dt = time_oracle(args.config, args.steps, args.warmup)
+        line = {"metric": metric, "value": v, "unit": "dof/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
+                "cpu_baseline": {"value": v, "unit": "dof/s", "cores": cores, "kind": "oracle", "sample": desc},
+                "e2e": {"value": v, "unit": "dof/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2304_14021_b200 as pd
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    u0 = make_u0(p)
+    u0_d = torch.from_numpy(u0).to(dev)
+    s = pd.Solver(p, device=local, stream=stream.cuda_stream)
+    U = torch.zeros(s.shape, dtype=torch.float64, device=dev)       # U⁰ = 0 (R#5)
+    info = pd.pd_iter_info()
+    for _ in range(args.warmup):
+        info = s.iterate(u0_d, U, info)
+    s.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            info = s.iterate(u0_d, U, info)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = s.profile_read()
+    s.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * p.dofs / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (largest device time in the timed region)
+    peak, peak_src = measured_peaks()
+    top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    kernels = {}
+    for name, (n, tot) in prof.items():
+        avg = tot / max(n, 1)
+        bpd = BYTES_PER_DOF.get(name)
+        kernels[name] = {"avg_ms": avg, "share": tot / (ms if ms > 0 else 1),
+                         "gbs": (bpd * p.dofs / (avg * 1e-3) / 1e9) if bpd else None}
+    if top:
+        name, (n, tot) = top
+        avg = tot / n
+        bpd = BYTES_PER_DOF.get(name, 16.0)
+        ach = bpd * p.dofs / (avg * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(name)
+        except Exception:
+            pass
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_source": peak_src, "traffic": traffic,
+                "algorithmic_bytes_per_launch": bpd * p.dofs}
+    # whole-iteration HBM efficiency at the design byte count
+    design_bytes = sum(BYTES_PER_DOF[k] for k in BYTES_PER_DOF) * p.dofs
+
+    # end-to-end through the host-buffer C-ABI call (H2D u0, K iterations, D2H u_{N_t})
+    e2e = None
+    if not args.no_e2e:
+        from dataclasses import replace
+        pe = replace(p, fixed_iters=p.fixed_iters or 3)
+        se = pd.Solver(pe, device=local, stream=stream.cuda_stream)
+        u0h = np.ascontiguousarray(u0)
+        se.solve_host(u0h)           # warm-up (allocates the library-owned iterate)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        reps = 2
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            uT, rc, sinfo = se.solve_host(u0h)
+        te = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": world * pe.fixed_iters * pe.dofs / te, "unit": "dof/s",
+               "h2d_bytes_per_step": int(u0h.nbytes), "d2h_bytes_per_step": int(uT.nbytes + 32 * pe.fixed_iters),
+               "step": f"paradiag_solve_host: H2D u0, {pe.fixed_iters} iterations, D2H u_Nt",
+               "seconds_per_step": te}
+        se.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc, dt = time_oracle(args.config, 1, 0)
+        cpu = {"value": v, "unit": "dof/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "dof/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(cfg, parallelism="replicas" if world > 1 else "single-gpu"),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps * s.launches_per_iteration(),
+                "clocks": clk.summary(), "kernels": kernels,
+                "iteration_hbm_frac_at_design_bytes": design_bytes / (ms_step * 1e-3) / 1e9 / peak,
+                "last_iter": {"delta_max": info.delta_max, "u_max": info.u_max}}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,184 @@
+/*
+ * paradiag.h — C ABI of the B200-native ParaDiag preconditioner library (libparadiag.so).
+ *
+ * Garai & Mandal, "Diagonalization Based Parallel-in-Time Method for a Class of Fourth Order
+ * Time Dependent PDEs" (arXiv 2304.14021).  Citations "P:L" are lines of /root/reference/PAPER.md;
+ * "R#n" are the readings listed in DESIGN.md §3.
+ *
+ * The hot path is the α-circulant preconditioner application δ = P_α⁻¹ r, the paper's three
+ * steps (eq. pintiter1; CH PinT-I P:491-499, eq. pintiter_CH):
+ *   Step-(1) scale by Γ_α = diag(α^{j/N_t}) and DFT along time for every spatial dof;
+ *   Step-(2) N_t independent shifted spatial solves (d_l I + A) x = ŝ_l  (1D: pentadiagonal LU
+ *            + one nested-residual refinement; 2D: DCT-I (Neumann) / DST-I (hinged) diagonalisation,
+ *            CH: per-mode divide by d_l - J̄Λ + ε²Λ²);
+ *   Step-(3) inverse DFT along time and unscale by Γ_α⁻¹.
+ * plus the all-at-once residual r = b - K(U) and the defect-correction
+ * update U ← U + ω δ that together form one ParaDiag iteration.
+ *
+ * Conventions for every entry point
+ *  - Pointers named d_* / U / r / delta / u0 are CUDA DEVICE pointers to float64 arrays owned by
+ *    the caller; the library owns only its internal workspace.  *_host entry points take HOST
+ *    pointers instead (pageable or pinned).
+ *  - Layout: U, r, delta are [nt][ny][nx] row-major contiguous (time slowest, x fastest), holding
+ *    u_1..u_{N_t} (u_0 excluded, as the paper's U).  u0 is [ny][nx].  ny = 1 in 1D.
+ *    Neumann unknowns include the boundary nodes (m+1 per axis); hinged (u = Δu = 0,
+ *    P:703 case (ii)) unknowns are the interior nodes (m-1 per axis).  h = 1/m.
+ *  - Work is enqueued on the stream passed to paradiag_init, in order.  apply_precond and
+ *    residual are asynchronous; iterate / solve synchronise once per iteration on 4 scalars.
+ *  - A handle must not be used from two host threads at once.
+ *  - Return value: PD_OK (0), PD_NOT_CONVERGED (1, a status), or a negative error code;
+ *    paradiag_strerror() names it and paradiag_last_error() gives a detail string for the
+ *    calling thread.  No entry point falls back to a CPU path: without a usable sm_100a device
+ *    they return PD_ECUDA.
+ */
+#ifndef PARADIAG_H
+#define PARADIAG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARADIAG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PD_API __attribute__((visibility("default")))
+#else
+#define PD_API
+#endif
+
+/* return codes (SPEC-style error convention) */
+#define PD_OK              0
+#define PD_NOT_CONVERGED   1   /* status, not an error: non-convergence is a flag            */
+#define PD_EINVAL        (-1)  /* invalid problem / argument                                  */
+#define PD_ESINGULAR     (-2)  /* some shifted system d_l + e_l μ is (numerically) singular   */
+#define PD_ECUDA         (-3)  /* CUDA runtime failure (incl. no device / wrong arch)          */
+#define PD_ENCCL         (-4)  /* reserved: multi-GPU communicator failure                     */
+#define PD_ENOMEM        (-5)  /* device allocation failed                                     */
+#define PD_EDIVERGED     (-6)  /* non-finite iterate / increment                               */
+
+/* problem kinds */
+#define PD_BIHARMONIC      0   /* u_t = -Δ²u                      A = Δ_h²  */
+#define PD_LINEAR_CH       1   /* u_t = -β²Δu - ε²Δ²u             A = β²Δ_h + ε²Δ_h²  */
+#define PD_CAHN_HILLIARD   2   /* u_t = Δ(u³ - u - ε²Δu), PinT-I           */
+
+/* boundary conditions */
+#define PD_BC_NEUMANN      0   /* ∂u = ∂Δu = 0, paper Δ_h with ghost reflection */
+#define PD_BC_HINGED       1   /* u = Δu = 0 (P:703 case (ii)), zero ghosts at each Δ_h (R#14)  */
+
+/* initial iterate U⁰ (R#5) */
+#define PD_INIT_BROADCAST  0   /* U⁰_n = u0 for every n */
+#define PD_INIT_ZERO       1   /* U⁰ = 0                */
+
+typedef struct pd_problem {
+  int32_t kind;          /* PD_BIHARMONIC | PD_LINEAR_CH | PD_CAHN_HILLIARD                     */
+  int32_t bc;            /* PD_BC_NEUMANN | PD_BC_HINGED (CH: Neumann only)                */
+  int32_t dim;           /* 1 or 2 (CH: 2 only)                                                  */
+  int32_t nt;            /* time steps per window, power of two in [2, 4096]                     */
+  int64_t m;             /* intervals per axis, h = 1/m; 2D: power of two in [4, 4096]; 1D ≥ 4   */
+  double  t_window;      /* window length T; Δt = T / nt, 1/Δt evaluated as nt / T (R#20)        */
+  double  alpha;         /* PinT parameter α ∈ (0, 1)                              */
+  double  theta;         /* θ-method parameter; 1.0 (backward Euler) only                        */
+  double  beta;          /* LINEAR_CH β; β² := fl(β·β)                                     */
+  double  eps;           /* LINEAR_CH / CH ε ≥ 0; ε² := fl(ε·ε)                                   */
+  double  tol;           /* stop when ‖δ‖∞ ≤ tol·‖U‖∞ (R#4)                                       */
+  double  omega;         /* damping cap: ω_k = min(omega, tau/‖δ_k‖∞) for CH (R#9); linear ω = 1 */
+  double  tau;
+  int32_t n_windows;     /* sequential windows, u0 ← U_{N_t} between them                */
+  int32_t max_iter;      /* iteration cap per window                                              */
+  int32_t fixed_iters;   /* > 0: run exactly this many iterations per window, no stop test (c5)  */
+  int32_t init;          /* PD_INIT_BROADCAST | PD_INIT_ZERO                                      */
+} pd_problem;
+
+typedef struct pd_handle pd_handle;
+
+typedef struct pd_iter_info {
+  int32_t iters;         /* iterations done in the current window after this call                */
+  int32_t converged;     /* ‖δ‖∞ ≤ tol·‖U‖∞ reached                                               */
+  double  delta_max;     /* ‖δ_k‖∞ (undamped increment)                                           */
+  double  u_max;         /* ‖U^k‖∞ after the update                                               */
+  double  rel;           /* delta_max / u_max                                                     */
+  double  jbar;          /* J̄ = mean(3U²-1) used by the CH preconditioner (0 for linear)          */
+  double  omega;         /* damping factor applied                                                */
+} pd_iter_info;
+
+#define PD_MAX_WINDOWS 64
+typedef struct pd_solve_info {
+  int32_t windows_done;
+  int32_t converged;     /* all windows converged (fixed_iters > 0: always 0)                      */
+  int32_t iters[PD_MAX_WINDOWS];
+  double  last_rel[PD_MAX_WINDOWS];
+  double  seconds;       /* host wall time of the call                                             */
+} pd_solve_info;
+
+/* ABI version (PARADIAG_ABI_VERSION); lets a binding check it loaded the library it expects. */
+PD_API int paradiag_abi_version(void);
+
+/* Name of a return code; never NULL. */
+PD_API const char* paradiag_strerror(int code);
+
+/* Detail message of the last failing call on this host thread ("" if none). */
+PD_API const char* paradiag_last_error(void);
+
+/* Device workspace the handle will allocate for `p` (bytes, excluding the caller's U/r/δ).
+ * Returns PD_EINVAL if the problem is not supported. */
+PD_API int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes);
+
+/* Create a handle on CUDA device `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream).  Validates the problem (PD_EINVAL), checks the shifted systems for
+ * singularity (PD_ESINGULAR), builds the Γ_α / d_l / Λ / twiddle tables and, in 1D, factorises
+ * the N_t/2+1 pentadiagonal matrices d_l I + A (no pivoting).  On success *out owns all workspace. */
+PD_API int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle** out);
+
+/* Residual r = b - K(U) of the all-at-once system (P:127-149 linear; -G(U) of P:460-463 for CH,
+ * mixed form v = U³ - U - ε²Δ_h U, r = Δ_h v - (U_n - U_{n-1})/Δt), with U_0 := u0, stencils in
+ * nested form (R#15).  For CH also reduces J̄ = mean(3U² - 1) into the handle (device-resident),
+ * which the next paradiag_apply_precond_dev-style use (iterate) consumes.  r must not alias U.
+ * If jbar_out != NULL the call synchronises and stores J̄ there (0 for linear kinds). */
+PD_API int paradiag_residual(pd_handle* h, const double* u0, const double* U, double* r, double* jbar_out);
+
+/* δ = P_α⁻¹ r — Steps (1)-(3), P:158-169 / P:491-499.  `jbar` is the scalar Jacobian average used
+ * by CH (ignored otherwise).  r and delta may alias (in-place).  Asynchronous. */
+PD_API int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double jbar);
+
+/* One ParaDiag iteration on window data: r = b - K(U) (or -G(U)), δ = P_α⁻¹ r, U ← U + ω δ, with
+ * ω = 1 (linear) or min(omega, tau/‖δ‖∞) (CH, R#9).  Fills *info (synchronises on 4 scalars).
+ * Returns PD_EDIVERGED if a non-finite value appeared. */
+PD_API int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_info* info);
+
+/* Full solve: for each window, set U⁰ (broadcast or zero), iterate until ‖δ‖∞ ≤ tol‖U‖∞ (or
+ * exactly fixed_iters times), then hand u_{N_t} to the next window.  u0 is not modified;
+ * on return U holds the last window's iterate.  PD_NOT_CONVERGED if a window hit max_iter. */
+PD_API int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* info);
+
+/* As paradiag_solve but with HOST buffers: copies u0_host ([ny][nx]) to the device, solves into
+ * a library-owned U, and copies the final time slice u_{N_t} of the last window to uT_host
+ * ([ny][nx]).  The copies are part of the call (end-to-end path). */
+PD_API int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd_solve_info* info);
+
+/* Number of kernel launches one paradiag_iterate enqueues (for launch accounting). */
+PD_API int paradiag_launches_per_iteration(const pd_handle* h);
+
+/* Per-kernel device time, measured with CUDA events recorded around each launch on the
+ * handle's stream during paradiag_iterate / paradiag_solve (enable with paradiag_profile). */
+typedef struct pd_kernel_time {
+  char    name[32];
+  int32_t launches;
+  double  total_ms;
+} pd_kernel_time;
+
+/* Enable (1) / disable (0) per-kernel event timing and reset the accumulators. */
+PD_API int paradiag_profile(pd_handle* h, int enable);
+
+/* Copy up to max_entries accumulated kernel timings into out; *n_out = entries available. */
+PD_API int paradiag_profile_read(const pd_handle* h, pd_kernel_time* out, int max_entries, int* n_out);
+
+/* Release all device memory of the handle.  NULL is a no-op. */
+PD_API void paradiag_destroy(pd_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARADIAG_H */

@@ -1,0 +1,273 @@
+"""Python binding of libparadiag.so (include/paradiag.h) — argument marshalling only.
+
+Every step of the ParaDiag hot path runs in the sm_100a kernels behind the C ABI; this module
+converts torch CUDA tensors to device pointers and calls the entry points of the same names.
+There is no CPU fallback: if the shared library is missing or the device is not an sm_100a
+B200, calls raise ``ParadiagError``.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libparadiag.so")
+
+PD_OK, PD_NOT_CONVERGED = 0, 1
+PD_EINVAL, PD_ESINGULAR, PD_ECUDA, PD_ENCCL, PD_ENOMEM, PD_EDIVERGED = -1, -2, -3, -4, -5, -6
+KINDS = {"biharmonic": 0, "linear_ch": 1, "cahn_hilliard": 2}
+BCS = {"neumann": 0, "hinged": 1}
+INITS = {"broadcast": 0, "zero": 1}
+MAX_WINDOWS = 64
+
+
+class ParadiagError(RuntimeError):
+    def __init__(self, code, where, detail=""):
+        self.code = code
+        super().__init__(f"{where}: {strerror(code)} ({detail})")
+
+
+class pd_problem(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("bc", ctypes.c_int32), ("dim", ctypes.c_int32),
+                ("nt", ctypes.c_int32), ("m", ctypes.c_int64), ("t_window", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("theta", ctypes.c_double), ("beta", ctypes.c_double),
+                ("eps", ctypes.c_double), ("tol", ctypes.c_double), ("omega", ctypes.c_double),
+                ("tau", ctypes.c_double), ("n_windows", ctypes.c_int32), ("max_iter", ctypes.c_int32),
+                ("fixed_iters", ctypes.c_int32), ("init", ctypes.c_int32)]
+
+
+class pd_iter_info(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("delta_max", ctypes.c_double),
+                ("u_max", ctypes.c_double), ("rel", ctypes.c_double), ("jbar", ctypes.c_double),
+                ("omega", ctypes.c_double)]
+
+
+class pd_solve_info(ctypes.Structure):
+    _fields_ = [("windows_done", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("iters", ctypes.c_int32 * MAX_WINDOWS), ("last_rel", ctypes.c_double * MAX_WINDOWS),
+                ("seconds", ctypes.c_double)]
+
+
+class pd_kernel_time(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int32), ("total_ms", ctypes.c_double)]
+
+
+_lib = None
+EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", "paradiag_strerror", "paradiag_last_error", "paradiag_workspace_bytes",
+           "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_iterate",
+           "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy"]
+
+
+def load(path: str = LIB_PATH):
+    """Load libparadiag.so (built by build.py / __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ParadiagError(PD_ECUDA, "load", f"{path} not built; run python paper_2304_14021_b200/build.py")
+    lib = ctypes.CDLL(path)
+    vp, P = ctypes.c_void_p, ctypes.POINTER
+    lib.paradiag_abi_version.restype = ctypes.c_int
+    lib.paradiag_strerror.restype = ctypes.c_char_p
+    lib.paradiag_strerror.argtypes = [ctypes.c_int]
+    lib.paradiag_last_error.restype = ctypes.c_char_p
+    lib.paradiag_workspace_bytes.argtypes = [P(pd_problem), P(ctypes.c_size_t)]
+    lib.paradiag_init.argtypes = [P(pd_problem), ctypes.c_int, vp, P(vp)]
+    lib.paradiag_residual.argtypes = [vp, vp, vp, vp, P(ctypes.c_double)]
+    lib.paradiag_apply_precond.argtypes = [vp, vp, vp, ctypes.c_double]
+    lib.paradiag_iterate.argtypes = [vp, vp, vp, P(pd_iter_info)]
+    lib.paradiag_solve.argtypes = [vp, vp, vp, P(pd_solve_info)]
+    lib.paradiag_solve_host.argtypes = [vp, vp, vp, P(pd_solve_info)]
+    lib.paradiag_launches_per_iteration.argtypes = [vp]
+    lib.paradiag_profile.argtypes = [vp, ctypes.c_int]
+    lib.paradiag_profile_read.argtypes = [vp, P(pd_kernel_time), ctypes.c_int, P(ctypes.c_int)]
+    lib.paradiag_destroy.argtypes = [vp]
+    lib.paradiag_destroy.restype = None
+    for name in EXPORTS:
+        if name not in ("paradiag_destroy",):
+            getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
+    if lib.paradiag_abi_version() != 1:
+        raise ParadiagError(PD_ECUDA, "load", "ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def strerror(code: int) -> str:
+    try:
+        return load().paradiag_strerror(code).decode()
+    except Exception:  # library missing: still name the code
+        return f"status {code}"
+
+
+def _check(rc, where):
+    if rc < 0:
+        raise ParadiagError(rc, where, load().paradiag_last_error().decode())
+    return rc
+
+
+def make_problem(obj=None, **kw) -> pd_problem:
+    """pd_problem from keyword arguments or from any object carrying the same field names
+    (e.g. workloads.Problem).  kind/bc/init accept the names in KINDS/BCS/INITS."""
+    f = {}
+    if obj is not None:
+        for k in ("kind", "bc", "dim", "nt", "m", "t_window", "alpha", "theta", "beta", "eps", "tol",
+                  "omega", "tau", "n_windows", "max_iter", "fixed_iters", "init"):
+            if hasattr(obj, k):
+                f[k] = getattr(obj, k)
+    f.update(kw)
+    p = pd_problem()
+    p.kind = KINDS[f["kind"]] if isinstance(f["kind"], str) else int(f["kind"])
+    p.bc = BCS[f["bc"]] if isinstance(f["bc"], str) else int(f["bc"])
+    p.dim = int(f["dim"])
+    p.nt = int(f["nt"])
+    p.m = int(f["m"])
+    p.t_window = float(f["t_window"])
+    p.alpha = float(f["alpha"])
+    p.theta = float(f.get("theta", 1.0))
+    p.beta = float(f.get("beta", 0.0))
+    p.eps = float(f.get("eps", 0.0))
+    p.tol = float(f.get("tol", 1e-10))
+    p.omega = float(f.get("omega", 1.0))
+    tau = f.get("tau", float("inf"))
+    p.tau = float(tau) if tau is not None else float("inf")
+    p.n_windows = int(f.get("n_windows", 1))
+    p.max_iter = int(f.get("max_iter", 100))
+    fi = f.get("fixed_iters")
+    p.fixed_iters = int(fi) if fi else 0
+    init = f.get("init", "broadcast")
+    p.init = INITS[init] if isinstance(init, str) else int(init)
+    return p
+
+
+def _ptr(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ParadiagError(PD_EINVAL, name, "expected a contiguous float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------- thin C-ABI mirrors
+def paradiag_workspace_bytes(problem: pd_problem) -> int:
+    b = ctypes.c_size_t(0)
+    _check(load().paradiag_workspace_bytes(ctypes.byref(problem), ctypes.byref(b)), "paradiag_workspace_bytes")
+    return b.value
+
+
+def paradiag_init(problem: pd_problem, device: int = 0, stream=None) -> ctypes.c_void_p:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device).cuda_stream
+    h = ctypes.c_void_p()
+    _check(load().paradiag_init(ctypes.byref(problem), int(device), ctypes.c_void_p(stream), ctypes.byref(h)),
+           "paradiag_init")
+    return h
+
+
+def paradiag_residual(h, u0, U, r, want_jbar=False):
+    j = ctypes.c_double(0.0)
+    _check(load().paradiag_residual(h, _ptr(u0, "u0"), _ptr(U, "U"), _ptr(r, "r"),
+                                    ctypes.byref(j) if want_jbar else None), "paradiag_residual")
+    return j.value
+
+
+def paradiag_apply_precond(h, r, delta, jbar: float = 0.0):
+    _check(load().paradiag_apply_precond(h, _ptr(r, "r"), _ptr(delta, "delta"), float(jbar)),
+           "paradiag_apply_precond")
+
+
+def paradiag_iterate(h, u0, U, info: pd_iter_info = None) -> pd_iter_info:
+    info = info or pd_iter_info()
+    _check(load().paradiag_iterate(h, _ptr(u0, "u0"), _ptr(U, "U"), ctypes.byref(info)), "paradiag_iterate")
+    return info
+
+
+def paradiag_solve(h, u0, U):
+    info = pd_solve_info()
+    rc = _check(load().paradiag_solve(h, _ptr(u0, "u0"), _ptr(U, "U"), ctypes.byref(info)), "paradiag_solve")
+    return rc, info
+
+
+def paradiag_solve_host(h, u0_host: np.ndarray, uT_host: np.ndarray):
+    for a in (u0_host, uT_host):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise ParadiagError(PD_EINVAL, "paradiag_solve_host", "host arrays must be contiguous float64")
+    info = pd_solve_info()
+    rc = _check(load().paradiag_solve_host(h, u0_host.ctypes.data_as(ctypes.c_void_p),
+                                           uT_host.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info)),
+                "paradiag_solve_host")
+    return rc, info
+
+
+def paradiag_launches_per_iteration(h) -> int:
+    return load().paradiag_launches_per_iteration(h)
+
+
+def paradiag_profile(h, enable: bool = True):
+    _check(load().paradiag_profile(h, 1 if enable else 0), "paradiag_profile")
+
+
+def paradiag_profile_read(h) -> dict:
+    """{kernel name: (launches, total_ms)} accumulated since paradiag_profile(h, True)."""
+    n = ctypes.c_int(0)
+    buf = (pd_kernel_time * 32)()
+    _check(load().paradiag_profile_read(h, buf, 32, ctypes.byref(n)), "paradiag_profile_read")
+    return {buf[i].name.decode(): (buf[i].launches, buf[i].total_ms) for i in range(min(n.value, 32))}
+
+
+def paradiag_destroy(h):
+    if h:
+        load().paradiag_destroy(h)
+
+
+class Solver:
+    """Owns a handle; shapes follow the C ABI ([nt][ny][nx] iterates, [ny][nx] u0)."""
+
+    def __init__(self, problem, device: int = 0, stream=None):
+        self.problem = problem if isinstance(problem, pd_problem) else make_problem(problem)
+        self.device = device
+        self.h = paradiag_init(self.problem, device, stream)
+        n = self.problem.m + 1 if self.problem.bc == 0 else self.problem.m - 1
+        self.nx = n
+        self.ny = n if self.problem.dim == 2 else 1
+        self.shape = (self.problem.nt, self.ny, self.nx)
+
+    def empty(self):
+        import torch
+        return torch.empty(self.shape, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def residual(self, u0, U, r, want_jbar=False):
+        return paradiag_residual(self.h, u0, U, r, want_jbar)
+
+    def apply_precond(self, r, delta, jbar=0.0):
+        paradiag_apply_precond(self.h, r, delta, jbar)
+
+    def iterate(self, u0, U, info=None):
+        return paradiag_iterate(self.h, u0, U, info)
+
+    def solve(self, u0, U):
+        return paradiag_solve(self.h, u0, U)
+
+    def solve_host(self, u0_host):
+        uT = np.empty((self.ny, self.nx), dtype=np.float64)
+        rc, info = paradiag_solve_host(self.h, np.ascontiguousarray(u0_host, dtype=np.float64).reshape(self.ny, self.nx), uT)
+        return uT, rc, info
+
+    def profile(self, enable=True):
+        paradiag_profile(self.h, enable)
+
+    def profile_read(self):
+        return paradiag_profile_read(self.h)
+
+    def launches_per_iteration(self):
+        return paradiag_launches_per_iteration(self.h)
+
+    def close(self):
+        if self.h:
+            paradiag_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,62 @@
+// common.cuh — complex helpers, reductions and small utilities shared by the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PD_DEV __device__ __forceinline__
+
+namespace pd {
+
+PD_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+PD_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+PD_DEV double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+PD_DEV double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+PD_DEV double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// 1 / z
+PD_DEV double2 cinv(double2 z) {
+  const double q = 1.0 / (z.x * z.x + z.y * z.y);
+  return make_double2(z.x * q, -z.y * q);
+}
+
+// Device-resident per-iteration scalars.  |x| of a finite double orders like its bit pattern, so a
+// max-abs reduction is an integer atomicMax on the bits (deterministic; NaN sorts above +inf).
+struct DevStats {
+  unsigned long long dmax_bits;   // ‖δ‖∞ of the last preconditioner application
+  unsigned long long umax_bits;   // ‖U‖∞ after the update
+  double jbar;                    // J̄ = mean(3U² - 1) (CH)
+  double omega;                   // damping applied by the update
+};
+
+PD_DEV unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+PD_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide max of |v| folded into *dst with one atomic per warp.
+PD_DEV void warp_atomic_max_abs(unsigned long long* dst, double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+  b = warp_max_u64(b);
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(dst, b);
+}
+
+PD_DEV int bitrev(int v, int bits) { return bits ? (int)(__brev((unsigned)v) >> (32 - bits)) : 0; }
+
+// SMEM index padding: one 16-byte slot per 16 complex values keeps strided radix passes
+// conflict-free (stride-16 lanes land on consecutive 16-byte bank groups).
+PD_DEV int pad16(int p) { return p + (p >> 4); }
+__host__ __device__ constexpr int padded16(int n) { return n + (n >> 4) + 1; }
+
+}  // namespace pd

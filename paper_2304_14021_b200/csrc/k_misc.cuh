@@ -1,0 +1,53 @@
+// k_misc.cuh — defect-correction update U ← U + ω δ (R#9 damping), initial iterates, scalars.
+#pragma once
+#include "common.cuh"
+
+namespace pd {
+
+PD_DEV double stats_omega(const DevStats* st, int damped, double omega_cap, double tau) {
+  if (!damped) return 1.0;
+  const double dmax = __longlong_as_double((long long)st->dmax_bits);
+  return dmax > 0.0 ? fmin(omega_cap, tau / dmax) : omega_cap;
+}
+
+// U += ω δ over n doubles; ‖U‖∞ reduced into st->umax_bits.  Vectorised by double2 when aligned.
+__global__ void __launch_bounds__(256)
+k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, DevStats* st,
+         int damped, double omega_cap, double tau) {
+  const double w = stats_omega(st, damped, omega_cap, tau);
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->omega = w;
+  double lmax = 0.0;
+  const size_t n2 = n / 2;
+  double2* U2 = reinterpret_cast<double2*>(U);
+  const double2* D2 = reinterpret_cast<const double2*>(delta);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+    double2 u = U2[i];
+    const double2 d = __ldg(D2 + i);
+    u.x += w * d.x;
+    u.y += w * d.y;
+    U2[i] = u;
+    lmax = fmax(lmax, fmax(fabs(u.x), fabs(u.y)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double u = U[n - 1] + w * delta[n - 1];
+    U[n - 1] = u;
+    lmax = fmax(lmax, fabs(u));
+  }
+  warp_atomic_max_abs(&st->umax_bits, lmax);
+}
+
+// U⁰: broadcast u0 to every time slice, or zero (R#5).
+__global__ void k_init_iterate(double* __restrict__ U, const double* __restrict__ u0, size_t ns,
+                               size_t total, int zero) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+    U[i] = zero ? 0.0 : __ldg(u0 + i % ns);
+}
+
+__global__ void k_reset_stats(DevStats* st) {
+  st->dmax_bits = 0ull;
+  st->umax_bits = 0ull;
+}
+
+__global__ void k_set_jbar(DevStats* st, double jbar) { st->jbar = jbar; }
+
+}  // namespace pd

@@ -1,0 +1,674 @@
+// paradiag.cu — C ABI (include/paradiag.h) and the single-GPU iteration engine.
+//
+// One ParaDiag iteration = residual (P:127-149 / P:452-463) → P_α⁻¹ (P:158-169 / P:491-499) →
+// update U ← U + ω δ.  2D pass order (spatial-first):
+//   x-DTT (r → δ) · y-DTT · fused time pass (Γ_α·DFT · per-mode divide · IDFT·Γ_α⁻¹) · y-DTT · x-DTT
+// 1D: time DFT → batched pentadiagonal solves per bin → inverse time DFT.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/paradiag.h"
+#include "common.cuh"
+#include "fft.cuh"
+#include "k_misc.cuh"
+#include "k_penta.cuh"
+#include "k_residual.cuh"
+#include "k_spatial.cuh"
+#include "k_time.cuh"
+
+using namespace pd;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define PD_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? PD_ENOMEM : PD_ECUDA,               \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+#define PD_LAUNCHED()                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(PD_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));   \
+  } while (0)
+
+enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
+                K_TFWD1D, K_PENTA, K_TINV1D, PD_NKERNELS };
+const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
+                                         "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
+                                         "time_fwd_1d", "penta_solve", "time_inv_1d"};
+
+constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
+constexpr int kTime1DWarps = 4;
+constexpr int kLineWarps = 4;   // spatial DTT: lines per CTA
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+int ilog2(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+}  // namespace
+
+struct pd_handle {
+  pd_problem P{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nx = 0, ny = 0;
+  int64_t ns = 0, total = 0;
+  int log2nt = 0, log2h = 0, twlog = 0, nb = 0;
+  bool neumann = true;
+  double inv_dt = 0, inv_h2 = 0, b2 = 0, e2 = 0;
+  // device buffers
+  double* work = nullptr;             // 2D: δ/r workspace [nt][ns]; 1D: r [nt][nx]
+  double2* spec = nullptr;            // 1D spectra [nx][nb] and scratch
+  double2* w1 = nullptr;
+  double2* w2 = nullptr;
+  double* gam = nullptr;
+  double* ginv = nullptr;
+  double2* dl = nullptr;
+  double* lam = nullptr;
+  double2* tw = nullptr;
+  double2* trig = nullptr;
+  double* band = nullptr;
+  double2* fac = nullptr;             // 4 x [nx][nb]
+  DevStats* st = nullptr;
+  DevStats* st_host = nullptr;        // pinned
+  double* jpart = nullptr;
+  size_t njpart = 0;
+  double* u0buf = nullptr;
+  double* Uint = nullptr;             // solve_host's iterate
+  std::vector<void*> allocs;
+  // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
+  bool prof = false;
+  cudaEvent_t ev[PD_NKERNELS][2] = {};
+  bool ev_used[PD_NKERNELS] = {};
+  double prof_ms[PD_NKERNELS] = {};
+  int prof_n[PD_NKERNELS] = {};
+};
+
+namespace {
+
+void prof_begin(pd_handle* h, int id) {
+  if (!h->prof) return;
+  if (!h->ev[id][0]) {
+    cudaEventCreate(&h->ev[id][0]);
+    cudaEventCreate(&h->ev[id][1]);
+  }
+  cudaEventRecord(h->ev[id][0], h->stream);
+}
+void prof_end(pd_handle* h, int id) {
+  if (!h->prof) return;
+  cudaEventRecord(h->ev[id][1], h->stream);
+  h->ev_used[id] = true;
+}
+// after a stream sync: fold this iteration's event pairs into the accumulators
+void prof_collect(pd_handle* h) {
+  if (!h->prof) return;
+  for (int i = 0; i < PD_NKERNELS; ++i)
+    if (h->ev_used[i]) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, h->ev[i][0], h->ev[i][1]) == cudaSuccess) {
+        h->prof_ms[i] += ms;
+        h->prof_n[i] += 1;
+      }
+      h->ev_used[i] = false;
+    }
+}
+
+template <typename T>
+int dalloc(pd_handle* h, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+  if (e != cudaSuccess)
+    return fail(PD_ENOMEM, std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + "): " + cudaGetErrorString(e));
+  h->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return PD_OK;
+}
+
+int validate(const pd_problem* p) {
+  if (!p) return fail(PD_EINVAL, "problem is NULL");
+  if (p->kind < 0 || p->kind > 2) return fail(PD_EINVAL, "unknown kind");
+  if (p->bc < 0 || p->bc > 1) return fail(PD_EINVAL, "unknown bc");
+  if (p->dim != 1 && p->dim != 2) return fail(PD_EINVAL, "dim must be 1 or 2");
+  if (p->kind == PD_CAHN_HILLIARD && (p->dim != 2 || p->bc != PD_BC_NEUMANN))
+    return fail(PD_EINVAL, "Cahn-Hilliard is supported in 2D with Neumann BCs (P:59)");
+  if (!is_pow2(p->nt) || p->nt < 2 || p->nt > 4096) return fail(PD_EINVAL, "nt must be a power of two in [2, 4096]");
+  if (p->dim == 2 && (!is_pow2(p->m) || p->m < 4 || p->m > 4096))
+    return fail(PD_EINVAL, "2D: m (intervals per axis) must be a power of two in [4, 4096]");
+  if (p->dim == 1 && (p->m < 4 || p->m > (1 << 20))) return fail(PD_EINVAL, "1D: m must be in [4, 2^20]");
+  if (!(p->alpha > 0.0 && p->alpha < 1.0)) return fail(PD_EINVAL, "alpha must be in (0, 1) (P:308)");
+  if (p->theta != 1.0) return fail(PD_EINVAL, "theta = 1 (backward Euler) only");
+  if (!(p->t_window > 0.0) || !std::isfinite(p->t_window)) return fail(PD_EINVAL, "t_window must be > 0");
+  if (!(p->eps >= 0.0)) return fail(PD_EINVAL, "eps must be >= 0");
+  if (p->fixed_iters <= 0 && !(p->tol > 0.0)) return fail(PD_EINVAL, "tol must be > 0");
+  if (p->n_windows < 1 || p->n_windows > PD_MAX_WINDOWS) return fail(PD_EINVAL, "n_windows out of range");
+  if (p->fixed_iters <= 0 && p->max_iter < 1) return fail(PD_EINVAL, "max_iter must be >= 1");
+  if (p->kind == PD_CAHN_HILLIARD && !(p->omega > 0.0 && p->tau > 0.0))
+    return fail(PD_EINVAL, "CH damping needs omega > 0 and tau > 0");
+  if (p->init != PD_INIT_BROADCAST && p->init != PD_INIT_ZERO) return fail(PD_EINVAL, "unknown init");
+  return PD_OK;
+}
+
+void geometry(const pd_problem* p, int* nx, int* ny) {
+  const int64_t n = p->bc == PD_BC_NEUMANN ? p->m + 1 : p->m - 1;
+  *nx = (int)n;
+  *ny = p->dim == 2 ? (int)n : 1;
+}
+
+double mu_of(const pd_problem* p, double Lam, double b2, double e2) {
+  if (p->kind == PD_BIHARMONIC) return Lam * Lam;
+  return b2 * Lam + e2 * (Lam * Lam);
+}
+
+template <typename K>
+int allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) PD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return PD_OK;
+}
+
+size_t time_smem(int nt, int warps) { return (size_t)warps * padded16(nt) * sizeof(double2); }
+size_t line_smem(int h) { return (size_t)kLineWarps * padded16(h) * sizeof(double2); }
+
+// ----------------------------------------------------------------------------- launches
+int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) {
+  ResidualParams R;
+  R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
+  R.neumann = h->neumann; R.kind = h->P.kind;
+  R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
+  dim3 blk = h->P.dim == 2 ? dim3(32, 8) : dim3(256, 1);
+  dim3 grd((h->nx + blk.x - 1) / blk.x, (h->ny + blk.y - 1) / blk.y, h->P.nt);
+  prof_begin(h, K_RESIDUAL);
+  k_residual<<<grd, blk, 0, h->stream>>>(u0, U, r, R, h->jpart);
+  prof_end(h, K_RESIDUAL);
+  PD_LAUNCHED();
+  if (h->P.kind == PD_CAHN_HILLIARD) {
+    prof_begin(h, K_JBAR);
+    k_jbar_finalize<<<1, 1024, 0, h->stream>>>(h->jpart, h->njpart, 1.0 / (double)h->total, h->st);
+    prof_end(h, K_JBAR);
+    PD_LAUNCHED();
+  }
+  return PD_OK;
+}
+
+LineParams line_params(pd_handle* h, int axis, unsigned long long* amax) {
+  LineParams L;
+  const int64_t nt = h->P.nt;
+  if (axis == 0) {      // rows: contiguous lines
+    L.nlines = nt * h->ny; L.A = 1; L.B = h->nx; L.C = 0; L.es = 1;
+  } else {              // columns: stride nx
+    L.nlines = nt * h->nx; L.A = h->nx; L.B = h->ns; L.C = 1; L.es = h->nx;
+  }
+  L.M = (int)h->P.m; L.log2h = h->log2h; L.trig = h->trig; L.tw = h->tw; L.twlog = h->twlog;
+  L.amax = amax;
+  return L;
+}
+
+int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid) {
+  LineParams L = line_params(h, axis, amax);
+  const unsigned grid = (unsigned)((L.nlines + kLineWarps - 1) / kLineWarps);
+  const size_t smem = line_smem(1 << h->log2h);
+  prof_begin(h, kid);
+  if (h->neumann) k_dtt_lines<1, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
+  else k_dtt_lines<0, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
+  prof_end(h, kid);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+TimeParams time_params(pd_handle* h, unsigned long long* amax) {
+  TimeParams T;
+  T.nt = h->P.nt; T.log2nt = h->log2nt; T.ns = h->ns; T.nx = h->nx;
+  T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.lamx = h->lam;
+  T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
+  T.tw = h->tw; T.twlog = h->twlog; T.amax = amax;
+  return T;
+}
+
+int precond(pd_handle* h, const double* r, double* delta) {
+  unsigned long long* dmax = &h->st->dmax_bits;
+  if (h->P.dim == 2) {
+    int rc;
+    if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
+    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD))) return rc;
+    TimeParams T = time_params(h, nullptr);
+    const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
+    prof_begin(h, K_TIME);
+    k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
+    prof_end(h, K_TIME);
+    PD_LAUNCHED();
+    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV))) return rc;
+    if ((rc = launch_lines(h, delta, delta, 0, dmax, K_XINV))) return rc;
+    return PD_OK;
+  }
+  TimeParams T = time_params(h, nullptr);
+  const unsigned grid = (unsigned)((h->ns + 2 * kTime1DWarps - 1) / (2 * kTime1DWarps));
+  const size_t smem = time_smem(h->P.nt, kTime1DWarps);
+  prof_begin(h, K_TFWD1D);
+  k_time_fwd_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(r, h->spec, T);
+  prof_end(h, K_TFWD1D);
+  PD_LAUNCHED();
+  PentaParams PP;
+  PP.n = h->nx; PP.nb = h->nb; PP.neumann = h->neumann; PP.kind = h->P.kind;
+  PP.inv_h2 = h->inv_h2; PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl;
+  const size_t nf = (size_t)h->nx * h->nb;
+  PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
+  prof_begin(h, K_PENTA);
+  k_penta_solve<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(h->spec, h->w1, h->w2, PP);
+  prof_end(h, K_PENTA);
+  PD_LAUNCHED();
+  T.amax = dmax;
+  prof_begin(h, K_TINV1D);
+  k_time_inv_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(h->spec, delta, T);
+  prof_end(h, K_TINV1D);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int launch_update(pd_handle* h, double* U, const double* delta) {
+  const int damped = h->P.kind == PD_CAHN_HILLIARD;
+  prof_begin(h, K_UPDATE);
+  k_update<<<148 * 8, 256, 0, h->stream>>>(U, delta, (size_t)h->total, h->st, damped, h->P.omega, h->P.tau);
+  prof_end(h, K_UPDATE);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int init_iterate(pd_handle* h, double* U, const double* u0) {
+  k_init_iterate<<<148 * 8, 256, 0, h->stream>>>(U, u0, (size_t)h->ns, (size_t)h->total,
+                                                  h->P.init == PD_INIT_ZERO);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
+  int rc;
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  if ((rc = launch_residual(h, u0, U, h->work))) return rc;
+  if ((rc = precond(h, h->work, h->work))) return rc;
+  if ((rc = launch_update(h, U, h->work))) return rc;
+  PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  double dmax, umax;
+  std::memcpy(&dmax, &h->st_host->dmax_bits, sizeof(double));
+  std::memcpy(&umax, &h->st_host->umax_bits, sizeof(double));
+  info->delta_max = dmax;
+  info->u_max = umax;
+  info->rel = umax > 0 ? dmax / umax : 0.0;
+  info->jbar = h->P.kind == PD_CAHN_HILLIARD ? h->st_host->jbar : 0.0;
+  info->omega = h->st_host->omega;
+  if (!std::isfinite(dmax) || !std::isfinite(umax)) return fail(PD_EDIVERGED, "non-finite increment or iterate");
+  return PD_OK;
+}
+
+int check_handle(pd_handle* h) {
+  if (!h) return fail(PD_EINVAL, "handle is NULL");
+  PD_CUDA(cudaSetDevice(h->device));
+  return PD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int paradiag_abi_version(void) { return PARADIAG_ABI_VERSION; }
+
+const char* paradiag_strerror(int code) {
+  switch (code) {
+    case PD_OK: return "PD_OK";
+    case PD_NOT_CONVERGED: return "PD_NOT_CONVERGED";
+    case PD_EINVAL: return "PD_EINVAL: invalid problem or argument";
+    case PD_ESINGULAR: return "PD_ESINGULAR: singular shifted system";
+    case PD_ECUDA: return "PD_ECUDA: CUDA failure";
+    case PD_ENCCL: return "PD_ENCCL: communicator failure";
+    case PD_ENOMEM: return "PD_ENOMEM: device allocation failed";
+    case PD_EDIVERGED: return "PD_EDIVERGED: non-finite values";
+    default: return "unknown paradiag status";
+  }
+}
+
+const char* paradiag_last_error(void) { return g_last_error.c_str(); }
+
+int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!bytes) return fail(PD_EINVAL, "bytes is NULL");
+  int nx, ny;
+  geometry(p, &nx, &ny);
+  const size_t ns = (size_t)nx * ny, total = ns * p->nt, nb = p->nt / 2 + 1;
+  size_t b = total * sizeof(double) + ns * sizeof(double);
+  if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
+  b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
+  b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
+  *bytes = b;
+  return PD_OK;
+}
+
+int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle** out) {
+  if (!out) return fail(PD_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = validate(p);
+  if (rc) return rc;
+  int ndev = 0;
+  PD_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(PD_ECUDA, "no such CUDA device");
+  PD_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  PD_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(PD_ECUDA, "libparadiag is built for sm_100a (B200); device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+
+  pd_handle* h = new (std::nothrow) pd_handle();
+  if (!h) return fail(PD_ENOMEM, "host allocation");
+  h->P = *p;
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  geometry(p, &h->nx, &h->ny);
+  h->ns = (int64_t)h->nx * h->ny;
+  h->total = h->ns * p->nt;
+  h->neumann = p->bc == PD_BC_NEUMANN;
+  h->log2nt = ilog2(p->nt);
+  h->nb = p->nt / 2 + 1;
+  h->inv_dt = (double)p->nt / p->t_window;                  // R#20
+  h->inv_h2 = (double)p->m * (double)p->m;
+  h->b2 = p->beta * p->beta;
+  h->e2 = p->eps * p->eps;
+  const int M = (int)p->m;
+  h->log2h = p->dim == 2 ? ilog2(M) - 1 : 0;
+  h->twlog = std::max(h->log2nt, h->log2h);
+
+  auto cleanup = [&](int code) {
+    paradiag_destroy(h);
+    return code;
+  };
+#define PD_TRY(x) do { int rc_ = (x); if (rc_) return cleanup(rc_); } while (0)
+
+  // ---- host tables (closed forms P:156; readings R#1, R#2, R#11)
+  const int nt = p->nt;
+  std::vector<double> gam(nt), ginv(nt), lam(h->nx);
+  std::vector<double2> dl(nt), tw(size_t(1) << h->twlog), trig(M + 1);
+  const double lna = std::log(p->alpha);
+  const double z = std::exp(lna / nt);
+  const double spatial_scale = p->dim == 2 ? 1.0 / ((2.0 * M) * (2.0 * M)) : 1.0;
+  for (int j = 0; j < nt; ++j) {
+    gam[j] = std::exp(j * lna / nt);
+    ginv[j] = std::exp(-j * lna / nt) * (spatial_scale / nt);
+  }
+  for (int l = 0; l < nt; ++l) {
+    const double ang = 2.0 * M_PI * l / nt;
+    dl[l] = make_double2((1.0 - z * std::cos(ang)) * h->inv_dt, (z * std::sin(ang)) * h->inv_dt);
+  }
+  for (int i = 0; i < h->nx; ++i) {
+    const int pidx = h->neumann ? i : i + 1;
+    const double s = std::sin(pidx * M_PI / (2.0 * M));
+    lam[i] = -4.0 * h->inv_h2 * s * s;
+  }
+  const size_t TWN = size_t(1) << h->twlog;
+  for (size_t k = 0; k < TWN; ++k) {
+    const double ang = 2.0 * M_PI * (double)k / (double)TWN;
+    tw[k] = make_double2(std::cos(ang), -std::sin(ang));
+  }
+  for (int j = 0; j <= M; ++j) trig[j] = make_double2(std::cos(M_PI * j / M), std::sin(M_PI * j / M));
+
+  // ---- singularity check of d_l + μ (linear kinds): only l = 0 and N_t/2 have real d_l
+  if (p->kind != PD_CAHN_HILLIARD) {
+    double worst = INFINITY;
+    for (int l : {0, nt / 2}) {
+      for (int i = 0; i < h->nx; ++i)
+        for (int j = 0; j < (p->dim == 2 ? h->ny : 1); ++j) {
+          const double Lam = lam[i] + (p->dim == 2 ? lam[j] : 0.0);
+          const double mu = mu_of(p, Lam, h->b2, h->e2);
+          const double den = std::hypot(dl[l].x + mu, dl[l].y) / (std::fabs(dl[l].x) + std::fabs(mu) + 1e-300);
+          worst = std::min(worst, den);
+        }
+    }
+    if (!(worst > 1e-13)) {
+      delete h;
+      return fail(PD_ESINGULAR, "shifted system d_l + mu numerically singular (relative " + std::to_string(worst) + ")");
+    }
+  }
+
+  // ---- device buffers
+  PD_TRY(dalloc(h, &h->work, (size_t)h->total));
+  PD_TRY(dalloc(h, &h->u0buf, (size_t)h->ns));
+  PD_TRY(dalloc(h, &h->gam, nt));
+  PD_TRY(dalloc(h, &h->ginv, nt));
+  PD_TRY(dalloc(h, &h->dl, nt));
+  PD_TRY(dalloc(h, &h->lam, h->nx));
+  PD_TRY(dalloc(h, &h->tw, TWN));
+  PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
+  PD_TRY(dalloc(h, &h->st, 1));
+  {
+    cudaError_t e = cudaMallocHost(&h->st_host, sizeof(DevStats));
+    if (e != cudaSuccess) return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
+  }
+  if (p->kind == PD_CAHN_HILLIARD) {
+    const size_t gx = (h->nx + 31) / 32, gy = (h->ny + 7) / 8;
+    h->njpart = gx * gy * nt;
+    PD_TRY(dalloc(h, &h->jpart, h->njpart));
+  }
+  auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
+  if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
+      up(h->dl, dl.data(), nt * sizeof(double2)) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
+      up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)))
+    return cleanup(fail(PD_ECUDA, "table upload failed"));
+
+  if (p->dim == 1) {
+    const size_t nf = (size_t)h->nx * h->nb;
+    PD_TRY(dalloc(h, &h->spec, nf));
+    PD_TRY(dalloc(h, &h->w1, nf));
+    PD_TRY(dalloc(h, &h->w2, nf));
+    PD_TRY(dalloc(h, &h->fac, 4 * nf));
+    PD_TRY(dalloc(h, &h->band, 5 * (size_t)h->nx));
+    // assembled A = β²D + ε²D² or D² with D = m²·T, T the integer tridiagonal of P:109-118
+    const int n = h->nx;
+    auto Tij = [&](int i, int j) -> double {
+      if (j < 0 || j >= n) return 0.0;
+      if (i == j) return -2.0;
+      if (std::abs(i - j) != 1) return 0.0;
+      if (h->neumann && i == 0 && j == 1) return 2.0;
+      if (h->neumann && i == n - 1 && j == n - 2) return 2.0;
+      return 1.0;
+    };
+    std::vector<double> band(5 * (size_t)n);
+    const double m2 = h->inv_h2, m4 = m2 * m2;
+    for (int i = 0; i < n; ++i)
+      for (int k = -2; k <= 2; ++k) {
+        const int j = i + k;
+        double t2 = 0.0;
+        for (int q = i - 1; q <= i + 1; ++q)
+          if (q >= 0 && q < n) t2 += Tij(i, q) * Tij(q, j);
+        const double t1 = Tij(i, j);
+        const double a = p->kind == PD_BIHARMONIC ? m4 * t2 : h->b2 * m2 * t1 + h->e2 * m4 * t2;
+        band[(size_t)(k + 2) * n + i] = (j >= 0 && j < n) ? a : 0.0;
+      }
+    if (up(h->band, band.data(), band.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "band upload"));
+    PentaParams PP;
+    PP.n = n; PP.nb = h->nb; PP.neumann = h->neumann; PP.kind = p->kind; PP.inv_h2 = h->inv_h2;
+    PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl;
+    PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
+    k_penta_factor<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(PP);
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(PD_ECUDA, "penta factor launch"));
+    PD_TRY(allow_smem(k_time_fwd_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
+    PD_TRY(allow_smem(k_time_inv_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
+  } else {
+    PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
+    PD_TRY(allow_smem(k_dtt_lines<1, kLineWarps>, line_smem(1 << h->log2h)));
+    PD_TRY(allow_smem(k_dtt_lines<0, kLineWarps>, line_smem(1 << h->log2h)));
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
+#undef PD_TRY
+  *out = h;
+  return PD_OK;
+}
+
+int paradiag_residual(pd_handle* h, const double* u0, const double* U, double* r, double* jbar_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!u0 || !U || !r) return fail(PD_EINVAL, "NULL buffer");
+  if (r == U) return fail(PD_EINVAL, "r must not alias U");
+  if ((rc = launch_residual(h, u0, U, r))) return rc;
+  if (jbar_out) {
+    PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
+    PD_CUDA(cudaStreamSynchronize(h->stream));
+    *jbar_out = h->P.kind == PD_CAHN_HILLIARD ? h->st_host->jbar : 0.0;
+  }
+  return PD_OK;
+}
+
+int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double jbar) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!r || !delta) return fail(PD_EINVAL, "NULL buffer");
+  if (h->P.kind == PD_CAHN_HILLIARD) {
+    k_set_jbar<<<1, 1, 0, h->stream>>>(h->st, jbar);
+    PD_LAUNCHED();
+  }
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  return precond(h, r, delta);
+}
+
+int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!u0 || !U || !info) return fail(PD_EINVAL, "NULL argument");
+  if (reinterpret_cast<uintptr_t>(U) % 16) return fail(PD_EINVAL, "U must be 16-byte aligned");
+  pd_iter_info tmp = *info;
+  rc = iteration(h, u0, U, &tmp);
+  tmp.iters = info->iters + 1;
+  tmp.converged = (h->P.fixed_iters <= 0) && tmp.delta_max <= h->P.tol * tmp.u_max;
+  *info = tmp;
+  return rc;
+}
+
+int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* info) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!u0 || !U || !info) return fail(PD_EINVAL, "NULL argument");
+  if (reinterpret_cast<uintptr_t>(U) % 16) return fail(PD_EINVAL, "U must be 16-byte aligned");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::memset(info, 0, sizeof(*info));
+  const double* cur_u0 = u0;
+  int status = PD_OK;
+  bool all_conv = true;
+  for (int w = 0; w < h->P.n_windows; ++w) {
+    if ((rc = init_iterate(h, U, cur_u0))) return rc;
+    const int kmax = h->P.fixed_iters > 0 ? h->P.fixed_iters : h->P.max_iter;
+    bool conv = false;
+    int k = 0;
+    pd_iter_info it{};
+    for (k = 1; k <= kmax; ++k) {
+      if ((rc = iteration(h, cur_u0, U, &it))) {
+        info->iters[w] = k;
+        info->windows_done = w;
+        return rc;
+      }
+      if (h->P.fixed_iters <= 0 && it.delta_max <= h->P.tol * it.u_max) {
+        conv = true;
+        break;
+      }
+    }
+    info->iters[w] = std::min(k, kmax);
+    info->last_rel[w] = it.rel;
+    info->windows_done = w + 1;
+    all_conv = all_conv && conv;
+    if (!conv && h->P.fixed_iters <= 0) status = PD_NOT_CONVERGED;
+    if (w + 1 < h->P.n_windows) {      // hand-off: u0 ← U_{N_t}
+      PD_CUDA(cudaMemcpyAsync(h->u0buf, U + (size_t)(h->P.nt - 1) * h->ns, h->ns * sizeof(double),
+                              cudaMemcpyDeviceToDevice, h->stream));
+      cur_u0 = h->u0buf;
+    }
+  }
+  info->converged = h->P.fixed_iters > 0 ? 0 : (all_conv ? 1 : 0);
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return status;
+}
+
+int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd_solve_info* info) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!u0_host || !uT_host || !info) return fail(PD_EINVAL, "NULL argument");
+  if (!h->Uint && (rc = dalloc(h, &h->Uint, (size_t)h->total))) return rc;
+  // window 1's u0 is staged in the hand-off buffer; it is only overwritten after window 1 ends
+  double* d_u0 = h->u0buf;
+  PD_CUDA(cudaMemcpyAsync(d_u0, u0_host, h->ns * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  rc = paradiag_solve(h, d_u0, h->Uint, info);
+  if (rc < 0) return rc;
+  PD_CUDA(cudaMemcpyAsync(uT_host, h->Uint + (size_t)(h->P.nt - 1) * h->ns, h->ns * sizeof(double),
+                          cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  return rc;
+}
+
+int paradiag_launches_per_iteration(const pd_handle* h) {
+  if (!h) return 0;
+  int n = 1 /*reset*/ + 1 /*residual*/ + 1 /*update*/;
+  n += h->P.dim == 2 ? 5 : 3;
+  if (h->P.kind == PD_CAHN_HILLIARD) n += 1;
+  return n;
+}
+
+int paradiag_profile(pd_handle* h, int enable) {
+  if (!h) return fail(PD_EINVAL, "handle is NULL");
+  h->prof = enable != 0;
+  for (int i = 0; i < PD_NKERNELS; ++i) {
+    h->prof_ms[i] = 0.0;
+    h->prof_n[i] = 0;
+    h->ev_used[i] = false;
+  }
+  return PD_OK;
+}
+
+int paradiag_profile_read(const pd_handle* h, pd_kernel_time* out, int max_entries, int* n_out) {
+  if (!h || !n_out) return fail(PD_EINVAL, "NULL argument");
+  int n = 0;
+  for (int i = 0; i < PD_NKERNELS; ++i) {
+    if (!h->prof_n[i]) continue;
+    if (out && n < max_entries) {
+      std::memset(&out[n], 0, sizeof(pd_kernel_time));
+      std::strncpy(out[n].name, kKernelNames[i], sizeof(out[n].name) - 1);
+      out[n].launches = h->prof_n[i];
+      out[n].total_ms = h->prof_ms[i];
+    }
+    ++n;
+  }
+  *n_out = n;
+  return PD_OK;
+}
+
+void paradiag_destroy(pd_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (int i = 0; i < PD_NKERNELS; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (h->ev[i][j]) cudaEventDestroy(h->ev[i][j]);
+  for (void* q : h->allocs) cudaFree(q);
+  if (h->st_host) cudaFreeHost(h->st_host);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+"""C-ABI library: loads, exports every symbol include/paradiag.h declares, validates problems
+on the host.  No compute calls (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2304_14021_b200 as pd
+from workloads import config, CONFIGS
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "paradiag.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2304_14021_b200 import build
+    build.build()
+    return pd.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    decl = set(re.findall(r"\b(paradiag_\w+)\s*\(", open(HDR).read()))
+    assert len(decl) >= 12
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(pd.EXPORTS) == decl
+
+
+def test_abi_version_and_strerror(lib):
+    assert lib.paradiag_abi_version() == 1
+    assert pd.strerror(pd.PD_EINVAL).startswith("PD_EINVAL")
+    assert pd.strerror(pd.PD_ESINGULAR).startswith("PD_ESINGULAR")
+
+
+def test_struct_layout_matches_header():
+    # pd_problem: 4 int32, int64, 8 doubles, 4 int32 -> 104 bytes with natural alignment
+    assert ctypes.sizeof(pd.pd_problem) == 104
+    assert ctypes.sizeof(pd.pd_iter_info) == 48
+    assert ctypes.sizeof(pd.pd_solve_info) == 8 + 64 * 4 + 64 * 8 + 8
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_workspace_bytes_all_configs(lib, name):
+    b = pd.paradiag_workspace_bytes(pd.make_problem(config(name)))
+    p = config(name)
+    assert b >= p.dofs * 8
+
+
+@pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=100), dict(nt=1),
+                                 dict(theta=0.5), dict(m=100), dict(eps=-1.0), dict(t_window=0.0),
+                                 dict(kind="cahn_hilliard"), dict(n_windows=0), dict(tol=0.0)])
+def test_invalid_problems_rejected(lib, bad):
+    p = pd.make_problem(config("c3"), **bad)
+    with pytest.raises(pd.ParadiagError) as e:
+        pd.paradiag_workspace_bytes(p)
+    assert e.value.code == pd.PD_EINVAL
+
+
+def test_ch_requires_2d_neumann(lib):
+    p = pd.make_problem(config("c4"), dim=1)
+    with pytest.raises(pd.ParadiagError):
+        pd.paradiag_workspace_bytes(p)
+
+
+def test_init_without_device_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    rc = lib.paradiag_init(ctypes.byref(pd.make_problem(config("c1"))), 0, None, ctypes.byref(h))
+    assert rc == pd.PD_ECUDA and not h.value

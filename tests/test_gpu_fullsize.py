@@ -1,0 +1,76 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+c3/c4: iteration counts and sampled iterate values vs oracle golden files written by
+tools/make_golden.py (oracle only).  c3/c5: sampled values of the K-th iterate vs the closed-form
+per-mode WR iterate (oracle/modespace.py), computed here on the host.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from _helpers import to_dev
+from oracle import modespace, diagnostics
+from workloads import config, make_u0
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _samples(U, pts):
+    import torch
+    idx = torch.tensor([[n, iy, ix] for n, iy, ix in pts], device=U.device)
+    return U[idx[:, 0], idx[:, 1], idx[:, 2]].cpu().numpy()
+
+
+def test_c3_full(cuda_lib):
+    p = config("c3")
+    g = json.load(open(os.path.join(GOLD, "c3_full.json")))
+    u0 = make_u0(p)
+    s = cuda_lib.Solver(p)
+    U = s.empty()
+    rc, info = s.solve(to_dev(u0), U)
+    assert rc == 0 and info.iters[0] == g["windows"][0]["iters"] == 3
+    w = g["windows"][0]
+    pts = [tuple(x) for x in w["points"]]
+    umax = float(U.abs().max())
+    got = _samples(U, pts)
+    assert np.abs(got - np.array(w["values"])).max() <= 1e-10 * umax
+    gm, c0 = modespace.mode_iterates(p, u0, info.iters[0])
+    assert np.abs(got - modespace.sample(p, gm, c0, pts)).max() <= 1e-10 * umax
+
+
+def test_c4_full(cuda_lib):
+    p = config("c4")
+    g = json.load(open(os.path.join(GOLD, "c4_full.json")))
+    u0 = make_u0(p)
+    s = cuda_lib.Solver(p)
+    U = s.empty()
+    rc, info = s.solve(to_dev(u0), U)
+    assert rc == 0
+    assert list(info.iters[:p.n_windows]) == [w["iters"] for w in g["windows"]]
+    w = g["windows"][-1]
+    pts = [tuple(x) for x in w["points"]]
+    got = _samples(U, pts)
+    assert np.abs(got - np.array(w["values"])).max() <= 1e-8 * float(U.abs().max())
+    last = U[-1].cpu().numpy()
+    assert abs(diagnostics.mass(p, last) - g["mass_u0"]) <= 1e-12
+    assert abs(diagnostics.energy(p, last) - w["energy_end"]) <= 1e-8 * abs(w["energy_end"])
+
+
+def test_c5_full_fixed_K(cuda_lib):
+    p = config("c5")
+    u0 = make_u0(p)
+    s = cuda_lib.Solver(p)
+    U = s.empty()
+    rc, info = s.solve(to_dev(u0), U)
+    assert info.iters[0] == 3
+    rng = np.random.default_rng(55)
+    pts = [(int(rng.integers(p.nt)), int(rng.integers(p.ny)), int(rng.integers(p.nx))) for _ in range(40)]
+    pts += [(p.nt - 1, 0, 0), (p.nt - 1, p.ny - 1, p.nx - 1), (p.nt - 1, 1024, 1024), (0, 0, 2048)]
+    got = _samples(U, pts)
+    umax = float(U.abs().max())
+    gm, c0 = modespace.mode_iterates(p, u0, 3)
+    ref = modespace.sample(p, gm, c0, pts)
+    assert np.abs(got - ref).max() <= 1e-10 * umax
