@@ -60,3 +60,26 @@ PD_DEV int pad16(int p) { return p + (p >> 4); }
 __host__ __device__ constexpr int padded16(int n) { return n + (n >> 4) + 1; }
 
 }  // namespace pd
+
+namespace pd {
+
+// ---- cp.async (LDGSTS): global -> shared without register staging; many copies in flight
+PD_DEV void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+PD_DEV void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+PD_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+PD_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+PD_DEV void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Double-index padding of a line buffer: two doubles (one complex slot) per 32 doubles, so that the
+// complex view of the same buffer is exactly pad16() (2·pad16(n) == dpad(2n)).
+PD_DEV int dpad(int j) { return j + 2 * (j >> 5); }
+__host__ __device__ constexpr int dpadded(int m) { return ((m + 2 * (m >> 5) + 2) + 1) & ~1; }
+
+}  // namespace pd

@@ -112,7 +112,7 @@ PD_DEV double2 twiddle(const double2* __restrict__ tw, int idx) {
 // One DIF pass of radix R = 2^r on a transform of size N = 2^log2n starting at stage s.
 template <int r, int SIGN>
 PD_DEV void dif_pass(double2* buf, int log2n, int s, const double2* __restrict__ tw, int twlog,
-                     int lane) {
+                     int lane, const double* __restrict__ pre = nullptr) {
   constexpr int R = 1 << r;
   const int log2H = log2n - s, log2Q = log2H - r;
   const int H = 1 << log2H, Q = 1 << log2Q;
@@ -124,6 +124,10 @@ PD_DEV void dif_pass(double2* buf, int log2n, int s, const double2* __restrict__
     double2 v[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) v[t] = buf[pad16(base + t * Q)];
+    if (pre) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[t] = cscale(v[t], __ldg(pre + base + t * Q));
+    }
     dif_reg<R, SIGN>(v);
 #pragma unroll
     for (int t = 1; t < R; ++t) {
@@ -138,7 +142,7 @@ PD_DEV void dif_pass(double2* buf, int log2n, int s, const double2* __restrict__
 // One DIT pass of radix R = 2^r: sub-transforms of size Q = 2^log2Q are combined into H = R·Q.
 template <int r, int SIGN>
 PD_DEV void dit_pass(double2* buf, int log2n, int log2Q, const double2* __restrict__ tw, int twlog,
-                     int lane) {
+                     int lane, const double* __restrict__ post = nullptr) {
   constexpr int R = 1 << r;
   const int log2H = log2Q + r;
   const int H = 1 << log2H, Q = 1 << log2Q;
@@ -156,22 +160,29 @@ PD_DEV void dit_pass(double2* buf, int log2n, int log2Q, const double2* __restri
       if (j) v[t] = cmul(v[t], twiddle<SIGN>(tw, e << tshift));
     }
     dit_reg<R, SIGN>(v);
+    if (post) {
+#pragma unroll
+      for (int t = 0; t < R; ++t) v[t] = cscale(v[t], __ldg(post + base + t * Q));
+    }
 #pragma unroll
     for (int t = 0; t < R; ++t) buf[pad16(base + t * Q)] = v[t];
   }
 }
 
-// Forward (SIGN=-1) or inverse (SIGN=+1) DIF FFT: natural in, bit-reversed out.
+// Forward (SIGN=-1) or inverse (SIGN=+1) DIF FFT: natural in, bit-reversed out.  `pre`
+// (optional, real, natural order) scales the input on the fly in the first pass.
 template <int SIGN>
-PD_DEV void warp_fft_dif(double2* buf, int log2n, const double2* __restrict__ tw, int twlog, int lane) {
+PD_DEV void warp_fft_dif(double2* buf, int log2n, const double2* __restrict__ tw, int twlog, int lane,
+                         const double* __restrict__ pre = nullptr) {
   int s = 0;
   while (s < log2n) {
     const int r = min(4, log2n - s);
+    const double* p = s == 0 ? pre : nullptr;
     switch (r) {
-      case 4: dif_pass<4, SIGN>(buf, log2n, s, tw, twlog, lane); break;
-      case 3: dif_pass<3, SIGN>(buf, log2n, s, tw, twlog, lane); break;
-      case 2: dif_pass<2, SIGN>(buf, log2n, s, tw, twlog, lane); break;
-      default: dif_pass<1, SIGN>(buf, log2n, s, tw, twlog, lane); break;
+      case 4: dif_pass<4, SIGN>(buf, log2n, s, tw, twlog, lane, p); break;
+      case 3: dif_pass<3, SIGN>(buf, log2n, s, tw, twlog, lane, p); break;
+      case 2: dif_pass<2, SIGN>(buf, log2n, s, tw, twlog, lane, p); break;
+      default: dif_pass<1, SIGN>(buf, log2n, s, tw, twlog, lane, p); break;
     }
     __syncwarp();
     s += r;
@@ -180,18 +191,21 @@ PD_DEV void warp_fft_dif(double2* buf, int log2n, const double2* __restrict__ tw
 
 // DIT FFT: bit-reversed in, natural out.  The first pass takes the remainder radix so that the
 // pass list is the DIF list reversed.
+// `post` (optional, real, natural order) scales the output in the last pass.
 template <int SIGN>
-PD_DEV void warp_fft_dit(double2* buf, int log2n, const double2* __restrict__ tw, int twlog, int lane) {
+PD_DEV void warp_fft_dit(double2* buf, int log2n, const double2* __restrict__ tw, int twlog, int lane,
+                         const double* __restrict__ post = nullptr) {
   int log2Q = 0;
   int rem = log2n & 3;
   while (log2Q < log2n) {
     const int r = rem ? rem : 4;
     rem = 0;
+    const double* p = log2Q + r >= log2n ? post : nullptr;
     switch (r) {
-      case 4: dit_pass<4, SIGN>(buf, log2n, log2Q, tw, twlog, lane); break;
-      case 3: dit_pass<3, SIGN>(buf, log2n, log2Q, tw, twlog, lane); break;
-      case 2: dit_pass<2, SIGN>(buf, log2n, log2Q, tw, twlog, lane); break;
-      default: dit_pass<1, SIGN>(buf, log2n, log2Q, tw, twlog, lane); break;
+      case 4: dit_pass<4, SIGN>(buf, log2n, log2Q, tw, twlog, lane, p); break;
+      case 3: dit_pass<3, SIGN>(buf, log2n, log2Q, tw, twlog, lane, p); break;
+      case 2: dit_pass<2, SIGN>(buf, log2n, log2Q, tw, twlog, lane, p); break;
+      default: dit_pass<1, SIGN>(buf, log2n, log2Q, tw, twlog, lane, p); break;
     }
     __syncwarp();
     log2Q += r;

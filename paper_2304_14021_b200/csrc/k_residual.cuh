@@ -138,4 +138,121 @@ __global__ void k_jbar_finalize(const double* __restrict__ jpart, size_t np, dou
   if (threadIdx.x == 0) st->jbar = sh[0] * inv_count;
 }
 
+// ------------------------------------------------------------------------------------------
+// 2D row-streaming residual.  A CTA of 128 threads owns one time slice n and a strip of 124
+// output columns (+2 halo columns on each side, one column per thread) and streams the
+// extended rows -2..ny+1 through a cp.async ring of depth RD: row r is in flight RD rows before
+// it is used, so each U element is read from HBM once (halo columns/rows excepted).  The BC
+// extension is applied per row/column as a sign: Neumann even reflection (ghost u_{-1} = u_1,
+// P:110-117), hinged odd reflection about the boundary node (u = 0 there, Δu = 0 ⇒ L(u) ghosts 0,
+// R#14) — evaluating the stencil on the extended grid reproduces the nested definitions exactly.
+// L(u) (or v = u³ - u - ε²L(u) for CH) is formed for row r-1, the outer L for row r-2, with the
+// x-neighbours exchanged through two double-buffered shared rows.
+constexpr int kResStrip = 124;
+constexpr int kResRing = 8;
+
+PD_DEV void ext_map(int g, int n, int neumann, int& idx, double& sgn) {
+  if (neumann) {
+    if (g < 0) g = -g;
+    if (g > n - 1) g = 2 * (n - 1) - g;
+    idx = min(max(g, 0), n - 1);
+    sgn = 1.0;
+  } else {
+    if (g >= 0 && g < n) { idx = g; sgn = 1.0; }
+    else if (g == -1 || g == n) { idx = 0; sgn = 0.0; }
+    else if (g < -1) { idx = min(-g - 2, n - 1); sgn = -1.0; }
+    else { idx = max(2 * n - g, 0); sgn = -1.0; }
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_residual_2d(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
+              ResidualParams P, double* __restrict__ jpart) {
+  __shared__ double ring_u[kResRing][128];
+  __shared__ double ring_p[kResRing][128];
+  __shared__ double su[2][128];
+  __shared__ double sv[2][128];
+  __shared__ double wsum[4];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * kResStrip;
+  const int n = blockIdx.y;
+  const size_t ns = (size_t)P.nx * P.ny;
+  const double* s = U + (size_t)n * ns;
+  const double* sp = n == 0 ? u0 : U + (size_t)(n - 1) * ns;
+  const int gx = x0 - 2 + tid;
+  int cx;
+  double sxg;
+  ext_map(gx, P.nx, P.neumann, cx, sxg);
+  const bool outcol = tid >= 2 && tid < kResStrip + 2 && gx < P.nx;
+  const int nrows = P.ny + 4;             // extended rows, grid row = r - 2
+  const bool ch = P.kind == 2;
+
+  auto issue = [&](int rr) {              // copies for iteration rr: u ext row rr, prev grid row rr-4
+    if (rr < nrows) {
+      int cy;
+      double sy;
+      ext_map(rr - 2, P.ny, P.neumann, cy, sy);
+      cp_async8(&ring_u[rr % kResRing][tid], s + (size_t)cy * P.nx + cx);
+      const int pr = rr - 4;
+      if (outcol && pr >= 0 && pr < P.ny) cp_async8(&ring_p[rr % kResRing][tid], sp + (size_t)pr * P.nx + gx);
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int rr = 0; rr < kResRing; ++rr) issue(rr);
+
+  double u_m2 = 0, u_m1 = 0;              // u at ext rows r-2, r-1
+  // at the top of iteration rr: u_m1/u_m2 = u at ext rows rr-1/rr-2; v_m1/v_m2 = inner value at ext
+  // rows rr-2/rr-3 (computed one iteration later than u); L_m1 = L(u) at ext row rr-2
+  double v_m2 = 0, v_m1 = 0;
+  double L_m1 = 0;
+  double jloc = 0.0;
+  for (int rr = 0; rr < nrows; ++rr) {
+    cp_async_wait_group<kResRing - 1>();
+    int cy;
+    double sy;
+    ext_map(rr - 2, P.ny, P.neumann, cy, sy);
+    const double uc = ring_u[rr % kResRing][tid] * (sxg * sy);
+    const double uprev = ring_p[rr % kResRing][tid];
+    issue(rr + kResRing);
+    su[rr & 1][tid] = uc;
+    __syncthreads();
+    // inner stage at ext row rr-1: L(u), or v = u³ - u - ε² L(u) for CH
+    double inner = 0.0, Lr = 0.0;
+    if (rr >= 2 && tid >= 1 && tid < 127) {
+      const double* row = su[(rr - 1) & 1];
+      Lr = ((row[tid - 1] + row[tid + 1]) + (u_m2 + uc) - 4.0 * u_m1) * P.inv_h2;
+      inner = ch ? u_m1 * u_m1 * u_m1 - u_m1 - P.e2 * Lr : Lr;
+    }
+    sv[(rr - 1) & 1][tid] = inner;
+    __syncthreads();
+    // outer stage at ext row rr-2 (grid row rr-4)
+    if (rr >= 4 && outcol) {
+      const double* row = sv[(rr - 2) & 1];
+      const double outer = ((row[tid - 1] + row[tid + 1]) + (v_m2 + inner) - 4.0 * v_m1) * P.inv_h2;
+      const double uo = u_m2;               // u at ext row rr-2
+      const double dtime = (uo - uprev) * P.inv_dt;
+      double out;
+      if (ch) {
+        out = outer - dtime;
+        jloc += 3.0 * uo * uo - 1.0;
+      } else {
+        const double Au = P.kind == 0 ? outer : P.b2 * L_m1 + P.e2 * outer;
+        out = -dtime - Au;
+      }
+      r[(size_t)n * ns + (size_t)(rr - 4) * P.nx + gx] = out;
+    }
+    u_m2 = u_m1; u_m1 = uc;
+    v_m2 = v_m1; v_m1 = inner;
+    L_m1 = Lr;
+  }
+  cp_async_wait_all();
+  if (ch) {
+    const double v = warp_sum(jloc);
+    if ((tid & 31) == 0) wsum[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) jpart[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = (wsum[0] + wsum[1]) + (wsum[2] + wsum[3]);
+  }
+}
+
 }  // namespace pd

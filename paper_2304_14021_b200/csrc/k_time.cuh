@@ -41,34 +41,39 @@ PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {
   return -jbar * Lam + P.e2 * (Lam * Lam);
 }
 
-// Load the tile's pencil pairs into shared memory (natural order), scaled by γ_j.
+// Stage the tile's pencil pairs in shared memory with cp.async (natural time order; the
+// γ_j scaling is applied on the fly by the first FFT pass).  Points past ns are zero.
 template <int NWARP>
 PD_DEV void load_pairs(const double* __restrict__ in, double2* smem, int64_t s0, const TimeParams& P) {
   const int pitch = padded16(P.nt);
-  for (int idx = threadIdx.x; idx < NWARP * P.nt; idx += NWARP * 32) {
-    const int j = idx / NWARP, w = idx - j * NWARP;
-    const int64_t s = s0 + 2 * w;
-    const double* row = in + (size_t)j * P.ns;
-    const double a = s < P.ns ? __ldg(row + s) : 0.0;
-    const double b = s + 1 < P.ns ? __ldg(row + s + 1) : 0.0;
-    const double g = __ldg(P.gam + j);
-    smem[w * pitch + pad16(j)] = make_double2(a * g, b * g);
+  double* sd = reinterpret_cast<double*>(smem);
+  for (int idx = threadIdx.x; idx < 2 * NWARP * P.nt; idx += NWARP * 32) {
+    const int j = idx / (2 * NWARP), rem = idx - j * (2 * NWARP);
+    const int w = rem >> 1, c = rem & 1;
+    const int64_t s = s0 + rem;
+    double* d = sd + 2 * (w * pitch + pad16(j)) + c;
+    if (s < P.ns) cp_async8(d, in + (size_t)j * P.ns + s);
+    else *d = 0.0;
   }
+  cp_async_commit();
+  cp_async_wait_all();
 }
 
+// Write the tile back (outputs already scaled by the last FFT pass).
 template <int NWARP>
 PD_DEV void store_pairs(double* __restrict__ out, const double2* smem, int64_t s0, const TimeParams& P) {
   const int pitch = padded16(P.nt);
+  const double* sd = reinterpret_cast<const double*>(smem);
   double lmax = 0.0;
-  for (int idx = threadIdx.x; idx < NWARP * P.nt; idx += NWARP * 32) {
-    const int j = idx / NWARP, w = idx - j * NWARP;
-    const int64_t s = s0 + 2 * w;
-    double* row = out + (size_t)j * P.ns;
-    const double2 v = smem[w * pitch + pad16(j)];
-    const double g = __ldg(P.ginv + j);
-    const double a = v.x * g, b = v.y * g;
-    if (s < P.ns) { row[s] = a; lmax = fmax(lmax, fabs(a)); }
-    if (s + 1 < P.ns) { row[s + 1] = b; lmax = fmax(lmax, fabs(b)); }
+  for (int idx = threadIdx.x; idx < 2 * NWARP * P.nt; idx += NWARP * 32) {
+    const int j = idx / (2 * NWARP), rem = idx - j * (2 * NWARP);
+    const int w = rem >> 1, c = rem & 1;
+    const int64_t s = s0 + rem;
+    if (s < P.ns) {
+      const double v = sd[2 * (w * pitch + pad16(j)) + c];
+      out[(size_t)j * P.ns + s] = v;
+      lmax = fmax(lmax, fabs(v));
+    }
   }
   if (P.amax) warp_atomic_max_abs(P.amax, lmax);
 }
@@ -85,7 +90,7 @@ k_time_solve_2d(const double* in, double* out, TimeParams P) {
   double2* buf = smem + warp * padded16(P.nt);
   const int64_t sa = s0 + 2 * warp;
   if (sa < P.ns) {
-    warp_fft_dif<-1>(buf, P.log2nt, P.tw, P.twlog, lane);
+    warp_fft_dif<-1>(buf, P.log2nt, P.tw, P.twlog, lane, P.gam);
     const double jbar = P.kind == 2 ? P.st->jbar : 0.0;
     const double mua = mode_mu(sa, P, jbar);
     const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
@@ -106,7 +111,7 @@ k_time_solve_2d(const double* in, double* out, TimeParams P) {
       if (m != l) buf[pm] = make_double2(Af.x + Bf.y, Bf.x - Af.y);
     }
     __syncwarp();
-    warp_fft_dit<+1>(buf, P.log2nt, P.tw, P.twlog, lane);
+    warp_fft_dit<+1>(buf, P.log2nt, P.tw, P.twlog, lane, P.ginv);
   }
   __syncthreads();
   store_pairs<NWARP>(out, smem, s0, P);
@@ -124,7 +129,7 @@ k_time_fwd_1d(const double* in, double2* spec, TimeParams P) {
   double2* buf = smem + warp * padded16(P.nt);
   const int64_t sa = s0 + 2 * warp;
   if (sa >= P.ns) return;
-  warp_fft_dif<-1>(buf, P.log2nt, P.tw, P.twlog, lane);
+  warp_fft_dif<-1>(buf, P.log2nt, P.tw, P.twlog, lane, P.gam);
   const int N = P.nt, half = N >> 1, nb = half + 1;
   for (int l = lane; l <= half; l += 32) {
     const double2 Zl = buf[pad16(bitrev(l, P.log2nt))];
@@ -153,7 +158,7 @@ k_time_inv_1d(const double2* spec, double* out, TimeParams P) {
       if (m != l) buf[pad16(bitrev(m, P.log2nt))] = make_double2(A.x + B.y, B.x - A.y);
     }
     __syncwarp();
-    warp_fft_dit<+1>(buf, P.log2nt, P.tw, P.twlog, lane);
+    warp_fft_dit<+1>(buf, P.log2nt, P.tw, P.twlog, lane, P.ginv);
   }
   __syncthreads();
   store_pairs<NWARP>(out, smem, s0, P);

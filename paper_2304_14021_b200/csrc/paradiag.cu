@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -22,6 +23,7 @@
 #include "k_residual.cuh"
 #include "k_spatial.cuh"
 #include "k_time.cuh"
+#include "k_fast.cuh"
 
 using namespace pd;
 
@@ -55,9 +57,18 @@ const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finali
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
                                          "time_fwd_1d", "penta_solve", "time_inv_1d"};
 
+constexpr int kFastTimeWarps = 4;  // register-FFT time pass (k_time2d_v2)
+constexpr int kFastRowWarps = 4;   // register-FFT rows
+// register-FFT columns: warps per CTA so that C = warps·32/E columns stays ≤ 64 (SMEM for the
+// [66][C] output staging) — E = transform length / 32
+constexpr int fast_col_warps(int E) { return E == 1 ? 2 : E == 2 ? 4 : 8; }
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr int kTime1DWarps = 4;
-constexpr int kLineWarps = 4;   // spatial DTT: lines per CTA
+constexpr int kLineWarps = 4;   // spatial DTT rows: one warp per row, 4 rows per CTA
+#ifndef PD_COLW
+#define PD_COLW 8
+#endif
+constexpr int kColW = PD_COLW;  // spatial DTT columns: adjacent columns per CTA (one warp each)
 
 bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 int ilog2(int64_t v) {
@@ -76,6 +87,7 @@ struct pd_handle {
   int64_t ns = 0, total = 0;
   int log2nt = 0, log2h = 0, twlog = 0, nb = 0;
   bool neumann = true;
+  bool fast = true;                   // register-FFT kernels (k_fast.cuh) where sizes allow
   double inv_dt = 0, inv_h2 = 0, b2 = 0, e2 = 0;
   // device buffers
   double* work = nullptr;             // 2D: δ/r workspace [nt][ns]; 1D: r [nt][nx]
@@ -187,18 +199,52 @@ int allow_smem(K kernel, size_t bytes) {
 }
 
 size_t time_smem(int nt, int warps) { return (size_t)warps * padded16(nt) * sizeof(double2); }
-size_t line_smem(int h) { return (size_t)kLineWarps * padded16(h) * sizeof(double2); }
+size_t fast_time_smem(int E) {
+  const size_t S = 2 * (32 / E) * kFastTimeWarps, tile = (size_t)32 * E * (S + 1);
+  return std::max(tile, (size_t)kFastTimeWarps * kWarpBufD) * sizeof(double);
+}
+size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
+size_t fast_cols_smem(int E) {
+  const size_t nw = fast_col_warps(E);
+  return (nw * kWarpBufD + 66 * nw * (32 / E)) * sizeof(double);
+}
+size_t rows_smem(int M) { return (size_t)kLineWarps * dpadded(M) * sizeof(double); }
+size_t cols_smem(int M) { return ((size_t)kColW * dpadded(M) + 66 * kColW) * sizeof(double); }
 
 // ----------------------------------------------------------------------------- launches
+template <int E>
+int fast_attrs_e() {
+  PD_CUDA(cudaFuncSetAttribute(k_time2d_v2<E, kFastTimeWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_time_smem(E)));
+  PD_CUDA(cudaFuncSetAttribute(k_rows_v2<1, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_rows_smem()));
+  PD_CUDA(cudaFuncSetAttribute(k_rows_v2<0, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_rows_smem()));
+  PD_CUDA(cudaFuncSetAttribute(k_cols_v2<1, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
+  PD_CUDA(cudaFuncSetAttribute(k_cols_v2<0, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
+  return PD_OK;
+}
+
+int setup_fast_attrs(pd_handle* h) {
+  if (!h->fast) return PD_OK;
+  int rc;
+  if ((rc = fast_attrs_e<1>()) || (rc = fast_attrs_e<2>()) || (rc = fast_attrs_e<4>()) || (rc = fast_attrs_e<8>()) ||
+      (rc = fast_attrs_e<16>()) || (rc = fast_attrs_e<32>()))
+    return rc;
+  return PD_OK;
+}
+
 int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) {
   ResidualParams R;
   R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
-  dim3 blk = h->P.dim == 2 ? dim3(32, 8) : dim3(256, 1);
-  dim3 grd((h->nx + blk.x - 1) / blk.x, (h->ny + blk.y - 1) / blk.y, h->P.nt);
   prof_begin(h, K_RESIDUAL);
-  k_residual<<<grd, blk, 0, h->stream>>>(u0, U, r, R, h->jpart);
+  if (h->P.dim == 2) {
+    dim3 grd((h->nx + kResStrip - 1) / kResStrip, h->P.nt);
+    k_residual_2d<<<grd, 128, 0, h->stream>>>(u0, U, r, R, h->jpart);
+  } else {
+    dim3 blk(256, 1);
+    dim3 grd((h->nx + blk.x - 1) / blk.x, 1, h->P.nt);
+    k_residual<<<grd, blk, 0, h->stream>>>(u0, U, r, R, h->jpart);
+  }
   prof_end(h, K_RESIDUAL);
   PD_LAUNCHED();
   if (h->P.kind == PD_CAHN_HILLIARD) {
@@ -212,27 +258,85 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
 
 LineParams line_params(pd_handle* h, int axis, unsigned long long* amax) {
   LineParams L;
-  const int64_t nt = h->P.nt;
-  if (axis == 0) {      // rows: contiguous lines
-    L.nlines = nt * h->ny; L.A = 1; L.B = h->nx; L.C = 0; L.es = 1;
-  } else {              // columns: stride nx
-    L.nlines = nt * h->nx; L.A = h->nx; L.B = h->ns; L.C = 1; L.es = h->nx;
-  }
+  L.nlines = (int64_t)h->P.nt * (axis == 0 ? h->ny : h->nx);
+  L.nx = h->nx;
+  L.ns = h->ns;
+  L.nel = h->nx;
   L.M = (int)h->P.m; L.log2h = h->log2h; L.trig = h->trig; L.tw = h->tw; L.twlog = h->twlog;
   L.amax = amax;
   return L;
 }
 
+template <int NEUMANN, int E>
+void launch_fast_line(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
+  if (axis == 0) {
+    const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
+    const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 16);
+    k_rows_v2<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, fast_rows_smem(), h->stream>>>(in, out, L);
+  } else {
+    constexpr int NW = fast_col_warps(E);
+    const int C = NW * (32 / E);
+    const int64_t groups = (int64_t)h->P.nt * ((h->nx + C - 1) / C);
+    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 16);
+    k_cols_v2<NEUMANN, E, NW><<<grid, NW * 32, fast_cols_smem(E), h->stream>>>(in, out, L);
+  }
+}
+
+template <int NEUMANN>
+bool fast_line(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
+  switch (L.M) {
+    case 64: launch_fast_line<NEUMANN, 1>(h, in, out, axis, L); return true;
+    case 128: launch_fast_line<NEUMANN, 2>(h, in, out, axis, L); return true;
+    case 256: launch_fast_line<NEUMANN, 4>(h, in, out, axis, L); return true;
+    case 512: launch_fast_line<NEUMANN, 8>(h, in, out, axis, L); return true;
+    case 1024: launch_fast_line<NEUMANN, 16>(h, in, out, axis, L); return true;
+    case 2048: launch_fast_line<NEUMANN, 32>(h, in, out, axis, L); return true;
+    default: return false;
+  }
+}
+
 int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid) {
   LineParams L = line_params(h, axis, amax);
-  const unsigned grid = (unsigned)((L.nlines + kLineWarps - 1) / kLineWarps);
-  const size_t smem = line_smem(1 << h->log2h);
   prof_begin(h, kid);
-  if (h->neumann) k_dtt_lines<1, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
-  else k_dtt_lines<0, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
+  const bool fast = h->fast && (h->neumann ? fast_line<1>(h, in, out, axis, L) : fast_line<0>(h, in, out, axis, L));
+  if (!fast) {
+    if (axis == 0) {
+      const unsigned grid = (unsigned)((L.nlines + kLineWarps - 1) / kLineWarps);
+      const size_t smem = rows_smem(L.M);
+      if (h->neumann) k_dtt_rows<1, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
+      else k_dtt_rows<0, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
+    } else {
+      const int64_t groups = (int64_t)h->P.nt * ((h->nx + kColW - 1) / kColW);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 64);
+      const size_t smem = cols_smem(L.M);
+      if (h->neumann) k_dtt_cols<1, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
+      else k_dtt_cols<0, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
+    }
+  }
   prof_end(h, kid);
   PD_LAUNCHED();
   return PD_OK;
+}
+
+template <int E>
+void launch_fast_time(pd_handle* h, const double* in, double* out, const TimeParams& T) {
+  constexpr int S = 2 * (32 / E) * kFastTimeWarps;
+  const int64_t tiles = (h->ns + S - 1) / S;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
+  k_time2d_v2<E, kFastTimeWarps><<<grid, kFastTimeWarps * 32, fast_time_smem(E), h->stream>>>(in, out, T);
+}
+
+bool fast_time(pd_handle* h, const double* in, double* out, const TimeParams& T) {
+  if (!h->fast) return false;
+  switch (h->P.nt) {
+    case 32: launch_fast_time<1>(h, in, out, T); return true;
+    case 64: launch_fast_time<2>(h, in, out, T); return true;
+    case 128: launch_fast_time<4>(h, in, out, T); return true;
+    case 256: launch_fast_time<8>(h, in, out, T); return true;
+    case 512: launch_fast_time<16>(h, in, out, T); return true;
+    case 1024: launch_fast_time<32>(h, in, out, T); return true;
+    default: return false;
+  }
 }
 
 TimeParams time_params(pd_handle* h, unsigned long long* amax) {
@@ -253,7 +357,8 @@ int precond(pd_handle* h, const double* r, double* delta) {
     TimeParams T = time_params(h, nullptr);
     const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
     prof_begin(h, K_TIME);
-    k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
+    if (!fast_time(h, delta, delta, T))
+      k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV))) return rc;
@@ -464,8 +569,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     if (e != cudaSuccess) return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
   }
   if (p->kind == PD_CAHN_HILLIARD) {
-    const size_t gx = (h->nx + 31) / 32, gy = (h->ny + 7) / 8;
-    h->njpart = gx * gy * nt;
+    h->njpart = (size_t)((h->nx + kResStrip - 1) / kResStrip) * nt;
     PD_TRY(dalloc(h, &h->jpart, h->njpart));
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
@@ -514,8 +618,12 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     PD_TRY(allow_smem(k_time_inv_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
   } else {
     PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
-    PD_TRY(allow_smem(k_dtt_lines<1, kLineWarps>, line_smem(1 << h->log2h)));
-    PD_TRY(allow_smem(k_dtt_lines<0, kLineWarps>, line_smem(1 << h->log2h)));
+    PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));
+    PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
+    PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
+    PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
+    if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
+    PD_TRY(setup_fast_attrs(h));
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
 #undef PD_TRY

@@ -30,6 +30,11 @@ CASES = {
     "c5_m128_nt4": twin("c5", m=128, nt=4),
     "c4_m32": twin("c4", m=32, nt=16, t_window=16e-4, n_windows=2),
     "c4_m16_nt8": twin("c4", m=16, nt=8, t_window=8e-4, n_windows=1),
+    # register-FFT (k_fast.cuh) sizes: transform lengths ≥ 32 on both axes and in time
+    "c5_m128_nt128": twin("c5", m=128, nt=128),
+    "c3_m256_nt64": twin("c3", m=256, nt=64),
+    "c4_m64_nt32": twin("c4", m=64, nt=32, t_window=32e-4, n_windows=1),
+    "c5_m64_nt256": twin("c5", m=64, nt=256),
 }
 
 
