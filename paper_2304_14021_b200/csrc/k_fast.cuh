@@ -54,46 +54,29 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
     }
     __syncthreads();
     fft4_s1_to_s2<E, -1>(v, T, LOG2NT, P.tw, P.twlog, lane);
-    // ---- per-mode divide.  lane = (pair pl, k1); v[k2] = Z[k1 + E k2]; Z_{N-l} of l = k1 + E k2
-    // lives in lane (pl, E-k1) register 31-k2 (k1 ≠ 0) or in this lane's register (32-k2)&31.
+    // ---- per-mode divide (Step-(2)).  lane = (pair pl, k1), v[k2] = Z[l], l = k1 + E k2.  The
+    // spectrum is parked in natural order in the warp scratch so every lane reads its Z_{N-l}
+    // with the same code path (no divergence, no register hazards).
     const int pl = lane / E, k1 = lane - pl * E;
     const int64_t sa = s0 + 2 * (warp * PP + pl);
     const double mua = sa < P.ns ? mode_mu(sa, P, jbar) : 0.0;
     const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
-    const int partner = pl * E + ((E - k1) & (E - 1));
-    auto combine = [&](double2 Zl, double2 Zm, int l) -> double2 {
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * NT + k1 + E * k2)] = v[k2];
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) {
+      const int l = k1 + E * k2;
+      const double2 Zl = v[k2];
+      const double2 Zm = T[tpad(pl * NT + ((NT - l) & (NT - 1)))];
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
-      const double2 Af = cmul(A, cinv(make_double2(d.x + mua, d.y)));
-      const double2 Bf = cmul(B, cinv(make_double2(d.x + mub, d.y)));
-      return make_double2(Af.x - Bf.y, Af.y + Bf.x);      // X_l = Af + i Bf
-    };
-    if (E > 1) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double2 ta = make_double2(__shfl_sync(0xffffffffu, v[31 - j].x, partner),
-                                        __shfl_sync(0xffffffffu, v[31 - j].y, partner));
-        const double2 tb = make_double2(__shfl_sync(0xffffffffu, v[j].x, partner),
-                                        __shfl_sync(0xffffffffu, v[j].y, partner));
-        if (k1 != 0) {
-          const double2 xa = combine(v[j], ta, k1 + E * j);
-          const double2 xb = combine(v[31 - j], tb, k1 + E * (31 - j));
-          v[j] = xa;
-          v[31 - j] = xb;
-        }
-      }
+      const double2 Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
+      const double2 Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
+      v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);      // X_l = Af + i Bf
     }
-    if (k1 == 0) {
-#pragma unroll
-      for (int j = 0; j <= 16; ++j) {
-        const int m = (32 - j) & 31;
-        const double2 xa = combine(v[j], v[m], E * j);
-        const double2 xb = combine(v[m], v[j], E * m);
-        v[j] = xa;
-        if (m != j) v[m] = xb;
-      }
-    }
+    __syncwarp();
     fft4_s2_to_s1<E, +1>(v, T, LOG2NT, P.tw, P.twlog, lane);
     __syncthreads();
 #pragma unroll
@@ -258,6 +241,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 k_cols_v2(const double* in, double* out, LineParams P) {
   using D = DttWarp<NEUMANN, E>;
   constexpr int C = NW * D::PL;
+  constexpr int SP = C + 1;                    // staging row pitch (bank skew)
   extern __shared__ double2 smem2[];
   double* base = reinterpret_cast<double*>(smem2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -290,7 +274,7 @@ k_cols_v2(const double* in, double* out, LineParams P) {
     __syncthreads();
     const int nl = max(0, min(D::PL, wcols - warp * D::PL));
     D::run(xb, nl, P, lane,
-           [&](int p, int idx, double v, int k0) { stage[(idx - 2 * k0 + 1) * C + warp * D::PL + p] = v; },
+           [&](int p, int idx, double v, int k0) { stage[(idx - 2 * k0 + 1) * SP + warp * D::PL + p] = v; },
            [&](int k0) {
              __syncthreads();
              int lo, hi;
@@ -304,7 +288,7 @@ k_cols_v2(const double* in, double* out, LineParams P) {
              for (int i = threadIdx.x; i < (hi - lo) * C; i += NW * 32) {
                const int r = i / C, c = i - r * C;
                if (c < wcols) {
-                 const double v = stage[(lo + r - 2 * k0 + 1) * C + c];
+                 const double v = stage[(lo + r - 2 * k0 + 1) * SP + c];
                  dst[(int64_t)(lo + r) * P.nx + c] = v;
                  lmax = fmax(lmax, fabs(v));
                }

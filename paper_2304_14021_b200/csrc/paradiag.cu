@@ -206,7 +206,7 @@ size_t fast_time_smem(int E) {
 size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
 size_t fast_cols_smem(int E) {
   const size_t nw = fast_col_warps(E);
-  return (nw * kWarpBufD + 66 * nw * (32 / E)) * sizeof(double);
+  return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
 }
 size_t rows_smem(int M) { return (size_t)kLineWarps * dpadded(M) * sizeof(double); }
 size_t cols_smem(int M) { return ((size_t)kColW * dpadded(M) + 66 * kColW) * sizeof(double); }

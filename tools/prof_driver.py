@@ -14,7 +14,8 @@ from workloads import config, make_u0  # noqa: E402
 nt = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 name = sys.argv[3] if len(sys.argv) > 3 else "c5"
-p = replace(config(name), nt=nt, t_window=config(name).t_window * nt / config(name).nt)
+m = int(sys.argv[4]) if len(sys.argv) > 4 else config(name).m
+p = replace(config(name), nt=nt, m=m, t_window=config(name).t_window * nt / config(name).nt)
 s = pd.Solver(p)
 u0 = torch.from_numpy(make_u0(p)).cuda()
 U = torch.zeros(s.shape, dtype=torch.float64, device="cuda")
