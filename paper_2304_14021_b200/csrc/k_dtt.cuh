@@ -1,0 +1,274 @@
+// k_dtt.cuh — DCT-I (Neumann) / DST-I (hinged) line passes of Step-(2) in 2D,
+// third version.  Mathematics as k_spatial.cuh: a length-M real-to-real
+// transform via one complex FFT of H = M/2 points (fft4.cuh, register resident, one warp holds
+// P = 32/E lines of M = 64E), then
+//   DCT-I: X_{2k} = 2 Re Y_k,  X_{2k+1} = X_1 - 2 Σ_{i=1}^{k} Im Y_i,  X_M = 2 (Re Z_0 - Im Z_0)
+//   DST-I: X_{2k} = -2 Im Y_k, X_{2k+1} = Re Y_0 + 2 Σ_{i=1}^{k} Re Y_i
+// with Y_k = E_k + W_M^k O_k split from Z_k and conj Z_{H-k}.
+//
+// What changed against k_fast.cuh (ncu r01a: the line kernels were issue-bound, 3.5 warp
+// instructions per point, 45% of them integer overhead):
+//   * the prefix sums run in a BLOCKED layout — lane b of a line owns k = 32b .. 32b+31, sums them
+//     serially in registers and needs a single segmented warp scan of the 32 block totals per line
+//     (before: one 5-step shuffle scan per 32 outputs);
+//   * the finished line is written back into the warp buffer (padded, bank-conflict free) and
+//     stored with coalesced row (or column-tile) stores — no per-chunk CTA barriers;
+//   * the next work item is prefetched into L2 while the current one computes, so HBM streams
+//     under the FFT arithmetic even at one or two CTAs per SM;
+//   * cos/sin(2πk/M) for the split come from a table laid out [j][b] so a warp's loads coalesce.
+#pragma once
+#include "common.cuh"
+#include "fft4.cuh"
+#include "k_spatial.cuh"
+
+namespace pd {
+
+// L2 prefetch hints (no data returned; never fault the kernel's own accesses)
+PD_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// one bulk prefetch of [p, p + bytes) rounded out to 16 B and clipped to [.., limit)
+PD_DEV void bulk_prefetch_l2(const void* p, size_t bytes, const void* limit) {
+  size_t a = (size_t)p & ~(size_t)15, e = ((size_t)p + bytes + 15) & ~(size_t)15;
+  const size_t lim = (size_t)limit & ~(size_t)15;
+  if (e > lim) e = lim;
+  if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
+__host__ __device__ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+
+template <int NEUMANN, int E>
+struct Dtt3 {
+  static constexpr int P = 32 / E, M = 64 * E, H = 32 * E, LDX = M + 2;
+  static constexpr int LOG2H = 5 + ilog2_c(E);
+  // output staging: stored index q of line p lives at p*LDO + q + q/64 (64-bit accesses of a
+  // half-warp land on 16 distinct banks for the blocked writes and the coalesced reads)
+  static constexpr int LDO_MIN = M + E + 1;
+  static constexpr int LDO = E >= 16 ? LDO_MIN : ((LDO_MIN + 15) / 16) * 16 + E;
+  static constexpr int BUF = (cmax3(2 * kWarpScratch + 2, P * LDX, P * LDO) + 1) & ~1;   // doubles per warp
+  PD_DEV static int opos(int q) { return q + (q >> 6); }
+
+  // Transform the P lines held in xb (line p at p*LDX, buffer index 0..M, hinged ends zero) and
+  // leave the outputs in xb at p*LDO + opos(stored index).  trig[j] = (cos, sin)(πj/M), j ≤ M;
+  // trig2 = (cos, sin)(2πk/M) stored at [j*E + b] for k = 32b + j.
+  PD_DEV static void transform(double* xb, const LineParams& L, const double2* __restrict__ trig2, int lane) {
+    double2 v[32];
+    double x1p[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      double acc = 0.0;
+      const double* x = xb + p * LDX;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int n = lane + 32 * e, j0 = 2 * n;
+        const double2 a = *reinterpret_cast<const double2*>(x + j0);   // x_{2n}, x_{2n+1}
+        const double m0 = x[M - j0], m1 = x[M - j0 - 1];
+        const double2 t0 = __ldg(L.trig + j0), t1 = __ldg(L.trig + j0 + 1);
+        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, t0.y), ymap<NEUMANN>(a.y, m1, t1.y));
+        if (NEUMANN) acc = fma(a.x - m0, t0.x, fma(a.y - m1, t1.x, acc));
+      }
+      x1p[p] = acc;
+    }
+    if (NEUMANN) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) x1p[p] = warp_sum(x1p[p]);
+    }
+    __syncwarp();
+    double2* T = reinterpret_cast<double2*>(xb);
+    fft4_s1_to_s2<E, -1>(v, T, LOG2H, L.tw, L.twlog, lane);
+    const int pl = lane / E, b = lane - pl * E;
+    {
+#pragma unroll
+      for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * H + b + E * k2)] = v[k2];   // natural order
+    }
+    __syncwarp();
+    // ---- blocked split + serial prefix: lane (pl, b) owns k = 32b + j
+    double run = 0.0;
+    double2 Z0 = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int k = 32 * b + j;
+      const double2 Zk = T[tpad(pl * H + k)];
+      const double2 Zm = T[tpad(pl * H + ((H - k) & (H - 1)))];
+      const double2 Ev = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+      const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+      const double2 t = __ldg(trig2 + j * E + b);
+      const double Yx = Ev.x + t.x * O.x + t.y * O.y;
+      const double Yy = Ev.y + t.x * O.y - t.y * O.x;
+      double ev, a;
+      if (NEUMANN) {
+        ev = 2.0 * Yx;
+        a = k == 0 ? 0.0 : Yy;
+      } else {
+        ev = -2.0 * Yy;
+        a = k == 0 ? Yx : 2.0 * Yx;
+      }
+      run += a;
+      v[j] = make_double2(ev, run);
+    }
+    if (NEUMANN) Z0 = T[tpad(pl * H)];
+    // segmented exclusive scan of the block totals over the E lanes of each line
+    double incl = run;
+#pragma unroll
+    for (int o = 1; o < E; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (b >= o) incl += t;
+    }
+    double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (b == 0) excl = 0.0;
+    double x1 = 0.0;
+    if (NEUMANN) {
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p == pl) x1 = x1p[p];
+    }
+    __syncwarp();                      // every lane has read T: overwrite with the outputs
+    double* ob = xb + pl * LDO;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int q = 64 * b + 2 * j;
+      if (NEUMANN) {
+        ob[opos(q)] = v[j].x;                                  // X_{2k}
+        ob[opos(q + 1)] = x1 - 2.0 * (excl + v[j].y);          // X_{2k+1}
+      } else {
+        ob[opos(q)] = excl + v[j].y;                           // X_{2k+1}: stored index 2k
+        if (q > 0) ob[opos(q - 1)] = v[j].x;                   // X_{2k}:   stored index 2k-1
+      }
+    }
+    if (NEUMANN && b == E - 1) ob[opos(M)] = 2.0 * (Z0.x - Z0.y);   // X_M
+    __syncwarp();
+  }
+};
+
+// ---------------------------------------------------------------- rows (contiguous lines)
+// Warps are independent: each takes P consecutive lines per step, prefetches its next group into
+// L2, stages the lines with cp.async, transforms and stores them coalesced.
+template <int NEUMANN, int E, int NW>
+__global__ void __launch_bounds__(NW * 32, 2)
+k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
+  using D = Dtt3<NEUMANN, E>;
+  extern __shared__ double2 smem2[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xb = reinterpret_cast<double*>(smem2) + (size_t)warp * D::BUF;
+  double lmax = 0.0;
+  const int64_t ngroups = (L.nlines + D::P - 1) / D::P;
+  const int64_t gstride = (int64_t)gridDim.x * NW;
+  const double* in_end = in + L.nlines * L.nx;
+  if (!NEUMANN) {
+    for (int p = lane; p < D::P; p += 32) {
+      xb[p * D::LDX] = 0.0;
+      xb[p * D::LDX + D::M] = 0.0;
+    }
+  }
+  for (int64_t g = (int64_t)blockIdx.x * NW + warp; g < ngroups; g += gstride) {
+    const int64_t L0 = g * D::P;
+    const int64_t rem = L.nlines - L0;
+    const int nl = rem < D::P ? (int)rem : D::P;
+    const double* src = in + L0 * L.nx;
+    if (lane == 0 && g + gstride < ngroups)
+      bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
+#pragma unroll
+    for (int p = 0; p < D::P; ++p) {
+      if (p < nl) {
+        double* x = xb + p * D::LDX + (NEUMANN ? 0 : 1);
+        const double* s = src + p * L.nx;
+        for (int e = lane; e < L.nel; e += 32) cp_async8(x + e, s + e);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    if (!NEUMANN) {   // hinged ghosts were overwritten by the previous outputs: restore zeros
+      for (int p = lane; p < D::P; p += 32) {
+        xb[p * D::LDX] = 0.0;
+        xb[p * D::LDX + D::M] = 0.0;
+      }
+      __syncwarp();
+    }
+    D::transform(xb, L, trig2, lane);
+    double* dst = out + L0 * L.nx;
+#pragma unroll
+    for (int p = 0; p < D::P; ++p) {
+      if (p < nl) {
+        const double* ob = xb + p * D::LDO;
+        double* d = dst + p * L.nx;
+        for (int q = lane; q < L.nel; q += 32) {
+          const double v = ob[D::opos(q)];
+          d[q] = v;
+          lmax = fmax(lmax, fabs(v));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (L.amax) warp_atomic_max_abs(L.amax, lmax);
+}
+
+// ---------------------------------------------------------------- columns (stride nx)
+// CTA = NW warps x P lines = C adjacent columns of one slice.  Rows of the tile are loaded C
+// doubles wide (cp.async straight into each column's line buffer), the next tile is prefetched
+// into L2 during the transforms, outputs are read back from the line buffers row by row.
+template <int NEUMANN, int E, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
+  using D = Dtt3<NEUMANN, E>;
+  constexpr int C = NW * D::P;
+  constexpr int NTH = NW * 32;
+  extern __shared__ double2 smem2[];
+  double* base = reinterpret_cast<double*>(smem2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xb = base + (size_t)warp * D::BUF;
+  const int64_t gx = (L.nx + C - 1) / C;
+  const int64_t nsl = L.nlines / L.nx;
+  const int64_t ngroups = nsl * gx;
+  double lmax = 0.0;
+  for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
+    const int64_t n = G / gx;
+    const int x0 = (int)((G - n * gx) * C);
+    const int wcols = min(C, (int)(L.nx - x0));
+    const double* src = in + n * L.ns + x0;
+    double* dst = out + n * L.ns + x0;
+    {
+      const int64_t Gn = G + gridDim.x;
+      if (Gn < ngroups) {
+        const int64_t nn = Gn / gx;
+        const int xn = (int)((Gn - nn * gx) * C);
+        const int wn = min(C, (int)(L.nx - xn));
+        const double* s = in + nn * L.ns + xn;
+        for (int e = threadIdx.x; e < L.nel; e += NTH) {
+          prefetch_l2(s + (int64_t)e * L.nx);
+          prefetch_l2(s + (int64_t)e * L.nx + wn - 1);
+        }
+      }
+    }
+    for (int i = threadIdx.x; i < L.nel * C; i += NTH) {
+      const int e = i / C, c = i - e * C;
+      if (c < wcols) {
+        const int w = c / D::P, p = c - w * D::P;
+        cp_async8(base + (size_t)w * D::BUF + p * D::LDX + bidx<NEUMANN>(e), src + (int64_t)e * L.nx + c);
+      }
+    }
+    cp_async_commit();
+    if (!NEUMANN) {
+      for (int p = lane; p < D::P; p += 32) {
+        xb[p * D::LDX] = 0.0;
+        xb[p * D::LDX + D::M] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    D::transform(xb, L, trig2, lane);
+    __syncthreads();
+    for (int i = threadIdx.x; i < L.nel * C; i += NTH) {
+      const int e = i / C, c = i - e * C;
+      if (c < wcols) {
+        const int w = c / D::P, p = c - w * D::P;
+        const double v = base[(size_t)w * D::BUF + p * D::LDO + D::opos(e)];
+        dst[(int64_t)e * L.nx + c] = v;
+        lmax = fmax(lmax, fabs(v));
+      }
+    }
+    __syncthreads();
+  }
+  if (L.amax) warp_atomic_max_abs(L.amax, lmax);
+}
+
+}  // namespace pd

@@ -24,6 +24,7 @@
 #include "k_spatial.cuh"
 #include "k_time.cuh"
 #include "k_fast.cuh"
+#include "k_dtt.cuh"
 
 using namespace pd;
 
@@ -100,6 +101,8 @@ struct pd_handle {
   double* lam = nullptr;
   double2* tw = nullptr;
   double2* trig = nullptr;
+  double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
+  int dtt_ver = 3;                    // line kernels: 3 = k_dtt.cuh, 2 = k_fast.cuh
   double* band = nullptr;
   double2* fac = nullptr;             // 4 x [nx][nb]
   DevStats* st = nullptr;
@@ -208,6 +211,10 @@ size_t fast_cols_smem(int E) {
   const size_t nw = fast_col_warps(E);
   return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
 }
+template <int E>
+size_t dtt3_rows_smem() { return (size_t)kFastRowWarps * Dtt3<1, E>::BUF * sizeof(double); }
+template <int E>
+size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * sizeof(double); }
 size_t rows_smem(int M) { return (size_t)kLineWarps * dpadded(M) * sizeof(double); }
 size_t cols_smem(int M) { return ((size_t)kColW * dpadded(M) + 66 * kColW) * sizeof(double); }
 
@@ -219,6 +226,10 @@ int fast_attrs_e() {
   PD_CUDA(cudaFuncSetAttribute(k_rows_v2<0, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_rows_smem()));
   PD_CUDA(cudaFuncSetAttribute(k_cols_v2<1, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
   PD_CUDA(cudaFuncSetAttribute(k_cols_v2<0, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
+  PD_CUDA(cudaFuncSetAttribute(k_rows3<1, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_rows_smem<E>()));
+  PD_CUDA(cudaFuncSetAttribute(k_rows3<0, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_rows_smem<E>()));
+  PD_CUDA(cudaFuncSetAttribute(k_cols3<1, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_cols_smem<E>()));
+  PD_CUDA(cudaFuncSetAttribute(k_cols3<0, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_cols_smem<E>()));
   return PD_OK;
 }
 
@@ -269,6 +280,20 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax) {
 
 template <int NEUMANN, int E>
 void launch_fast_line(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
+  if (h->dtt_ver == 3) {
+    if (axis == 0) {
+      const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
+      const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
+      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, dtt3_rows_smem<E>(), h->stream>>>(in, out, L, h->trig2);
+    } else {
+      constexpr int NW = fast_col_warps(E);
+      const int C = NW * (32 / E);
+      const int64_t groups = (int64_t)h->P.nt * ((h->nx + C - 1) / C);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+      k_cols3<NEUMANN, E, NW><<<grid, NW * 32, dtt3_cols_smem<E>(), h->stream>>>(in, out, L, h->trig2);
+    }
+    return;
+  }
   if (axis == 0) {
     const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
     const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 16);
@@ -535,6 +560,13 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     tw[k] = make_double2(std::cos(ang), -std::sin(ang));
   }
   for (int j = 0; j <= M; ++j) trig[j] = make_double2(std::cos(M_PI * j / M), std::sin(M_PI * j / M));
+  // k_dtt.cuh split table: (cos, sin)(2πk/M) for k = 32b + j stored at j*E + b, E = M/64
+  const int H2 = std::max(M / 2, 1), E2 = std::max(M / 64, 1);
+  std::vector<double2> trig2(H2);
+  for (int k = 0; k < H2; ++k) {
+    const int b = k / 32, j = k % 32;
+    trig2[(size_t)j * E2 + b] = trig[std::min(2 * k, M)];
+  }
 
   // ---- singularity check of d_l + μ (linear kinds): only l = 0 and N_t/2 have real d_l
   if (p->kind != PD_CAHN_HILLIARD) {
@@ -563,6 +595,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
   PD_TRY(dalloc(h, &h->lam, h->nx));
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
+  PD_TRY(dalloc(h, &h->trig2, (size_t)H2));
   PD_TRY(dalloc(h, &h->st, 1));
   {
     cudaError_t e = cudaMallocHost(&h->st_host, sizeof(DevStats));
@@ -575,7 +608,8 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
       up(h->dl, dl.data(), nt * sizeof(double2)) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
-      up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)))
+      up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
+      up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)))
     return cleanup(fail(PD_ECUDA, "table upload failed"));
 
   if (p->dim == 1) {
@@ -623,6 +657,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
+    if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
