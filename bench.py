@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_DOF = {  # algorithmic HBM bytes per space-time dof per launch
     "residual": 16.0, "dtt_x_fwd": 16.0, "dtt_y_fwd": 16.0, "time_solve_2d": 16.0,
-    "dtt_y_inv": 16.0, "dtt_x_inv": 16.0, "update": 24.0,
+    "dtt_y_inv": 16.0, "dtt_x_inv": 16.0, "update": 24.0, "dtt_x_inv_update": 24.0,
 }
 
 

@@ -60,6 +60,14 @@ PD_DEV double warp_sum(double v) {
   return v;
 }
 
+// Running max of |v| for the ‖δ‖∞ epilogues: a compare + select (fmax's NaN rules cost ~4x the
+// instructions).  A NaN is not propagated here; it reaches U through the update, whose ‖U‖∞
+// reduction (bit-pattern max, NaN sorts above +inf) and the host isfinite check catch it.
+PD_DEV double amax_acc(double m, double v) {
+  const double a = fabs(v);
+  return a > m ? a : m;
+}
+
 // Block-wide max of |v| folded into *dst with one atomic per warp.
 PD_DEV void warp_atomic_max_abs(unsigned long long* dst, double v) {
   unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));

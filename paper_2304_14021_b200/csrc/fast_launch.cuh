@@ -1,0 +1,118 @@
+// fast_launch.cuh — launch wrappers of the register-FFT passes (k_dtt.cuh line transforms,
+// k_fast.cuh time pass), one instantiation per E = transform length / 32 in its own translation
+// unit (fast_e<E>.cu) so the library builds in parallel.  paradiag.cu sees only the declarations.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "k_dtt.cuh"
+#include "k_fast.cuh"
+
+namespace pd {
+
+constexpr int kFastTimeWarps = 4;  // k_time2d_v2: warps per CTA
+constexpr int kFastRowWarps = 4;   // k_rows3 / k_rows_v2: warps per CTA (independent)
+// column kernels: warps per CTA (C = warps·32/E adjacent columns per tile)
+constexpr int fast_col_warps(int E) { return E == 1 ? 2 : E == 2 ? 4 : 8; }
+
+struct FastLaunch {
+  cudaStream_t stream;
+  int nt;                 // time slices
+  int nx;                 // points per row (square grids)
+  int64_t ns;             // points per slice
+  const double2* trig2;   // k_dtt.cuh split table
+  int dtt_ver;            // 3 = k_dtt.cuh, 2 = k_fast.cuh line kernels
+};
+
+template <int E>
+cudaError_t fast_attrs();
+template <int E>
+void fast_line(int neumann, int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F);
+template <int E>
+void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F);
+
+#ifdef PD_FAST_DEFINE
+inline size_t fast_time_smem(int E) {
+  const size_t S = 2 * (32 / E) * kFastTimeWarps, tile = (size_t)32 * E * (S + 1);
+  return std::max(tile, (size_t)kFastTimeWarps * kWarpBufD) * sizeof(double);
+}
+inline size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
+inline size_t fast_cols_smem(int E) {
+  const size_t nw = fast_col_warps(E);
+  return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
+}
+template <int E>
+size_t dtt3_rows_smem() { return (size_t)kFastRowWarps * Dtt3<1, E>::BUF * sizeof(double); }
+template <int E>
+size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * sizeof(double); }
+
+#define PD_ATTR(k, b)                                                                            \
+  do {                                                                                           \
+    cudaError_t e_ = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(b)); \
+    if (e_ != cudaSuccess) return e_;                                                            \
+  } while (0)
+
+template <int E>
+cudaError_t fast_attrs() {
+  PD_ATTR((k_time2d_v2<E, kFastTimeWarps>), fast_time_smem(E));
+  PD_ATTR((k_rows_v2<1, E, kFastRowWarps>), fast_rows_smem());
+  PD_ATTR((k_rows_v2<0, E, kFastRowWarps>), fast_rows_smem());
+  PD_ATTR((k_cols_v2<1, E, fast_col_warps(E)>), fast_cols_smem(E));
+  PD_ATTR((k_cols_v2<0, E, fast_col_warps(E)>), fast_cols_smem(E));
+  PD_ATTR((k_rows3<1, E, kFastRowWarps>), dtt3_rows_smem<E>());
+  PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>());
+  PD_ATTR((k_cols3<1, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols3<0, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
+  return cudaSuccess;
+}
+#undef PD_ATTR
+
+template <int NEUMANN, int E>
+void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F) {
+  constexpr int NW = fast_col_warps(E);
+  const int C = NW * (32 / E);
+  if (F.dtt_ver == 3) {
+    if (axis == 0) {
+      const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
+      const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
+      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, dtt3_rows_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+    } else {
+      const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+      k_cols3<NEUMANN, E, NW><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+    }
+    return;
+  }
+  if (axis == 0) {
+    const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
+    const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 16);
+    k_rows_v2<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, fast_rows_smem(), F.stream>>>(in, out, L);
+  } else {
+    const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
+    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 16);
+    k_cols_v2<NEUMANN, E, NW><<<grid, NW * 32, fast_cols_smem(E), F.stream>>>(in, out, L);
+  }
+}
+
+template <int E>
+void fast_line(int neumann, int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F) {
+  if (neumann) fast_line_bc<1, E>(axis, in, out, L, F);
+  else fast_line_bc<0, E>(axis, in, out, L, F);
+}
+
+template <int E>
+void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F) {
+  constexpr int S = 2 * (32 / E) * kFastTimeWarps;
+  const int64_t tiles = (F.ns + S - 1) / S;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
+  k_time2d_v2<E, kFastTimeWarps><<<grid, kFastTimeWarps * 32, fast_time_smem(E), F.stream>>>(in, out, T);
+}
+
+#define PD_FAST_INSTANTIATE(E)                                                                       \
+  template cudaError_t fast_attrs<E>();                                                             \
+  template void fast_line<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&); \
+  template void fast_time<E>(const double*, double*, const TimeParams&, const FastLaunch&);
+#endif
+
+}  // namespace pd

@@ -138,6 +138,52 @@ struct Dtt3 {
   }
 };
 
+// Store one staged line (opos layout) to contiguous global memory: 64-element chunks, pointer
+// increments only; the optional |v| max is a template switch (no work when it is off).
+template <bool AMAX>
+PD_DEV void store_line(const double* __restrict__ ob, double* __restrict__ d, int nel, int lane, double& lmax) {
+  int q0 = 0;
+  d += lane;
+  ob += lane;
+  for (; q0 + 64 <= nel; q0 += 64, ob += 65, d += 64) {
+    const double v0 = ob[0], v1 = ob[32];
+    d[0] = v0;
+    d[32] = v1;
+    if (AMAX) lmax = amax_acc(amax_acc(lmax, v0), v1);
+  }
+  for (int r = 0; q0 + lane + r < nel; r += 32) {
+    const double v = ob[r];
+    d[r] = v;
+    if (AMAX) lmax = amax_acc(lmax, v);
+  }
+}
+
+// Fused defect-correction update for the last pass (linear kinds, ω = 1): U_line += δ_line with
+// δ taken from the staged line (never written to HBM), ‖δ‖∞ and ‖U‖∞ (NaN-safe bit max).  The
+// whole U line is loaded into registers first (the transform's registers are dead by now), so
+// all of its loads are in flight together.
+template <int MAXJ>
+PD_DEV void update_line(const double* __restrict__ ob, double* __restrict__ U, int nel, int lane, double& dmax,
+                        unsigned long long& ubits) {
+  double uv[MAXJ];
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) {
+    const int q = lane + 32 * j;
+    uv[j] = q < nel ? U[q] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) {
+    const int q = lane + 32 * j;
+    if (q < nel) {
+      const double d = ob[q + (j >> 1)];          // opos(q): (lane + 32j) >> 6 == j >> 1
+      const double u = uv[j] + d;
+      U[q] = u;
+      dmax = amax_acc(dmax, d);
+      ubits = max(ubits, (unsigned long long)__double_as_longlong(u) & 0x7fffffffffffffffull);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- rows (contiguous lines)
 // Warps are independent: each takes P consecutive lines per step, prefetches its next group into
 // L2, stages the lines with cp.async, transforms and stores them coalesced.
@@ -149,6 +195,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* xb = reinterpret_cast<double*>(smem2) + (size_t)warp * D::BUF;
   double lmax = 0.0;
+  unsigned long long ubits = 0ull;
   const int64_t ngroups = (L.nlines + D::P - 1) / D::P;
   const int64_t gstride = (int64_t)gridDim.x * NW;
   const double* in_end = in + L.nlines * L.nx;
@@ -163,7 +210,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     const int64_t rem = L.nlines - L0;
     const int nl = rem < D::P ? (int)rem : D::P;
     const double* src = in + L0 * L.nx;
-    if (lane == 0 && g + gstride < ngroups)
+    if ((L.tune & 1) && lane == 0 && g + gstride < ngroups)
       bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
@@ -188,18 +235,18 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
-        const double* ob = xb + p * D::LDO;
-        double* d = dst + p * L.nx;
-        for (int q = lane; q < L.nel; q += 32) {
-          const double v = ob[D::opos(q)];
-          d[q] = v;
-          lmax = fmax(lmax, fabs(v));
-        }
+        if (L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
+        else if (L.amax) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
+        else store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
       }
     }
     __syncwarp();
   }
   if (L.amax) warp_atomic_max_abs(L.amax, lmax);
+  if (L.upd) {
+    ubits = warp_max_u64(ubits);
+    if (lane == 0 && ubits) atomicMax(L.umax, ubits);
+  }
 }
 
 // ---------------------------------------------------------------- columns (stride nx)
@@ -228,22 +275,37 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     double* dst = out + n * L.ns + x0;
     {
       const int64_t Gn = G + gridDim.x;
-      if (Gn < ngroups) {
+      if ((L.tune & 2) && Gn < ngroups) {
         const int64_t nn = Gn / gx;
         const int xn = (int)((Gn - nn * gx) * C);
         const int wn = min(C, (int)(L.nx - xn));
         const double* s = in + nn * L.ns + xn;
-        for (int e = threadIdx.x; e < L.nel; e += NTH) {
-          prefetch_l2(s + (int64_t)e * L.nx);
-          prefetch_l2(s + (int64_t)e * L.nx + wn - 1);
+        const double* lim = in + L.nlines * L.nx;
+        if (L.tune & 8) {      // one bulk prefetch per row segment, lane 0 of each warp
+          if (lane == 0)
+            for (int e = warp; e < L.nel; e += NW) bulk_prefetch_l2(s + (int64_t)e * L.nx, (size_t)wn * 8, lim);
+        } else {
+          for (int e = threadIdx.x; e < L.nel; e += NTH) {
+            prefetch_l2(s + (int64_t)e * L.nx);
+            prefetch_l2(s + (int64_t)e * L.nx + wn - 1);
+          }
         }
       }
     }
-    for (int i = threadIdx.x; i < L.nel * C; i += NTH) {
-      const int e = i / C, c = i - e * C;
-      if (c < wcols) {
-        const int w = c / D::P, p = c - w * D::P;
-        cp_async8(base + (size_t)w * D::BUF + p * D::LDX + bidx<NEUMANN>(e), src + (int64_t)e * L.nx + c);
+    // thread -> fixed column c = tid % C, rows e = tid / C + k·(NTH / C): pointer increments only
+    constexpr int RSTEP = NTH / C;
+    static_assert(64 % RSTEP == 0, "row step must divide 64");
+    constexpr int PER = 64 / RSTEP;
+    const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
+    const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
+    if (c_t < wcols) {
+      double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
+      const double* s = src + (int64_t)e_t * L.nx + c_t;
+      const int64_t rstride = (int64_t)RSTEP * L.nx;
+      for (int e0 = e_t; e0 < L.nel; e0 += 64, lb += 64, s += 64 * L.nx) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+          if (e0 + j * RSTEP < L.nel) cp_async8(lb + j * RSTEP, s + j * rstride);
       }
     }
     cp_async_commit();
@@ -257,13 +319,26 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     __syncthreads();
     D::transform(xb, L, trig2, lane);
     __syncthreads();
-    for (int i = threadIdx.x; i < L.nel * C; i += NTH) {
-      const int e = i / C, c = i - e * C;
-      if (c < wcols) {
-        const int w = c / D::P, p = c - w * D::P;
-        const double v = base[(size_t)w * D::BUF + p * D::LDO + D::opos(e)];
-        dst[(int64_t)e * L.nx + c] = v;
-        lmax = fmax(lmax, fabs(v));
+    if (c_t < wcols) {
+      const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
+      double* d = dst + (int64_t)e_t * L.nx + c_t;
+      const int64_t rstride = (int64_t)RSTEP * L.nx;
+      if (L.amax) {
+        for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65, d += 64 * L.nx) {
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            if (e0 + j * RSTEP < L.nel) {
+              const double v = ob[j * RSTEP];
+              d[j * rstride] = v;
+              lmax = amax_acc(lmax, v);
+            }
+        }
+      } else {
+        for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65, d += 64 * L.nx) {
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            if (e0 + j * RSTEP < L.nel) d[j * rstride] = ob[j * RSTEP];
+        }
       }
     }
     __syncthreads();

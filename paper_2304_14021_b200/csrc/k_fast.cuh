@@ -31,12 +31,38 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   double lmax = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t s0 = tile * S;
-    for (int i = threadIdx.x; i < NT * S; i += NW * 32) {
-      const int t = i / S, c = i - t * S;
-      const int64_t s = s0 + c;
-      double* d = sm + t * LD + c;
-      if (s < P.ns) cp_async8(d, in + (size_t)t * P.ns + s);
-      else *d = 0.0;
+    if ((P.tune & 4) && tile + gridDim.x < ntiles) {      // (tune bit 2) L2 prefetch of the CTA's next tile (k_dtt.cuh)
+      const int64_t sn = s0 + (int64_t)gridDim.x * S;
+      const int64_t last = min((int64_t)S, P.ns - sn) - 1;
+      if (P.tune & 8) {
+        if (lane == 0)
+          for (int t = warp; t < NT; t += NW)
+            bulk_prefetch_l2(in + (size_t)t * P.ns + sn, (size_t)(last + 1) * 8, in + (size_t)NT * P.ns);
+      } else {
+        for (int t = threadIdx.x; t < NT; t += NW * 32) {
+          prefetch_l2(in + (size_t)t * P.ns + sn);
+          prefetch_l2(in + (size_t)t * P.ns + sn + last);
+        }
+      }
+    }
+    // thread -> fixed point c = tid % S, slices t = tid / S + k·TSTEP: pointer increments only
+    // (tiles wider than the CTA, S > 32·NW, only occur for N_t = 32: threads take S/(32·NW) points)
+    constexpr int CPT = S > NW * 32 ? S / (NW * 32) : 1;          // points per thread
+    constexpr int TSTEP = CPT > 1 ? 1 : NW * 32 / S;
+    static_assert(CPT == 1 || S % (NW * 32) == 0, "tile width");
+    const int c_t = CPT > 1 ? threadIdx.x : threadIdx.x % S, t_t = CPT > 1 ? 0 : threadIdx.x / S;
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = c_t + cc * NW * 32;
+      const bool live = s0 + c < P.ns;
+      double* d = sm + t_t * LD + c;
+      const double* g = in + (size_t)t_t * P.ns + s0 + c;
+      const size_t gstep = (size_t)TSTEP * P.ns;
+#pragma unroll 4
+      for (int t = t_t; t < NT; t += TSTEP, d += TSTEP * LD, g += gstep) {
+        if (live) cp_async8(d, g);
+        else *d = 0.0;
+      }
     }
     cp_async_commit();
     cp_async_wait_all();
@@ -91,13 +117,23 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < NT * S; i += NW * 32) {
-      const int t = i / S, c = i - t * S;
-      const int64_t s = s0 + c;
-      if (s < P.ns) {
-        const double x = sm[t * LD + c];
-        out[(size_t)t * P.ns + s] = x;
-        lmax = fmax(lmax, fabs(x));
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = c_t + cc * NW * 32;
+      if (s0 + c >= P.ns) continue;
+      const double* d = sm + t_t * LD + c;
+      double* g = out + (size_t)t_t * P.ns + s0 + c;
+      const size_t gstep = (size_t)TSTEP * P.ns;
+      if (P.amax) {
+#pragma unroll 4
+        for (int t = t_t; t < NT; t += TSTEP, d += TSTEP * LD, g += gstep) {
+          const double x = *d;
+          *g = x;
+          lmax = amax_acc(lmax, x);
+        }
+      } else {
+#pragma unroll 4
+        for (int t = t_t; t < NT; t += TSTEP, d += TSTEP * LD, g += gstep) *g = *d;
       }
     }
     __syncthreads();

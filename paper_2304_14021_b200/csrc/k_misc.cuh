@@ -16,7 +16,10 @@ k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, Dev
          int damped, double omega_cap, double tau) {
   const double w = stats_omega(st, damped, omega_cap, tau);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->omega = w;
-  double lmax = 0.0;
+  // ‖U‖∞ as a max over |u| bit patterns: NaN sorts above +inf, so a non-finite iterate always
+  // reaches the host check (the ‖δ‖∞ epilogues of the line passes do not propagate NaN)
+  unsigned long long lbits = 0ull;
+  const unsigned long long absmask = 0x7fffffffffffffffull;
   const size_t n2 = n / 2;
   double2* U2 = reinterpret_cast<double2*>(U);
   const double2* D2 = reinterpret_cast<const double2*>(delta);
@@ -26,14 +29,17 @@ k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, Dev
     u.x += w * d.x;
     u.y += w * d.y;
     U2[i] = u;
-    lmax = fmax(lmax, fmax(fabs(u.x), fabs(u.y)));
+    const unsigned long long bx = (unsigned long long)__double_as_longlong(u.x) & absmask;
+    const unsigned long long by = (unsigned long long)__double_as_longlong(u.y) & absmask;
+    lbits = max(lbits, max(bx, by));
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const double u = U[n - 1] + w * delta[n - 1];
     U[n - 1] = u;
-    lmax = fmax(lmax, fabs(u));
+    lbits = max(lbits, (unsigned long long)__double_as_longlong(u) & absmask);
   }
-  warp_atomic_max_abs(&st->umax_bits, lmax);
+  lbits = warp_max_u64(lbits);
+  if ((threadIdx.x & 31) == 0 && lbits) atomicMax(&st->umax_bits, lbits);
 }
 
 // U⁰: broadcast u0 to every time slice, or zero (R#5).
@@ -46,6 +52,7 @@ __global__ void k_init_iterate(double* __restrict__ U, const double* __restrict_
 __global__ void k_reset_stats(DevStats* st) {
   st->dmax_bits = 0ull;
   st->umax_bits = 0ull;
+  st->omega = 1.0;      // the fused x-inverse + update pass (linear kinds) applies ω = 1
 }
 
 __global__ void k_set_jbar(DevStats* st, double jbar) { st->jbar = jbar; }

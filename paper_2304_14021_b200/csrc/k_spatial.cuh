@@ -33,6 +33,9 @@ struct LineParams {
   const double2* tw;     // FFT twiddles exp(-2πik/2^twlog)
   int twlog;
   unsigned long long* amax;   // optional: max |out| (NULL = off)
+  int tune;              // PARADIAG_TUNE bits (A/B switches for measurements; 0 = defaults)
+  double* upd;           // k_rows3 only: fused update U += out (out not stored), NULL = off
+  unsigned long long* umax;   // with upd: max |U| after the update (bit-pattern max, NaN-safe)
 };
 
 // buffer index of stored element e: Neumann x_e = node e; hinged x_{e+1} = interior node e+1

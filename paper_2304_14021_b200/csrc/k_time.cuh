@@ -31,6 +31,7 @@ struct TimeParams {
   const double2* tw;
   int twlog;
   unsigned long long* amax;   // optional max |out|
+  int tune;                   // PARADIAG_TUNE bits (A/B switches for measurements; 0 = defaults)
 };
 
 PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {

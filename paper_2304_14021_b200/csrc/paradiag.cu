@@ -23,8 +23,7 @@
 #include "k_residual.cuh"
 #include "k_spatial.cuh"
 #include "k_time.cuh"
-#include "k_fast.cuh"
-#include "k_dtt.cuh"
+#include "fast_launch.cuh"
 
 using namespace pd;
 
@@ -53,16 +52,11 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
-                K_TFWD1D, K_PENTA, K_TINV1D, PD_NKERNELS };
+                K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
-                                         "time_fwd_1d", "penta_solve", "time_inv_1d"};
+                                         "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update"};
 
-constexpr int kFastTimeWarps = 4;  // register-FFT time pass (k_time2d_v2)
-constexpr int kFastRowWarps = 4;   // register-FFT rows
-// register-FFT columns: warps per CTA so that C = warps·32/E columns stays ≤ 64 (SMEM for the
-// [66][C] output staging) — E = transform length / 32
-constexpr int fast_col_warps(int E) { return E == 1 ? 2 : E == 2 ? 4 : 8; }
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr int kTime1DWarps = 4;
 constexpr int kLineWarps = 4;   // spatial DTT rows: one warp per row, 4 rows per CTA
@@ -103,6 +97,7 @@ struct pd_handle {
   double2* trig = nullptr;
   double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
   int dtt_ver = 3;                    // line kernels: 3 = k_dtt.cuh, 2 = k_fast.cuh
+  int tune = 0;                       // PARADIAG_TUNE: A/B switches for measurements
   double* band = nullptr;
   double2* fac = nullptr;             // 4 x [nx][nb]
   DevStats* st = nullptr;
@@ -202,43 +197,18 @@ int allow_smem(K kernel, size_t bytes) {
 }
 
 size_t time_smem(int nt, int warps) { return (size_t)warps * padded16(nt) * sizeof(double2); }
-size_t fast_time_smem(int E) {
-  const size_t S = 2 * (32 / E) * kFastTimeWarps, tile = (size_t)32 * E * (S + 1);
-  return std::max(tile, (size_t)kFastTimeWarps * kWarpBufD) * sizeof(double);
-}
-size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
-size_t fast_cols_smem(int E) {
-  const size_t nw = fast_col_warps(E);
-  return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
-}
-template <int E>
-size_t dtt3_rows_smem() { return (size_t)kFastRowWarps * Dtt3<1, E>::BUF * sizeof(double); }
-template <int E>
-size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * sizeof(double); }
 size_t rows_smem(int M) { return (size_t)kLineWarps * dpadded(M) * sizeof(double); }
 size_t cols_smem(int M) { return ((size_t)kColW * dpadded(M) + 66 * kColW) * sizeof(double); }
 
 // ----------------------------------------------------------------------------- launches
-template <int E>
-int fast_attrs_e() {
-  PD_CUDA(cudaFuncSetAttribute(k_time2d_v2<E, kFastTimeWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_time_smem(E)));
-  PD_CUDA(cudaFuncSetAttribute(k_rows_v2<1, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_rows_smem()));
-  PD_CUDA(cudaFuncSetAttribute(k_rows_v2<0, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_rows_smem()));
-  PD_CUDA(cudaFuncSetAttribute(k_cols_v2<1, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
-  PD_CUDA(cudaFuncSetAttribute(k_cols_v2<0, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_cols_smem(E)));
-  PD_CUDA(cudaFuncSetAttribute(k_rows3<1, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_rows_smem<E>()));
-  PD_CUDA(cudaFuncSetAttribute(k_rows3<0, E, kFastRowWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_rows_smem<E>()));
-  PD_CUDA(cudaFuncSetAttribute(k_cols3<1, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_cols_smem<E>()));
-  PD_CUDA(cudaFuncSetAttribute(k_cols3<0, E, fast_col_warps(E)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtt3_cols_smem<E>()));
-  return PD_OK;
-}
-
 int setup_fast_attrs(pd_handle* h) {
   if (!h->fast) return PD_OK;
-  int rc;
-  if ((rc = fast_attrs_e<1>()) || (rc = fast_attrs_e<2>()) || (rc = fast_attrs_e<4>()) || (rc = fast_attrs_e<8>()) ||
-      (rc = fast_attrs_e<16>()) || (rc = fast_attrs_e<32>()))
-    return rc;
+  PD_CUDA(fast_attrs<1>());
+  PD_CUDA(fast_attrs<2>());
+  PD_CUDA(fast_attrs<4>());
+  PD_CUDA(fast_attrs<8>());
+  PD_CUDA(fast_attrs<16>());
+  PD_CUDA(fast_attrs<32>());
   return PD_OK;
 }
 
@@ -267,7 +237,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   return PD_OK;
 }
 
-LineParams line_params(pd_handle* h, int axis, unsigned long long* amax) {
+LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double* upd = nullptr) {
   LineParams L;
   L.nlines = (int64_t)h->P.nt * (axis == 0 ? h->ny : h->nx);
   L.nx = h->nx;
@@ -275,55 +245,37 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax) {
   L.nel = h->nx;
   L.M = (int)h->P.m; L.log2h = h->log2h; L.trig = h->trig; L.tw = h->tw; L.twlog = h->twlog;
   L.amax = amax;
+  L.tune = h->tune;
+  L.upd = upd;
+  L.umax = upd ? &h->st->umax_bits : nullptr;
   return L;
 }
 
-template <int NEUMANN, int E>
-void launch_fast_line(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
-  if (h->dtt_ver == 3) {
-    if (axis == 0) {
-      const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
-      const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
-      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, dtt3_rows_smem<E>(), h->stream>>>(in, out, L, h->trig2);
-    } else {
-      constexpr int NW = fast_col_warps(E);
-      const int C = NW * (32 / E);
-      const int64_t groups = (int64_t)h->P.nt * ((h->nx + C - 1) / C);
-      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
-      k_cols3<NEUMANN, E, NW><<<grid, NW * 32, dtt3_cols_smem<E>(), h->stream>>>(in, out, L, h->trig2);
-    }
-    return;
-  }
-  if (axis == 0) {
-    const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
-    const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 16);
-    k_rows_v2<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, fast_rows_smem(), h->stream>>>(in, out, L);
-  } else {
-    constexpr int NW = fast_col_warps(E);
-    const int C = NW * (32 / E);
-    const int64_t groups = (int64_t)h->P.nt * ((h->nx + C - 1) / C);
-    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 16);
-    k_cols_v2<NEUMANN, E, NW><<<grid, NW * 32, fast_cols_smem(E), h->stream>>>(in, out, L);
-  }
+FastLaunch fast_launch(pd_handle* h) {
+  FastLaunch F;
+  F.stream = h->stream; F.nt = h->P.nt; F.nx = h->nx; F.ns = h->ns; F.trig2 = h->trig2; F.dtt_ver = h->dtt_ver;
+  return F;
 }
 
-template <int NEUMANN>
-bool fast_line(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
+bool fast_line_any(pd_handle* h, const double* in, double* out, int axis, const LineParams& L) {
+  const FastLaunch F = fast_launch(h);
+  const int nm = h->neumann ? 1 : 0;
   switch (L.M) {
-    case 64: launch_fast_line<NEUMANN, 1>(h, in, out, axis, L); return true;
-    case 128: launch_fast_line<NEUMANN, 2>(h, in, out, axis, L); return true;
-    case 256: launch_fast_line<NEUMANN, 4>(h, in, out, axis, L); return true;
-    case 512: launch_fast_line<NEUMANN, 8>(h, in, out, axis, L); return true;
-    case 1024: launch_fast_line<NEUMANN, 16>(h, in, out, axis, L); return true;
-    case 2048: launch_fast_line<NEUMANN, 32>(h, in, out, axis, L); return true;
+    case 64: fast_line<1>(nm, axis, in, out, L, F); return true;
+    case 128: fast_line<2>(nm, axis, in, out, L, F); return true;
+    case 256: fast_line<4>(nm, axis, in, out, L, F); return true;
+    case 512: fast_line<8>(nm, axis, in, out, L, F); return true;
+    case 1024: fast_line<16>(nm, axis, in, out, L, F); return true;
+    case 2048: fast_line<32>(nm, axis, in, out, L, F); return true;
     default: return false;
   }
 }
 
-int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid) {
-  LineParams L = line_params(h, axis, amax);
+int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid,
+                 double* upd = nullptr) {
+  LineParams L = line_params(h, axis, amax, upd);
   prof_begin(h, kid);
-  const bool fast = h->fast && (h->neumann ? fast_line<1>(h, in, out, axis, L) : fast_line<0>(h, in, out, axis, L));
+  const bool fast = h->fast && fast_line_any(h, in, out, axis, L);
   if (!fast) {
     if (axis == 0) {
       const unsigned grid = (unsigned)((L.nlines + kLineWarps - 1) / kLineWarps);
@@ -343,23 +295,16 @@ int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned
   return PD_OK;
 }
 
-template <int E>
-void launch_fast_time(pd_handle* h, const double* in, double* out, const TimeParams& T) {
-  constexpr int S = 2 * (32 / E) * kFastTimeWarps;
-  const int64_t tiles = (h->ns + S - 1) / S;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
-  k_time2d_v2<E, kFastTimeWarps><<<grid, kFastTimeWarps * 32, fast_time_smem(E), h->stream>>>(in, out, T);
-}
-
-bool fast_time(pd_handle* h, const double* in, double* out, const TimeParams& T) {
+bool fast_time_any(pd_handle* h, const double* in, double* out, const TimeParams& T) {
   if (!h->fast) return false;
+  const FastLaunch F = fast_launch(h);
   switch (h->P.nt) {
-    case 32: launch_fast_time<1>(h, in, out, T); return true;
-    case 64: launch_fast_time<2>(h, in, out, T); return true;
-    case 128: launch_fast_time<4>(h, in, out, T); return true;
-    case 256: launch_fast_time<8>(h, in, out, T); return true;
-    case 512: launch_fast_time<16>(h, in, out, T); return true;
-    case 1024: launch_fast_time<32>(h, in, out, T); return true;
+    case 32: fast_time<1>(in, out, T, F); return true;
+    case 64: fast_time<2>(in, out, T, F); return true;
+    case 128: fast_time<4>(in, out, T, F); return true;
+    case 256: fast_time<8>(in, out, T, F); return true;
+    case 512: fast_time<16>(in, out, T, F); return true;
+    case 1024: fast_time<32>(in, out, T, F); return true;
     default: return false;
   }
 }
@@ -369,11 +314,22 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   T.nt = h->P.nt; T.log2nt = h->log2nt; T.ns = h->ns; T.nx = h->nx;
   T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.lamx = h->lam;
   T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
-  T.tw = h->tw; T.twlog = h->twlog; T.amax = amax;
+  T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune;
   return T;
 }
 
-int precond(pd_handle* h, const double* r, double* delta) {
+// The last 2D pass (x-inverse, rows) can apply the update U += δ itself (k_rows3 epilogue): only
+// the register-FFT v3 line kernels implement it.
+bool can_fuse_update(const pd_handle* h) {
+  // measured (d3f/d3g): the epilogue's U loads are exposed in the latency-bound line kernel, so the
+  // fused pass (20.4 ms) loses to x-inverse + streaming update (10.3 + 8.2 ms) — opt-in (tune 16)
+  return (h->tune & 16) && h->P.dim == 2 && h->P.kind != PD_CAHN_HILLIARD && h->fast && h->dtt_ver == 3 && h->P.m >= 64 &&
+         h->P.m <= 2048;
+}
+
+// δ = P_α⁻¹ r; with U_fused != NULL (can_fuse_update) the last pass adds δ to U_fused instead of
+// storing δ (‖δ‖∞ and ‖U‖∞ reduced on the way).
+int precond(pd_handle* h, const double* r, double* delta, double* U_fused = nullptr) {
   unsigned long long* dmax = &h->st->dmax_bits;
   if (h->P.dim == 2) {
     int rc;
@@ -382,11 +338,12 @@ int precond(pd_handle* h, const double* r, double* delta) {
     TimeParams T = time_params(h, nullptr);
     const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
     prof_begin(h, K_TIME);
-    if (!fast_time(h, delta, delta, T))
+    if (!fast_time_any(h, delta, delta, T))
       k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV))) return rc;
+    if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
     if ((rc = launch_lines(h, delta, delta, 0, dmax, K_XINV))) return rc;
     return PD_OK;
   }
@@ -435,8 +392,12 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
   if ((rc = launch_residual(h, u0, U, h->work))) return rc;
-  if ((rc = precond(h, h->work, h->work))) return rc;
-  if ((rc = launch_update(h, U, h->work))) return rc;
+  if (can_fuse_update(h)) {
+    if ((rc = precond(h, h->work, h->work, U))) return rc;
+  } else {
+    if ((rc = precond(h, h->work, h->work))) return rc;
+    if ((rc = launch_update(h, U, h->work))) return rc;
+  }
   PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
   PD_CUDA(cudaStreamSynchronize(h->stream));
   prof_collect(h);
@@ -658,6 +619,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
+    if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
@@ -768,7 +730,7 @@ int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd
 
 int paradiag_launches_per_iteration(const pd_handle* h) {
   if (!h) return 0;
-  int n = 1 /*reset*/ + 1 /*residual*/ + 1 /*update*/;
+  int n = 1 /*reset*/ + 1 /*residual*/ + (can_fuse_update(h) ? 0 : 1) /*update*/;
   n += h->P.dim == 2 ? 5 : 3;
   if (h->P.kind == PD_CAHN_HILLIARD) n += 1;
   return n;

@@ -4,7 +4,7 @@ tag=${1:-q}; mode=${2:-parity}
 mkdir -p gpurun_out
 if [ "$mode" != "bench" ]; then
   T=tests/test_gpu_parity.py; [ "$mode" = "full" ] && T="tests/test_gpu_parity.py tests/test_gpu_fullsize.py"
-  timeout 900 python -m pytest $T -m gpu -x -q > gpurun_out/${tag}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${tag}_tests.log
+  timeout 420 python -m pytest $T -m gpu -x -q > gpurun_out/${tag}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${tag}_tests.log
   tail -4 gpurun_out/${tag}_tests.log
 fi
 timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_bench.log 2>&1; echo "bench rc=$?"
