@@ -256,3 +256,135 @@ k_residual_2d(const double* __restrict__ u0, const double* __restrict__ U, doubl
 }
 
 }  // namespace pd
+
+namespace pd {
+
+// ------------------------------------------------------------------------------------------
+// 2D residual, tiled and time-marching (v2).  ncu r01b: the row-streaming kernel above issued 5.5
+// warp instructions per point (ring indexing, per-row BC maps, two barriers per row).  Here a CTA
+// owns a TY x TX output tile and marches over a chunk of time slices n0..n1-1:
+//   * the BC-extended tile of U_n (2-point halo; the even/odd extension signs of ext_map, hence the
+//     same nested ghost rules R#14/R#15) is staged with cp.async into one of two buffers while the
+//     previous slice computes — the per-element source offsets and signs are computed once;
+//   * U_{n-1} at the tile's outputs is kept in registers from the previous slice (only the chunk's
+//     first slice reads it from global), so U is read from HBM once;
+//   * inner values L(u) (CH: v = u³ - u - ε²L(u)) on the 1-point-haloed tile go to shared memory,
+//     then the outer stencil and the time difference.  Arithmetic and evaluation order are those of
+//     k_residual_2d.
+constexpr int kResTX = 64, kResTY = 32, kResThreads = 256, kResChunk = 32;
+constexpr int kResUX = kResTX + 4, kResUY = kResTY + 4;     // staged U tile
+constexpr int kResIX = kResTX + 2, kResIY = kResTY + 2;     // inner-value tile
+constexpr int kResUP = kResUX + 1, kResIP = kResIX + 1;     // pitches (odd: conflict-free columns)
+constexpr int kResUN = kResUY * kResUX;                     // staged elements
+constexpr int kResPer = (kResUN + kResThreads - 1) / kResThreads;
+constexpr int kResOut = kResTY * kResTX / kResThreads;      // outputs per thread
+constexpr size_t kResSmem = (2 * (size_t)kResUY * kResUP + (size_t)kResIY * kResIP) * sizeof(double);
+
+__global__ void __launch_bounds__(kResThreads)
+k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
+                ResidualParams P, double* __restrict__ jpart) {
+  extern __shared__ double2 smem2[];
+  double* const sU0 = reinterpret_cast<double*>(smem2);
+  double* const sU1 = sU0 + kResUY * kResUP;
+  double* const sI = sU1 + kResUY * kResUP;
+  __shared__ double wsum[kResThreads / 32];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * kResTX, y0 = blockIdx.y * kResTY;
+  const int n0 = blockIdx.z * kResChunk, n1 = min(n0 + kResChunk, P.nt);
+  const size_t ns = (size_t)P.nx * P.ny;
+  const bool ch = P.kind == 2;
+  // staging map (slice independent): element k of this thread -> smem slot, source offset, sign
+  int soff[kResPer], dpos[kResPer];
+  double sgn[kResPer];
+#pragma unroll
+  for (int k = 0; k < kResPer; ++k) {
+    const int i = tid + k * kResThreads;
+    const int ry = i / kResUX, rx = i - ry * kResUX;
+    int cy = 0, cx = 0;
+    double sy = 0.0, sg = 0.0;
+    if (i < kResUN) {
+      ext_map(y0 - 2 + ry, P.ny, P.neumann, cy, sy);
+      ext_map(x0 - 2 + rx, P.nx, P.neumann, cx, sg);
+    }
+    soff[k] = i < kResUN ? cy * P.nx + cx : -1;
+    dpos[k] = ry * kResUP + rx;
+    sgn[k] = sy * sg;
+  }
+  auto stage = [&](double* dst, int n) {
+#pragma unroll
+    for (int k = 0; k < kResPer; ++k)
+      if (soff[k] >= 0) cp_async8(dst + dpos[k], U + (size_t)n * ns + soff[k]);
+    cp_async_commit();
+  };
+  auto fix_signs = [&](double* dst) {     // hinged: odd extension (own elements only)
+    if (!P.neumann) {
+#pragma unroll
+      for (int k = 0; k < kResPer; ++k)
+        if (soff[k] >= 0) dst[dpos[k]] *= sgn[k];
+    }
+  };
+  // outputs of this thread: column tx, rows ty = tid / TX + 4j
+  const int tx = tid % kResTX, ty0 = tid / kResTX;
+  const int gx = x0 + tx;
+  double prev[kResOut];
+  {
+    const double* sp = n0 == 0 ? u0 : U + (size_t)(n0 - 1) * ns;
+#pragma unroll
+    for (int j = 0; j < kResOut; ++j) {
+      const int gy = y0 + ty0 + j * (kResThreads / kResTX);
+      prev[j] = (gx < P.nx && gy < P.ny) ? __ldg(sp + (size_t)gy * P.nx + gx) : 0.0;
+    }
+  }
+  double jloc = 0.0;
+  stage(sU0, n0);
+  for (int n = n0; n < n1; ++n) {
+    double* cur = ((n - n0) & 1) ? sU1 : sU0;
+    double* nxt = ((n - n0) & 1) ? sU0 : sU1;
+    cp_async_wait_all();
+    fix_signs(cur);
+    __syncthreads();                       // cur staged; previous slice done with nxt and sI
+    if (n + 1 < n1) stage(nxt, n + 1);
+    for (int i = tid; i < kResIY * kResIX; i += kResThreads) {
+      const int iy = i / kResIX, ix = i - iy * kResIX;
+      const double* c = cur + (iy + 1) * kResUP + (ix + 1);
+      const double uc = c[0];
+      const double Lr = ((c[-1] + c[1]) + (c[-kResUP] + c[kResUP]) - 4.0 * uc) * P.inv_h2;
+      sI[iy * kResIP + ix] = ch ? uc * uc * uc - uc - P.e2 * Lr : Lr;
+    }
+    __syncthreads();
+    double* rn = r + (size_t)n * ns;
+#pragma unroll
+    for (int j = 0; j < kResOut; ++j) {
+      const int ty = ty0 + j * (kResThreads / kResTX);
+      const int gy = y0 + ty;
+      const double* I = sI + (ty + 1) * kResIP + (tx + 1);
+      const double uo = cur[(ty + 2) * kResUP + (tx + 2)];
+      if (gx < P.nx && gy < P.ny) {
+        const double outer = ((I[-1] + I[1]) + (I[-kResIP] + I[kResIP]) - 4.0 * I[0]) * P.inv_h2;
+        const double dtime = (uo - prev[j]) * P.inv_dt;
+        double out;
+        if (ch) {
+          out = outer - dtime;
+          jloc += 3.0 * uo * uo - 1.0;
+        } else {
+          const double Au = P.kind == 0 ? outer : P.b2 * I[0] + P.e2 * outer;
+          out = -dtime - Au;
+        }
+        rn[(size_t)gy * P.nx + gx] = out;
+      }
+      prev[j] = uo;
+    }
+  }
+  if (ch) {
+    const double v = warp_sum(jloc);
+    if ((tid & 31) == 0) wsum[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kResThreads / 32; ++w) t += wsum[w];
+      jpart[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+}  // namespace pd

@@ -218,9 +218,17 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
   prof_begin(h, K_RESIDUAL);
+  size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
   if (h->P.dim == 2) {
-    dim3 grd((h->nx + kResStrip - 1) / kResStrip, h->P.nt);
-    k_residual_2d<<<grd, 128, 0, h->stream>>>(u0, U, r, R, h->jpart);
+    if (h->tune & 32) {     // previous row-streaming kernel (A/B)
+      dim3 grd((h->nx + kResStrip - 1) / kResStrip, h->P.nt);
+      k_residual_2d<<<grd, 128, 0, h->stream>>>(u0, U, r, R, h->jpart);
+      nparts = (size_t)grd.x * grd.y;
+    } else {
+      dim3 grd((h->nx + kResTX - 1) / kResTX, (h->ny + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
+      k_residual_tile<<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      nparts = (size_t)grd.x * grd.y * grd.z;
+    }
   } else {
     dim3 blk(256, 1);
     dim3 grd((h->nx + blk.x - 1) / blk.x, 1, h->P.nt);
@@ -230,7 +238,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   PD_LAUNCHED();
   if (h->P.kind == PD_CAHN_HILLIARD) {
     prof_begin(h, K_JBAR);
-    k_jbar_finalize<<<1, 1024, 0, h->stream>>>(h->jpart, h->njpart, 1.0 / (double)h->total, h->st);
+    k_jbar_finalize<<<1, 1024, 0, h->stream>>>(h->jpart, nparts, 1.0 / (double)h->total, h->st);
     prof_end(h, K_JBAR);
     PD_LAUNCHED();
   }
@@ -563,7 +571,9 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     if (e != cudaSuccess) return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
   }
   if (p->kind == PD_CAHN_HILLIARD) {
-    h->njpart = (size_t)((h->nx + kResStrip - 1) / kResStrip) * nt;
+    h->njpart = std::max((size_t)((h->nx + kResStrip - 1) / kResStrip) * nt,
+                         (size_t)((h->nx + kResTX - 1) / kResTX) * ((h->ny + kResTY - 1) / kResTY) *
+                             ((nt + kResChunk - 1) / kResChunk));
     PD_TRY(dalloc(h, &h->jpart, h->njpart));
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
@@ -617,6 +627,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
+    PD_TRY(allow_smem(k_residual_tile, kResSmem));
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
