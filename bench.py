@@ -10,8 +10,11 @@ flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
 
-Multi-GPU (torchrun): round 1 runs independent replicas per rank (weak scaling); the sharded
-all-to-all path is DESIGN.md §8 "next".
+Multi-GPU (torchrun, N > 1): the c5 grid is sharded in slabs over the ranks (paper_2304_14021_b200/
+dist.py) — row slabs for the residual / x transforms / update, column slabs for the y
+transforms and the time pass, NCCL all-to-all transposes between them and a 2-row residual halo —
+so the total problem is fixed (strong scaling).  --parallelism replicas runs N independent copies
+instead (weak scaling).
 """
 import argparse
 import json
@@ -115,6 +118,146 @@ def time_oracle(name, steps, warmup):
     return p.dofs / dt, cores, desc, dt
 
 
+class EventTimer:
+    """Device time of code regions (collectives) on the launching stream, summed per name."""
+
+    def __init__(self, stream):
+        import torch
+        self.torch, self.stream, self.pending, self.tot, self.cnt = torch, stream, [], {}, {}
+
+    def __call__(self, name):
+        timer = self
+
+        class _Ctx:
+            def __enter__(self_):
+                self_.e0 = timer.torch.cuda.Event(enable_timing=True)
+                self_.e1 = timer.torch.cuda.Event(enable_timing=True)
+                self_.e0.record(timer.stream)
+
+            def __exit__(self_, *a):
+                self_.e1.record(timer.stream)
+                timer.pending.append((name, self_.e0, self_.e1))
+                return False
+        return _Ctx()
+
+    def collect(self):
+        self.torch.cuda.synchronize()
+        for name, e0, e1 in self.pending:
+            self.tot[name] = self.tot.get(name, 0.0) + e0.elapsed_time(e1)
+            self.cnt[name] = self.cnt.get(name, 0) + 1
+        self.pending = []
+        return {k: self.tot[k] / self.cnt[k] for k in self.tot}
+
+
+def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
+    """c5 (or any 2D linear config) sharded over the ranks: one SlabRank per process, NCCL
+    collectives (strong scaling: the whole problem is fixed, value = total dofs / max-rank time)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2304_14021_b200 as pd
+    from paper_2304_14021_b200 import dist as pdist
+    L = pdist.SlabLayout(p.n, p.nt, world)
+    y0, nyl = L.rows[rank]
+    x0, nxl = L.cols[rank]
+    ops = pdist.GpuOps(p, local, stream.cuda_stream, y0, nyl, x0, nxl)
+    rk = pdist.SlabRank(L, rank, ops)
+    comm = pdist.TorchComm()
+    u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).to(dev)
+
+    def fresh_U():
+        if p.init == "zero":
+            return torch.zeros(L.row_slab(rank), dtype=torch.float64, device=dev)
+        return u0_l.reshape(1, nyl, p.n).expand(p.nt, nyl, p.n).contiguous().reshape(-1)
+
+    U_l = fresh_U()
+    for _ in range(args.warmup):
+        rk.iterate(u0_l, U_l, comm)
+    timer = EventTimer(stream)
+    pd.paradiag_profile(ops.h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            dmax, umax = rk.iterate(u0_l, U_l, comm, timer)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = pd.paradiag_profile_read(ops.h)
+    pd.paradiag_profile(ops.h, False)
+    coll = timer.collect()
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = p.dofs / (ms_step * 1e-3)
+    local_dofs = p.nt * nyl * p.n
+    peak, peak_src = measured_peaks()
+    kernels = {}
+    for name, (n, tot) in prof.items():
+        avg = tot / max(n, 1)
+        bpd = BYTES_PER_DOF.get(name)
+        kernels[name] = {"avg_ms": avg, "share": tot / (ms if ms > 0 else 1),
+                         "gbs": (bpd * local_dofs / (avg * 1e-3) / 1e9) if bpd else None}
+    top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    if top:
+        name, (n, tot) = top
+        avg = tot / n
+        bpd = BYTES_PER_DOF.get(name, 16.0)
+        ach = bpd * local_dofs / (avg * 1e-3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_src, "traffic": None, "algorithmic_bytes_per_launch": bpd * local_dofs,
+                "per": "rank 0 (its row / column slab)"}
+    # NVLink: bytes this rank sends per all-to-all (the local block stays on the device)
+    sent = 8 * (sum(L.fwd_send_splits(rank)) - L.block(rank, rank))
+    a2a = [coll[k] for k in ("alltoall_fwd", "alltoall_bwd") if k in coll]
+    nvlink = None
+    if a2a:
+        avg = sum(a2a) / len(a2a)
+        nvlink = {"achieved": sent / (avg * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s", "frac": sent / (avg * 1e-3) / 1e9 / 770.0,
+                  "peak_source": "guide: measured peer copy per direction", "bytes_per_alltoall": sent,
+                  "avg_ms": {k: coll[k] for k in coll}}
+    # end to end: H2D of the rank's u0 rows, K = 3 iterations, D2H of its u_{N_t} rows
+    e2e = None
+    if not args.no_e2e:
+        K = p.fixed_iters or 3
+        u0h = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).pin_memory()
+        outh = torch.empty((nyl, p.n), dtype=torch.float64).pin_memory()
+        dist.barrier()
+        t0 = time.perf_counter()
+        u0d = u0h.to(dev, non_blocking=True)
+        Ue = fresh_U()
+        for _ in range(K):
+            rk.iterate(u0d, Ue, comm)
+        outh.copy_(Ue.reshape(p.nt, nyl, p.n)[-1], non_blocking=True)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        e2e = {"value": K * p.dofs / te, "unit": "dof/s", "h2d_bytes_per_step": int(p.ns * 8),
+               "d2h_bytes_per_step": int(p.ns * 8), "step": f"H2D u0 slabs, {K} sharded iterations, D2H u_Nt slabs",
+               "seconds_per_step": te}
+    launches = 10 + 4 * world
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "dof/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(cfg, parallelism=f"slab{world}: row slabs (residual, x transforms, update) / column "
+                                                 f"slabs (y transforms, time pass), NCCL all-to-all + halo"),
+                "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
+                "gpu_launches": args.steps * launches * world, "clocks": clk.summary(), "kernels": kernels,
+                "last_iter": {"delta_max": dmax, "u_max": umax}}
+        print(json.dumps(line), flush=True)
+    ops.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -125,6 +268,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="per-kernel event timing (on by default)")
+    ap.add_argument("--parallelism", default="auto", choices=["auto", "slab", "replicas"],
+                    help="N > 1: slab-sharded (strong scaling, default for 2D linear configs) or replicas")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -157,11 +302,19 @@ def main():
     import paper_2304_14021_b200 as pd
 
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = (world > 1 and args.parallelism != "replicas" or args.parallelism == "slab") and p.dim == 2 \
+        and p.kind != "cahn_hilliard"
+    if world > 1 or sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     u0 = make_u0(p)
+    if sharded:
+        return run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric)
     u0_d = torch.from_numpy(u0).to(dev)
     s = pd.Solver(p, device=local, stream=stream.cuda_stream)
     U = torch.zeros(s.shape, dtype=torch.float64, device=dev)       # U⁰ = 0 (R#5)

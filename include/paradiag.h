@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PARADIAG_ABI_VERSION 1
+#define PARADIAG_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PD_API __attribute__((visibility("default")))
@@ -174,6 +174,45 @@ PD_API int paradiag_profile(pd_handle* h, int enable);
 
 /* Copy up to max_entries accumulated kernel timings into out; *n_out = entries available. */
 PD_API int paradiag_profile_read(const pd_handle* h, pd_kernel_time* out, int max_entries, int* n_out);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-rank (slab) mode — SURVEY §8(e), DESIGN.md §8.  "Step-(2) is fully parallel" and
+ * Steps (1)/(3) are independent per spatial point, so a 2D problem shards over P ranks (one process
+ * per GPU): rank r owns the ROW slab y ∈ [y0, y0+nyl) of every time slice for the residual, the
+ * x-direction transforms and the update, and the COLUMN slab x ∈ [x0, x0+nxl) (x-modes after the
+ * x transform) for the y-direction transforms and the time pass (Γ_α·DFT, per-mode divide, IDFT,
+ * Γ_α⁻¹).  Between the two layouts the caller runs an all-to-all transpose (torch.distributed /
+ * NCCL); the 2-row residual halo is exchanged with the neighbouring ranks.  The per-rank entry
+ * points below run only the local kernels; paper_2304_14021_b200/dist.py composes them.
+ * Buffers (all device, fp64, caller-owned):
+ *   u0_l [nyl][n], U_l / r_l / rows [nt][nyl][n]    row slab  (n = points per axis)
+ *   halo_lo / halo_hi [nt][2][n]                     global rows y0-2, y0-1 / y0+nyl, y0+nyl+1
+ *                                                    (NULL where the slab touches the boundary)
+ *   cols [nt][n][nxl]                                column slab (row stride nxl)
+ * Supported: 2D linear kinds (biharmonic, linearised CH), 64 <= m <= 2048, 32 <= nt <= 1024;
+ * otherwise PD_EINVAL.  nyl >= 3.
+ * ------------------------------------------------------------------------------------------- */
+PD_API int paradiag_init_slab(const pd_problem* p, int device, void* cuda_stream, int64_t y0, int64_t nyl,
+                              int64_t x0, int64_t nxl, pd_handle** out);
+PD_API int paradiag_slab_geometry(const pd_handle* h, int64_t* y0, int64_t* nyl, int64_t* x0, int64_t* nxl);
+/* r_l = b - K(U) on the row slab (nested stencils R#15), halos as above. */
+PD_API int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, const double* halo_lo,
+                                  const double* halo_hi, double* r_l);
+/* DCT-I / DST-I along x of every local row; want_dmax: fold max|out| into the
+ * handle's ‖δ‖∞ statistic (the inverse pass).  in may alias out. */
+PD_API int paradiag_slab_xpass(pd_handle* h, const double* in, double* out, int want_dmax);
+/* In place on the column slab: y transform, time pass (Steps (1)-(3) per spatial mode),
+ * inverse y transform. */
+PD_API int paradiag_slab_ypass(pd_handle* h, double* cols);
+/* U_l += δ_l (ω = 1) and fold max|U| into the handle's ‖U‖∞ statistic. */
+PD_API int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l);
+/* dst[a*d0 + b*d1 + c] = src[a*s0 + b*s1 + c], a < n0, b < n1, c < n2 (element strides): the pack /
+ * unpack of the transposes.  Any handle (its stream is used). */
+PD_API int paradiag_copy3d(pd_handle* h, const double* src, double* dst, int64_t n0, int64_t n1, int64_t n2,
+                           int64_t s0, int64_t s1, int64_t d0, int64_t d1);
+/* Zero the handle's ‖δ‖∞ / ‖U‖∞ statistics (asynchronous) / read them (synchronises the stream). */
+PD_API int paradiag_stats_reset(pd_handle* h);
+PD_API int paradiag_stats_read(pd_handle* h, double* dmax, double* umax);
 
 /* Release all device memory of the handle.  NULL is a no-op. */
 PD_API void paradiag_destroy(pd_handle* h);

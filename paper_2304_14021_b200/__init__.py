@@ -55,7 +55,11 @@ class pd_kernel_time(ctypes.Structure):
 _lib = None
 EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", "paradiag_strerror", "paradiag_last_error", "paradiag_workspace_bytes",
            "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_iterate",
-           "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy"]
+           "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy",
+           "paradiag_init_slab", "paradiag_slab_geometry", "paradiag_slab_residual", "paradiag_slab_xpass",
+           "paradiag_slab_ypass", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
+           "paradiag_stats_read"]
+ABI_VERSION = 2
 
 
 def load(path: str = LIB_PATH):
@@ -83,10 +87,20 @@ def load(path: str = LIB_PATH):
     lib.paradiag_profile_read.argtypes = [vp, P(pd_kernel_time), ctypes.c_int, P(ctypes.c_int)]
     lib.paradiag_destroy.argtypes = [vp]
     lib.paradiag_destroy.restype = None
+    i64 = ctypes.c_int64
+    lib.paradiag_init_slab.argtypes = [P(pd_problem), ctypes.c_int, vp, i64, i64, i64, i64, P(vp)]
+    lib.paradiag_slab_geometry.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
+    lib.paradiag_slab_residual.argtypes = [vp, vp, vp, vp, vp, vp]
+    lib.paradiag_slab_xpass.argtypes = [vp, vp, vp, ctypes.c_int]
+    lib.paradiag_slab_ypass.argtypes = [vp, vp]
+    lib.paradiag_slab_update.argtypes = [vp, vp, vp]
+    lib.paradiag_copy3d.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64]
+    lib.paradiag_stats_reset.argtypes = [vp]
+    lib.paradiag_stats_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_double)]
     for name in EXPORTS:
         if name not in ("paradiag_destroy",):
             getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
-    if lib.paradiag_abi_version() != 1:
+    if lib.paradiag_abi_version() != ABI_VERSION:
         raise ParadiagError(PD_ECUDA, "load", "ABI version mismatch")
     _lib = lib
     return lib
@@ -212,6 +226,58 @@ def paradiag_profile_read(h) -> dict:
     buf = (pd_kernel_time * 32)()
     _check(load().paradiag_profile_read(h, buf, 32, ctypes.byref(n)), "paradiag_profile_read")
     return {buf[i].name.decode(): (buf[i].launches, buf[i].total_ms) for i in range(min(n.value, 32))}
+
+
+def paradiag_init_slab(problem: pd_problem, device: int, stream, y0: int, nyl: int, x0: int, nxl: int):
+    h = ctypes.c_void_p()
+    _check(load().paradiag_init_slab(ctypes.byref(problem), int(device), ctypes.c_void_p(stream), int(y0), int(nyl),
+                                     int(x0), int(nxl), ctypes.byref(h)), "paradiag_init_slab")
+    return h
+
+
+def _optr(t, name):
+    return ctypes.c_void_p(None) if t is None else _ptr(t, name)
+
+
+def paradiag_slab_residual(h, u0_l, U_l, halo_lo, halo_hi, r_l):
+    _check(load().paradiag_slab_residual(h, _ptr(u0_l, "u0_l"), _ptr(U_l, "U_l"), _optr(halo_lo, "halo_lo"),
+                                         _optr(halo_hi, "halo_hi"), _ptr(r_l, "r_l")), "paradiag_slab_residual")
+
+
+def paradiag_slab_xpass(h, src, dst, want_dmax=False):
+    _check(load().paradiag_slab_xpass(h, _ptr(src, "in"), _ptr(dst, "out"), 1 if want_dmax else 0),
+           "paradiag_slab_xpass")
+
+
+def paradiag_slab_ypass(h, cols):
+    _check(load().paradiag_slab_ypass(h, _ptr(cols, "cols")), "paradiag_slab_ypass")
+
+
+def paradiag_slab_update(h, U_l, delta_l):
+    _check(load().paradiag_slab_update(h, _ptr(U_l, "U_l"), _ptr(delta_l, "delta_l")), "paradiag_slab_update")
+
+
+def paradiag_copy3d(h, src, dst, n, s, d, src_off=0, dst_off=0):
+    """dst[dst_off + a*d[0] + b*d[1] + c] = src[src_off + a*s[0] + b*s[1] + c], (a, b, c) < n.
+    src/dst are flat float64 CUDA tensors; offsets and strides in elements."""
+    import torch
+    for t, nm in ((src, "src"), (dst, "dst")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise ParadiagError(PD_EINVAL, nm, "expected a contiguous float64 CUDA tensor")
+    sp = ctypes.c_void_p(src.data_ptr() + 8 * int(src_off))
+    dp = ctypes.c_void_p(dst.data_ptr() + 8 * int(dst_off))
+    _check(load().paradiag_copy3d(h, sp, dp, int(n[0]), int(n[1]), int(n[2]), int(s[0]), int(s[1]), int(d[0]),
+                                  int(d[1])), "paradiag_copy3d")
+
+
+def paradiag_stats_reset(h):
+    _check(load().paradiag_stats_reset(h), "paradiag_stats_reset")
+
+
+def paradiag_stats_read(h):
+    a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(load().paradiag_stats_read(h, ctypes.byref(a), ctypes.byref(b)), "paradiag_stats_read")
+    return a.value, b.value
 
 
 def paradiag_destroy(h):

@@ -57,4 +57,17 @@ __global__ void k_reset_stats(DevStats* st) {
 
 __global__ void k_set_jbar(DevStats* st, double jbar) { st->jbar = jbar; }
 
+// dst[a·d0 + b·d1 + c] = src[a·s0 + b·s1 + c] for a < n0, b < n1, c < n2 — the pack / unpack of
+// the row-slab <-> column-slab transposes of a multi-rank run (one CTA per (a, b) row, grid-stride).
+__global__ void __launch_bounds__(256)
+k_copy3d(const double* __restrict__ src, double* __restrict__ dst, int64_t n0, int64_t n1, int64_t n2,
+         int64_t s0, int64_t s1, int64_t d0, int64_t d1) {
+  for (int64_t row = blockIdx.x; row < n0 * n1; row += gridDim.x) {
+    const int64_t a = row / n1, b = row - a * n1;
+    const double* s = src + a * s0 + b * s1;
+    double* d = dst + a * d0 + b * d1;
+    for (int64_t c = threadIdx.x; c < n2; c += blockDim.x) d[c] = __ldg(s + c);
+  }
+}
+
 }  // namespace pd

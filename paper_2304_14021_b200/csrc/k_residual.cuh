@@ -14,6 +14,12 @@ struct ResidualParams {
   double inv_h2;        // m² exactly
   double inv_dt;        // nt / T
   double b2, e2;        // fl(β·β), fl(ε·ε)
+  // row slab of a multi-rank run (k_residual_tile only): local rows are global rows
+  // [y0g, y0g + ny); rows y0g-2, y0g-1 come from hlo [nt][2][nx], rows y0g+ny, +1 from hhi.
+  // Single GPU: y0g = 0, nyg = ny, no halo buffers.
+  int y0g, nyg;
+  const double* hlo;
+  const double* hhi;
 };
 
 // Reflect an out-of-range Neumann index back onto the node grid (ghost u_{-1} = u_1).
@@ -293,27 +299,37 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
   const int n0 = blockIdx.z * kResChunk, n1 = min(n0 + kResChunk, P.nt);
   const size_t ns = (size_t)P.nx * P.ny;
   const bool ch = P.kind == 2;
-  // staging map (slice independent): element k of this thread -> smem slot, source offset, sign
-  int soff[kResPer], dpos[kResPer];
+  // staging map (slice independent): element k of this thread -> smem slot, source buffer
+  // (0: U, 1: lower halo, 2: upper halo) and offset within its slice, extension sign
+  int soff[kResPer], dpos[kResPer], ssel[kResPer];
   double sgn[kResPer];
 #pragma unroll
   for (int k = 0; k < kResPer; ++k) {
     const int i = tid + k * kResThreads;
     const int ry = i / kResUX, rx = i - ry * kResUX;
-    int cy = 0, cx = 0;
+    int cy = 0, cx = 0, sel = 0;
     double sy = 0.0, sg = 0.0;
     if (i < kResUN) {
-      ext_map(y0 - 2 + ry, P.ny, P.neumann, cy, sy);
+      ext_map(P.y0g + y0 - 2 + ry, P.nyg, P.neumann, cy, sy);     // global row
       ext_map(x0 - 2 + rx, P.nx, P.neumann, cx, sg);
+      cy -= P.y0g;                                                // local row
+      if (sy == 0.0) cy = 0;            // hinged boundary line: zeroed by the sign; load any local row
+      if (cy < 0) { sel = 1; cy += 2; }
+      else if (cy >= P.ny) { sel = 2; cy -= P.ny; }
     }
     soff[k] = i < kResUN ? cy * P.nx + cx : -1;
+    ssel[k] = sel;
     dpos[k] = ry * kResUP + rx;
     sgn[k] = sy * sg;
   }
+  const size_t hstride = 2 * (size_t)P.nx;
   auto stage = [&](double* dst, int n) {
 #pragma unroll
     for (int k = 0; k < kResPer; ++k)
-      if (soff[k] >= 0) cp_async8(dst + dpos[k], U + (size_t)n * ns + soff[k]);
+      if (soff[k] >= 0) {
+        const double* b = ssel[k] == 0 ? U + (size_t)n * ns : (ssel[k] == 1 ? P.hlo : P.hhi) + (size_t)n * hstride;
+        cp_async8(dst + dpos[k], b + soff[k]);
+      }
     cp_async_commit();
   };
   auto fix_signs = [&](double* dst) {     // hinged: odd extension (own elements only)

@@ -32,11 +32,12 @@ struct TimeParams {
   int twlog;
   unsigned long long* amax;   // optional max |out|
   int tune;                   // PARADIAG_TUNE bits (A/B switches for measurements; 0 = defaults)
+  int xoff;                   // column slab (multi-rank): global x of local column 0
 };
 
 PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {
   const int64_t q = s / P.nx, p = s - q * P.nx;
-  const double Lam = __ldg(P.lamx + p) + (P.nx == P.ns ? 0.0 : __ldg(P.lamx + q));
+  const double Lam = __ldg(P.lamx + P.xoff + p) + (P.nx == P.ns ? 0.0 : __ldg(P.lamx + q));
   if (P.kind == 0) return Lam * Lam;
   if (P.kind == 1) return P.b2 * Lam + P.e2 * (Lam * Lam);
   return -jbar * Lam + P.e2 * (Lam * Lam);

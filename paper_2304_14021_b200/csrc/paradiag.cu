@@ -98,6 +98,10 @@ struct pd_handle {
   double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
   int dtt_ver = 3;                    // line kernels: 3 = k_dtt.cuh, 2 = k_fast.cuh
   int tune = 0;                       // PARADIAG_TUNE: A/B switches for measurements
+  // slab mode (multi-rank): rows [y0, y0+nyl) for residual / x passes / update,
+  // columns [x0, x0+nxl) for the y passes and the time pass; buffers are the caller's
+  bool slab = false;
+  int y0 = 0, nyl = 0, x0 = 0, nxl = 0;
   double* band = nullptr;
   double2* fac = nullptr;             // 4 x [nx][nb]
   DevStats* st = nullptr;
@@ -217,6 +221,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
+  R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr;
   prof_begin(h, K_RESIDUAL);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
   if (h->P.dim == 2) {
@@ -322,7 +327,7 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   T.nt = h->P.nt; T.log2nt = h->log2nt; T.ns = h->ns; T.nx = h->nx;
   T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.lamx = h->lam;
   T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
-  T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune;
+  T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune; T.xoff = 0;
   return T;
 }
 
@@ -464,7 +469,13 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   return PD_OK;
 }
 
+int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** out, bool slab);
+
 int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle** out) {
+  return init_impl(p, device, cuda_stream, out, false);
+}
+
+int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** out, bool slab) {
   if (!out) return fail(PD_EINVAL, "out is NULL");
   *out = nullptr;
   int rc = validate(p);
@@ -556,7 +567,7 @@ int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle*
   }
 
   // ---- device buffers
-  PD_TRY(dalloc(h, &h->work, (size_t)h->total));
+  if (!slab) PD_TRY(dalloc(h, &h->work, (size_t)h->total));   // slab mode: caller-owned buffers
   PD_TRY(dalloc(h, &h->u0buf, (size_t)h->ns));
   PD_TRY(dalloc(h, &h->gam, nt));
   PD_TRY(dalloc(h, &h->ginv, nt));
@@ -772,6 +783,168 @@ int paradiag_profile_read(const pd_handle* h, pd_kernel_time* out, int max_entri
     ++n;
   }
   *n_out = n;
+  return PD_OK;
+}
+
+// ----------------------------------------------------------------------------- slab mode
+int paradiag_init_slab(const pd_problem* p, int device, void* cuda_stream, int64_t y0, int64_t nyl, int64_t x0,
+                       int64_t nxl, pd_handle** out) {
+  if (!out) return fail(PD_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = validate(p);
+  if (rc) return rc;
+  if (p->dim != 2 || p->kind == PD_CAHN_HILLIARD)
+    return fail(PD_EINVAL, "slab mode: 2D linear kinds only (CH runs as replicas, DESIGN.md §8)");
+  if (p->m < 64 || p->m > 2048 || p->nt < 32 || p->nt > 1024)
+    return fail(PD_EINVAL, "slab mode: needs the register-FFT sizes (64 <= m <= 2048, 32 <= nt <= 1024)");
+  int nx, ny;
+  geometry(p, &nx, &ny);
+  if (y0 < 0 || nyl < 3 || y0 + nyl > ny || x0 < 0 || nxl < 1 || x0 + nxl > nx)
+    return fail(PD_EINVAL, "slab mode: row slab needs >= 3 rows and both slabs inside the grid");
+  // a single-GPU handle of the same problem provides the tables; its iterate-sized workspace is
+  // not allocated in slab mode (the caller owns every buffer)
+  pd_problem q = *p;
+  rc = init_impl(&q, device, cuda_stream, out, true);
+  if (rc) return rc;
+  pd_handle* h = *out;
+  h->slab = true;
+  h->y0 = (int)y0; h->nyl = (int)nyl; h->x0 = (int)x0; h->nxl = (int)nxl;
+  return PD_OK;
+}
+
+int paradiag_slab_geometry(const pd_handle* h, int64_t* y0, int64_t* nyl, int64_t* x0, int64_t* nxl) {
+  if (!h || !h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (y0) *y0 = h->y0;
+  if (nyl) *nyl = h->nyl;
+  if (x0) *x0 = h->x0;
+  if (nxl) *nxl = h->nxl;
+  return PD_OK;
+}
+
+int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, const double* halo_lo,
+                           const double* halo_hi, double* r_l) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (!u0_l || !U_l || !r_l) return fail(PD_EINVAL, "NULL buffer");
+  if ((h->y0 > 0 && !halo_lo) || (h->y0 + h->nyl < h->ny && !halo_hi))
+    return fail(PD_EINVAL, "interior slab edges need halo rows");
+  ResidualParams R;
+  R.nx = h->nx; R.ny = h->nyl; R.nt = h->P.nt; R.dim = 2;
+  R.neumann = h->neumann; R.kind = h->P.kind;
+  R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
+  R.y0g = h->y0; R.nyg = h->ny; R.hlo = halo_lo; R.hhi = halo_hi;
+  prof_begin(h, K_RESIDUAL);
+  dim3 grd((h->nx + kResTX - 1) / kResTX, (h->nyl + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
+  k_residual_tile<<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
+  prof_end(h, K_RESIDUAL);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_slab_xpass(pd_handle* h, const double* in, double* out, int want_dmax) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (!in || !out) return fail(PD_EINVAL, "NULL buffer");
+  LineParams L = line_params(h, 0, want_dmax ? &h->st->dmax_bits : nullptr);
+  L.nlines = (int64_t)h->P.nt * h->nyl;
+  prof_begin(h, want_dmax ? K_XINV : K_XFWD);
+  const bool ok = fast_line_any(h, in, out, 0, L);
+  prof_end(h, want_dmax ? K_XINV : K_XFWD);
+  if (!ok) return fail(PD_EINVAL, "slab mode: unsupported line length");
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_slab_ypass(pd_handle* h, double* buf) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (!buf) return fail(PD_EINVAL, "NULL buffer");
+  // column slab [nt][ny][nxl]: lines along y with row stride nxl
+  LineParams L = line_params(h, 1, nullptr);
+  L.nlines = (int64_t)h->P.nt * h->nxl;
+  L.nx = h->nxl;
+  L.ns = (int64_t)h->ny * h->nxl;
+  L.nel = h->ny;
+  FastLaunch F = fast_launch(h);
+  F.nx = h->nxl;
+  F.ns = L.ns;
+  TimeParams T = time_params(h, nullptr);
+  T.ns = L.ns;
+  T.nx = h->nxl;
+  T.xoff = h->x0;
+  const int nm = h->neumann ? 1 : 0;
+  auto yline = [&](int kid) {
+    prof_begin(h, kid);
+    switch (L.M) {
+      case 64: fast_line<1>(nm, 1, buf, buf, L, F); break;
+      case 128: fast_line<2>(nm, 1, buf, buf, L, F); break;
+      case 256: fast_line<4>(nm, 1, buf, buf, L, F); break;
+      case 512: fast_line<8>(nm, 1, buf, buf, L, F); break;
+      case 1024: fast_line<16>(nm, 1, buf, buf, L, F); break;
+      default: fast_line<32>(nm, 1, buf, buf, L, F); break;
+    }
+    prof_end(h, kid);
+  };
+  yline(K_YFWD);
+  prof_begin(h, K_TIME);
+  switch (h->P.nt) {
+    case 32: fast_time<1>(buf, buf, T, F); break;
+    case 64: fast_time<2>(buf, buf, T, F); break;
+    case 128: fast_time<4>(buf, buf, T, F); break;
+    case 256: fast_time<8>(buf, buf, T, F); break;
+    case 512: fast_time<16>(buf, buf, T, F); break;
+    default: fast_time<32>(buf, buf, T, F); break;
+  }
+  prof_end(h, K_TIME);
+  yline(K_YINV);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (!U_l || !delta_l) return fail(PD_EINVAL, "NULL buffer");
+  prof_begin(h, K_UPDATE);
+  k_update<<<148 * 8, 256, 0, h->stream>>>(U_l, delta_l, (size_t)h->P.nt * h->nyl * h->nx, h->st, 0, 1.0, 1.0);
+  prof_end(h, K_UPDATE);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_copy3d(pd_handle* h, const double* src, double* dst, int64_t n0, int64_t n1, int64_t n2, int64_t s0,
+                    int64_t s1, int64_t d0, int64_t d1) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (n0 <= 0 || n1 <= 0 || n2 <= 0) return PD_OK;
+  if (!src || !dst) return fail(PD_EINVAL, "NULL buffer");
+  const int64_t rows = n0 * n1;
+  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 16);
+  k_copy3d<<<grid, 256, 0, h->stream>>>(src, dst, n0, n1, n2, s0, s1, d0, d1);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_stats_reset(pd_handle* h) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_stats_read(pd_handle* h, double* dmax, double* umax) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  if (dmax) std::memcpy(dmax, &h->st_host->dmax_bits, sizeof(double));
+  if (umax) std::memcpy(umax, &h->st_host->umax_bits, sizeof(double));
   return PD_OK;
 }
 

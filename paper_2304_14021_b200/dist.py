@@ -1,0 +1,309 @@
+"""Multi-rank ParaDiag iteration: one process per GPU, the 2D grid sharded in slabs (SURVEY §8(e),
+DESIGN.md §8).
+
+Why it shards ("Step-(2) is fully parallel"): the preconditioner is three commuting
+transforms — x, y (DCT-I / DST-I) and time (Γ_α·DFT) — with a per-mode divide
+in the middle.  Each rank r owns
+
+  * the ROW slab  y ∈ rows[r] of every time slice: residual (needs a 2-row halo from
+    the neighbouring ranks), x transforms, update;
+  * the COLUMN slab x ∈ cols[r] (x-modes after the x transform): y transforms and the time pass
+    (complete time pencils of every local point, so Step-(2) needs no further communication).
+
+Between the layouts an all-to-all transposes the data (forward after the x transform, backward
+before the inverse x transform).  The collectives are torch.distributed (NCCL on GPUs, gloo in
+the CPU tests); every local step runs in the C-ABI library (slab entry points of
+include/paradiag.h) through ``GpuOps``.  The copy descriptors of the packs / unpacks and of the
+halo are computed once here (``SlabLayout``), so a CPU stand-in for the local kernels (the
+world-size-2 gloo test) exercises exactly the layout and collective logic of the GPU path.
+
+Buffers per rank (fp64): row slab [nt][nyl][n], column slab [nt][n][nxl], send / receive
+buffers of the larger transpose block sum, halos [nt][2][n].
+"""
+from dataclasses import dataclass
+from typing import List, Tuple
+
+Desc = Tuple[Tuple[int, int, int], Tuple[int, int], Tuple[int, int], int, int]   # n, s, d, src_off, dst_off
+
+
+def split(n: int, parts: int) -> List[Tuple[int, int]]:
+    """Contiguous near-even split of range(n): (start, count) per part; the first n % parts parts
+    get one extra element."""
+    base, extra = divmod(n, parts)
+    out, s = [], 0
+    for p in range(parts):
+        c = base + (1 if p < extra else 0)
+        out.append((s, c))
+        s += c
+    return out
+
+
+@dataclass
+class SlabLayout:
+    """Slab geometry of an n x n grid with nt slices over P ranks, and the copy descriptors
+    (``paradiag_copy3d`` form) of every pack / unpack."""
+    n: int
+    nt: int
+    P: int
+
+    def __post_init__(self):
+        self.rows = split(self.n, self.P)
+        self.cols = split(self.n, self.P)
+        if min(c for _, c in self.rows) < 3:
+            raise ValueError("slab mode needs at least 3 rows per rank")
+
+    # sizes (elements)
+    def row_slab(self, r):
+        return self.nt * self.rows[r][1] * self.n
+
+    def col_slab(self, r):
+        return self.nt * self.n * self.cols[r][1]
+
+    def block(self, rr, cq):
+        """elements of the (row slab rr) x (column slab cq) block of all slices"""
+        return self.nt * self.rows[rr][1] * self.cols[cq][1]
+
+    # forward transpose: rows -> columns
+    def fwd_send_splits(self, r):
+        return [self.block(r, q) for q in range(self.P)]
+
+    def fwd_recv_splits(self, q):
+        return [self.block(s, q) for s in range(self.P)]
+
+    def fwd_pack(self, r) -> List[Desc]:
+        """rows[r] slab [nt][nyl][n] -> send buffer, block q = [nt][nyl][nxl_q]"""
+        nyl, out, off = self.rows[r][1], [], 0
+        for q in range(self.P):
+            x0, nxl = self.cols[q]
+            out.append(((self.nt, nyl, nxl), (nyl * self.n, self.n), (nyl * nxl, nxl), x0, off))
+            off += self.block(r, q)
+        return out
+
+    def fwd_unpack(self, q) -> List[Desc]:
+        """receive buffer (block s = [nt][nyl_s][nxl]) -> column slab [nt][n][nxl] rows y_s.."""
+        nxl, out, off = self.cols[q][1], [], 0
+        for s in range(self.P):
+            y0, nyl = self.rows[s]
+            out.append(((self.nt, nyl, nxl), (nyl * nxl, nxl), (self.n * nxl, nxl), off, y0 * nxl))
+            off += self.block(s, q)
+        return out
+
+    # backward transpose: columns -> rows (the mirror of the forward one)
+    def bwd_send_splits(self, q):
+        return self.fwd_recv_splits(q)
+
+    def bwd_recv_splits(self, r):
+        return self.fwd_send_splits(r)
+
+    def bwd_pack(self, q) -> List[Desc]:
+        return [(n, d, s, do, so) for (n, s, d, so, do) in self.fwd_unpack(q)]
+
+    def bwd_unpack(self, r) -> List[Desc]:
+        return [(n, d, s, do, so) for (n, s, d, so, do) in self.fwd_pack(r)]
+
+    # residual halo: first / last two local rows of every slice, packed [nt][2][n]
+    def halo_pack(self, r) -> Tuple[Desc, Desc]:
+        nyl = self.rows[r][1]
+        lo = ((self.nt, 2, self.n), (nyl * self.n, self.n), (2 * self.n, self.n), 0, 0)
+        hi = ((self.nt, 2, self.n), (nyl * self.n, self.n), (2 * self.n, self.n), (nyl - 2) * self.n, 0)
+        return lo, hi
+
+    def halo_size(self):
+        return self.nt * 2 * self.n
+
+
+class GpuOps:
+    """The local steps of one rank, in the sm_100a library (slab entry points)."""
+
+    def __init__(self, problem, device, stream, y0, nyl, x0, nxl):
+        from . import paradiag_init_slab, make_problem, pd_problem
+        import torch
+        self.problem = problem if isinstance(problem, pd_problem) else make_problem(problem)
+        self.device = device
+        self.torch = torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self.h = paradiag_init_slab(self.problem, device, stream, y0, nyl, x0, nxl)
+
+    def empty(self, count):
+        return self.torch.empty(count, dtype=self.torch.float64, device=f"cuda:{self.device}")
+
+    def copy(self, src, dst, desc: Desc):
+        from . import paradiag_copy3d
+        n, s, d, so, do = desc
+        paradiag_copy3d(self.h, src, dst, n, s, d, so, do)
+
+    def residual(self, u0_l, U_l, hlo, hhi, r_l):
+        from . import paradiag_slab_residual
+        paradiag_slab_residual(self.h, u0_l, U_l, hlo, hhi, r_l)
+
+    def xpass(self, src, dst, want_dmax=False):
+        from . import paradiag_slab_xpass
+        paradiag_slab_xpass(self.h, src, dst, want_dmax)
+
+    def ypass(self, cols):
+        from . import paradiag_slab_ypass
+        paradiag_slab_ypass(self.h, cols)
+
+    def update(self, U_l, delta_l):
+        from . import paradiag_slab_update
+        paradiag_slab_update(self.h, U_l, delta_l)
+
+    def stats_reset(self):
+        from . import paradiag_stats_reset
+        paradiag_stats_reset(self.h)
+
+    def stats_read(self):
+        from . import paradiag_stats_read
+        return paradiag_stats_read(self.h)
+
+    def close(self):
+        from . import paradiag_destroy
+        if self.h:
+            paradiag_destroy(self.h)
+            self.h = None
+
+
+class TorchComm:
+    """Collectives of a real multi-process run (torch.distributed, NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_to_all(self, recv, send, recv_splits, send_splits):
+        self.dist.all_to_all_single(recv[:sum(recv_splits)], send[:sum(send_splits)], recv_splits, send_splits,
+                                    group=self.group)
+
+    def halo(self, send_lo, send_hi, recv_lo, recv_hi):
+        """send_lo -> rank-1 (its upper halo), send_hi -> rank+1 (its lower halo)"""
+        ops = []
+        P2P = self.dist.P2POp
+        if self.rank > 0:
+            ops += [P2P(self.dist.isend, send_lo, self.rank - 1, self.group),
+                    P2P(self.dist.irecv, recv_lo, self.rank - 1, self.group)]
+        if self.rank < self.world - 1:
+            ops += [P2P(self.dist.isend, send_hi, self.rank + 1, self.group),
+                    P2P(self.dist.irecv, recv_hi, self.rank + 1, self.group)]
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def allreduce_max(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
+
+class SlabRank:
+    """State and phases of one rank.  ``iterate`` runs one defect-correction iteration
+    U ← U + P_α⁻¹(b − K U) on the rank's row slab."""
+
+    def __init__(self, layout: SlabLayout, rank: int, ops):
+        self.L, self.r, self.ops = layout, rank, ops
+        self.y0, self.nyl = layout.rows[rank]
+        self.x0, self.nxl = layout.cols[rank]
+        P = layout.P
+        tsz = max(sum(layout.fwd_send_splits(rank)), sum(layout.fwd_recv_splits(rank)))
+        self.rows = ops.empty(layout.row_slab(rank))         # r, then δ
+        self.cols = ops.empty(layout.col_slab(rank))
+        self.send = ops.empty(tsz)
+        self.recv = ops.empty(tsz)
+        hs = layout.halo_size()
+        self.hsend_lo, self.hsend_hi = ops.empty(hs), ops.empty(hs)
+        self.hlo = ops.empty(hs) if rank > 0 else None
+        self.hhi = ops.empty(hs) if rank < P - 1 else None
+        self._dummy = ops.empty(hs) if (self.hlo is None or self.hhi is None) else None
+
+    # ---- phases (each only enqueues local work)
+    def phase_halo_pack(self, U_l):
+        lo, hi = self.L.halo_pack(self.r)
+        self.ops.stats_reset()
+        self.ops.copy(U_l, self.hsend_lo, lo)
+        self.ops.copy(U_l, self.hsend_hi, hi)
+
+    def phase_residual_xfwd(self, u0_l, U_l):
+        self.ops.residual(u0_l, U_l, self.hlo, self.hhi, self.rows)
+        self.ops.xpass(self.rows, self.rows)
+        for d in self.L.fwd_pack(self.r):
+            self.ops.copy(self.rows, self.send, d)
+
+    def phase_ypass(self):
+        for d in self.L.fwd_unpack(self.r):
+            self.ops.copy(self.recv, self.cols, d)
+        self.ops.ypass(self.cols)
+        for d in self.L.bwd_pack(self.r):
+            self.ops.copy(self.cols, self.send, d)
+
+    def phase_xinv_update(self, U_l):
+        for d in self.L.bwd_unpack(self.r):
+            self.ops.copy(self.recv, self.rows, d)
+        self.ops.xpass(self.rows, self.rows, want_dmax=True)
+        self.ops.update(U_l, self.rows)
+
+    # ---- one iteration of a real multi-process run
+    def iterate(self, u0_l, U_l, comm: TorchComm, timer=None):
+        """timer: optional callable(name) -> context manager timing a collective on the device"""
+        L, r = self.L, self.r
+        tm = timer or (lambda name: _Null())
+        self.phase_halo_pack(U_l)
+        with tm("halo"):
+            comm.halo(self.hsend_lo, self.hsend_hi, self.hlo if self.hlo is not None else self._dummy,
+                      self.hhi if self.hhi is not None else self._dummy)
+        self.phase_residual_xfwd(u0_l, U_l)
+        with tm("alltoall_fwd"):
+            comm.all_to_all(self.recv, self.send, L.fwd_recv_splits(r), L.fwd_send_splits(r))
+        self.phase_ypass()
+        with tm("alltoall_bwd"):
+            comm.all_to_all(self.recv, self.send, L.bwd_recv_splits(r), L.bwd_send_splits(r))
+        self.phase_xinv_update(U_l)
+        dmax, umax = self.ops.stats_read()
+        t = self.ops.empty(2) if hasattr(self.ops, "empty") else None
+        t[0], t[1] = dmax, umax
+        comm.allreduce_max(t)
+        return float(t[0]), float(t[1])
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def iterate_virtual(ranks: List[SlabRank], u0s, Us):
+    """All P ranks of a layout in ONE process (one GPU): the same phases in rank order with the
+    collectives emulated by buffer copies — the multi-rank data path checked on a single device
+    (no rank waits on another, so nothing can deadlock)."""
+    P = len(ranks)
+    L = ranks[0].L
+    for k in range(P):
+        ranks[k].phase_halo_pack(Us[k])
+    for k in range(P):
+        if k > 0:
+            ranks[k].hlo.copy_(ranks[k - 1].hsend_hi)
+        if k < P - 1:
+            ranks[k].hhi.copy_(ranks[k + 1].hsend_lo)
+    for k in range(P):
+        ranks[k].phase_residual_xfwd(u0s[k], Us[k])
+    _alltoall_virtual(ranks, [L.fwd_send_splits(k) for k in range(P)])
+    for k in range(P):
+        ranks[k].phase_ypass()
+    _alltoall_virtual(ranks, [L.bwd_send_splits(k) for k in range(P)])
+    for k in range(P):
+        ranks[k].phase_xinv_update(Us[k])
+    st = [rk.ops.stats_read() for rk in ranks]
+    return max(s[0] for s in st), max(s[1] for s in st)
+
+
+def _alltoall_virtual(ranks, send_splits):
+    P = len(ranks)
+    soff = [[sum(send_splits[s][:q]) for q in range(P)] for s in range(P)]
+    for q in range(P):
+        off = 0
+        for s in range(P):
+            c = send_splits[s][q]
+            ranks[q].recv[off:off + c].copy_(ranks[s].send[soff[s][q]:soff[s][q] + c])
+            off += c

@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.paradiag_abi_version() == 1
+    assert lib.paradiag_abi_version() == pd.ABI_VERSION == 2
     assert pd.strerror(pd.PD_EINVAL).startswith("PD_EINVAL")
     assert pd.strerror(pd.PD_ESINGULAR).startswith("PD_ESINGULAR")
 

@@ -1,0 +1,77 @@
+"""Multi-rank (slab) data path on ONE GPU: P virtual ranks run the phases of
+paper_2304_14021_b200/dist.py in rank order with the collectives emulated by copies
+(iterate_virtual), against the single-GPU iteration (the same kernels, unsharded) and the oracle.
+
+The sharded path differs from the single-GPU one only in which two spatial modes share a
+time-pass pencil (the column slab regroups them), so the two agree to rounding; for the hinged
+biharmonic twin (cond(I + ΔtA) ≈ 1e9) that is ≈ 2e-11 of max|U| on the decayed late slices, so the
+bar here is 5e-11 (and 1e-10 against the oracle, the parity bar)."""
+import numpy as np
+import pytest
+
+from _helpers import to_dev, rel_err
+from oracle import iterate
+from workloads import twin, make_u0
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c5_m128_nt32": twin("c5", m=128, nt=32),          # Neumann, 129 rows
+    "c3_m128_nt32": twin("c3", m=128, nt=32),          # hinged, 127 rows
+    "c5_m64_nt64": twin("c5", m=64, nt=64),
+}
+
+
+def _slabs(cuda_lib, p, P):
+    from paper_2304_14021_b200 import dist
+    L = dist.SlabLayout(p.n, p.nt, P)
+    ranks = []
+    for r in range(P):
+        y0, nyl = L.rows[r]
+        x0, nxl = L.cols[r]
+        ops = dist.GpuOps(p, 0, None, y0, nyl, x0, nxl)
+        ranks.append(dist.SlabRank(L, r, ops))
+    return L, ranks
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_virtual_ranks_match_single_gpu(cuda_lib, name, P):
+    import torch
+    from paper_2304_14021_b200 import dist
+    p = CASES[name]
+    u0 = make_u0(p)
+    U0 = iterate.initial_iterate(p, u0)
+    s = cuda_lib.Solver(p)
+    U = to_dev(U0, p)
+    u0d = to_dev(u0)
+    L, ranks = _slabs(cuda_lib, p, P)
+    Us = [U.clone()[:, y0:y0 + nyl, :].contiguous().reshape(-1) for (y0, nyl) in L.rows]
+    u0s = [u0d[y0:y0 + nyl, :].contiguous() for (y0, nyl) in L.rows]
+    info = None
+    U_o = U0
+    for k in range(3):
+        info = s.iterate(u0d, U, info)
+        dmax, umax = dist.iterate_virtual(ranks, u0s, Us)
+        U_o, io = iterate.iterate_once(p, u0, U_o)
+        got = torch.cat([Us[r].reshape(p.nt, L.rows[r][1], p.n) for r in range(P)], dim=1)
+        assert rel_err(got.cpu().numpy(), U.cpu().numpy()) <= 5e-11, k
+        # against the oracle: as accurate as the unsharded GPU path (un-converged iterates of the
+        # hinged twin carry ≈1e-9 of rounding amplification in both)
+        e_single = rel_err(U.cpu().numpy(), U_o)
+        assert rel_err(got.cpu().numpy(), U_o) <= max(1e-10, 1.1 * e_single), k
+        assert abs(dmax - info.delta_max) <= 5e-11 * max(info.delta_max, info.u_max)
+        assert abs(umax - info.u_max) <= 5e-11 * info.u_max
+    for rk in ranks:
+        rk.ops.close()
+
+
+def test_slab_entry_points_reject_bad_geometry(cuda_lib):
+    p = CASES["c5_m64_nt64"]
+    with pytest.raises(cuda_lib.ParadiagError):
+        cuda_lib.paradiag_init_slab(cuda_lib.make_problem(p), 0, 0, 0, 2, 0, 10)       # < 3 rows
+    with pytest.raises(cuda_lib.ParadiagError):
+        cuda_lib.paradiag_init_slab(cuda_lib.make_problem(p), 0, 0, 60, 10, 0, 10)     # past the grid
+    q = twin("c4", m=64, nt=32)
+    with pytest.raises(cuda_lib.ParadiagError):                                          # CH: replicas only
+        cuda_lib.paradiag_init_slab(cuda_lib.make_problem(q), 0, 0, 0, 10, 0, 10)
