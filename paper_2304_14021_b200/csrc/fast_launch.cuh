@@ -64,6 +64,8 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>());
   PD_ATTR((k_cols3<1, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<0, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols3<1, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
+  PD_ATTR((k_cols3<0, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
   return cudaSuccess;
 }
 #undef PD_ATTR
@@ -77,6 +79,11 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
       const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
       const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
       k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, dtt3_rows_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+    } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
+      constexpr int C4 = 4 * (32 / E);
+      const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 2);
+      k_cols3<NEUMANN, E, 4><<<grid, 128, (size_t)4 * Dtt3<1, E>::BUF * sizeof(double), F.stream>>>(in, out, L, F.trig2);
     } else {
       const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
       const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);

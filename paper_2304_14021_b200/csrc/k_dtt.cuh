@@ -254,7 +254,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
 // doubles wide (cp.async straight into each column's line buffer), the next tile is prefetched
 // into L2 during the transforms, outputs are read back from the line buffers row by row.
 template <int NEUMANN, int E, int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
+__global__ void __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1)
 k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
   using D = Dtt3<NEUMANN, E>;
   constexpr int C = NW * D::P;

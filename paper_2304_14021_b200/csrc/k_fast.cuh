@@ -90,18 +90,29 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
 #pragma unroll
     for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * NT + k1 + E * k2)] = v[k2];
     __syncwarp();
+    // Hermitian pairing: d_{N-l} = conj(d_l) and μ is real, so with Af = A_l/(d_l+μa),
+    // Bf = B_l/(d_l+μb) the mirror bin is X_{N-l} = conj(Af) + i conj(Bf) — one pair of complex
+    // reciprocals serves both bins.  Lane (pl, k1) handles its bins k2 < 16 and their mirrors, which
+    // live in the upper half (k2 >= 16) of lane E-k1 (itself for k1 = 0, E/2); the mirrors go
+    // through the parked slots.  Bin N/2 (lane k1 = 0, k2 = 16) is its own mirror.
 #pragma unroll
-    for (int k2 = 0; k2 < 32; ++k2) {
+    for (int k2 = 0; k2 <= 16; ++k2) {
+      if (k2 == 16 && k1 != 0) break;
       const int l = k1 + E * k2;
-      const double2 Zl = v[k2];
-      const double2 Zm = T[tpad(pl * NT + ((NT - l) & (NT - 1)))];
+      const int m = (NT - l) & (NT - 1);
+      const double2 Zl = k2 < 16 ? v[k2] : T[tpad(pl * NT + l)];
+      const double2 Zm = T[tpad(pl * NT + m)];
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
       const double2 Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
       const double2 Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
-      v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);      // X_l = Af + i Bf
+      if (k2 < 16) v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);       // X_l = Af + i Bf
+      T[tpad(pl * NT + m)] = make_double2(Af.x + Bf.y, Bf.x - Af.y);      // X_{N-l}
     }
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 16; k2 < 32; ++k2) v[k2] = T[tpad(pl * NT + k1 + E * k2)];
     __syncwarp();
     fft4_s2_to_s1<E, +1>(v, T, LOG2NT, P.tw, P.twlog, lane);
     __syncthreads();
