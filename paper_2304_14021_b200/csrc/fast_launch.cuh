@@ -33,9 +33,9 @@ template <int E>
 void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F);
 
 #ifdef PD_FAST_DEFINE
-inline size_t fast_time_smem(int E) {
-  const size_t S = 2 * (32 / E) * kFastTimeWarps, tile = (size_t)32 * E * (S + 1);
-  return std::max(tile, (size_t)kFastTimeWarps * kWarpBufD) * sizeof(double);
+inline size_t fast_time_smem(int E, int nw = kFastTimeWarps) {
+  const size_t S = 2 * (32 / E) * nw, tile = (size_t)32 * E * (S + 1);
+  return std::max(tile, (size_t)nw * kWarpBufD) * sizeof(double);
 }
 inline size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
 inline size_t fast_cols_smem(int E) {
@@ -56,12 +56,13 @@ size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * s
 template <int E>
 cudaError_t fast_attrs() {
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps>), fast_time_smem(E));
+  if (fast_time_smem(E, 8) <= 227 * 1024) PD_ATTR((k_time2d_v2<E, 8>), fast_time_smem(E, 8));
   PD_ATTR((k_rows_v2<1, E, kFastRowWarps>), fast_rows_smem());
   PD_ATTR((k_rows_v2<0, E, kFastRowWarps>), fast_rows_smem());
   PD_ATTR((k_cols_v2<1, E, fast_col_warps(E)>), fast_cols_smem(E));
   PD_ATTR((k_cols_v2<0, E, fast_col_warps(E)>), fast_cols_smem(E));
-  PD_ATTR((k_rows3<1, E, kFastRowWarps>), dtt3_rows_smem<E>());
-  PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>());
+  PD_ATTR((k_rows3<1, E, kFastRowWarps>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_cols3<1, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<0, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<1, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
@@ -78,7 +79,9 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
     if (axis == 0) {
       const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
       const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
-      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, dtt3_rows_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+      // tune 256: pad the dynamic smem so only one CTA (4 warps) fits per SM (occupancy probe)
+      const size_t smem = dtt3_rows_smem<E>() + ((L.tune & 256) ? 100 * 1024 : 0);
+      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
       constexpr int C4 = 4 * (32 / E);
       const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);
@@ -110,6 +113,13 @@ void fast_line(int neumann, int axis, const double* in, double* out, const LineP
 
 template <int E>
 void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F) {
+  if ((T.tune & 128) && fast_time_smem(E, 8) <= 227 * 1024) {   // 8-warp CTAs, one per SM (A/B)
+    constexpr int S8 = 2 * (32 / E) * 8;
+    const int64_t tiles8 = (F.ns + S8 - 1) / S8;
+    const unsigned grid8 = (unsigned)std::min<int64_t>(tiles8, 148);
+    k_time2d_v2<E, 8><<<grid8, 256, fast_time_smem(E, 8), F.stream>>>(in, out, T);
+    return;
+  }
   constexpr int S = 2 * (32 / E) * kFastTimeWarps;
   const int64_t tiles = (F.ns + S - 1) / S;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);

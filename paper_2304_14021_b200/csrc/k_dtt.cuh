@@ -49,7 +49,10 @@ struct Dtt3 {
   // Transform the P lines held in xb (line p at p*LDX, buffer index 0..M, hinged ends zero) and
   // leave the outputs in xb at p*LDO + opos(stored index).  trig[j] = (cos, sin)(πj/M), j ≤ M;
   // trig2 = (cos, sin)(2πk/M) stored at [j*E + b] for k = 32b + j.
-  PD_DEV static void transform(double* xb, const LineParams& L, const double2* __restrict__ trig2, int lane) {
+  // g scales every output (the Γ_α / Γ_α⁻¹·normalisation factor of the line's time slice when the
+  // y passes carry it for the time pass; 1 otherwise) at no extra arithmetic.
+  PD_DEV static void transform(double* xb, const LineParams& L, const double2* __restrict__ trig2, int lane,
+                               double g = 1.0) {
     double2 v[32];
     double x1p[P];
 #pragma unroll
@@ -81,6 +84,7 @@ struct Dtt3 {
     }
     __syncwarp();
     // ---- blocked split + serial prefix: lane (pl, b) owns k = 32b + j
+    const double g2 = 2.0 * g;
     double run = 0.0;
     double2 Z0 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -95,11 +99,11 @@ struct Dtt3 {
       const double Yy = Ev.y + t.x * O.y - t.y * O.x;
       double ev, a;
       if (NEUMANN) {
-        ev = 2.0 * Yx;
+        ev = g2 * Yx;
         a = k == 0 ? 0.0 : Yy;
       } else {
-        ev = -2.0 * Yy;
-        a = k == 0 ? Yx : 2.0 * Yx;
+        ev = -g2 * Yy;
+        a = k == 0 ? g * Yx : g2 * Yx;
       }
       run += a;
       v[j] = make_double2(ev, run);
@@ -120,6 +124,7 @@ struct Dtt3 {
       for (int p = 0; p < P; ++p)
         if (p == pl) x1 = x1p[p];
     }
+    const double gx1 = g * x1;
     __syncwarp();                      // every lane has read T: overwrite with the outputs
     double* ob = xb + pl * LDO;
 #pragma unroll
@@ -127,13 +132,13 @@ struct Dtt3 {
       const int q = 64 * b + 2 * j;
       if (NEUMANN) {
         ob[opos(q)] = v[j].x;                                  // X_{2k}
-        ob[opos(q + 1)] = x1 - 2.0 * (excl + v[j].y);          // X_{2k+1}
+        ob[opos(q + 1)] = fma(-g2, excl + v[j].y, gx1);        // X_{2k+1} = g(X_1 - 2 S_k)
       } else {
         ob[opos(q)] = excl + v[j].y;                           // X_{2k+1}: stored index 2k
         if (q > 0) ob[opos(q - 1)] = v[j].x;                   // X_{2k}:   stored index 2k-1
       }
     }
-    if (NEUMANN && b == E - 1) ob[opos(M)] = 2.0 * (Z0.x - Z0.y);   // X_M
+    if (NEUMANN && b == E - 1) ob[opos(M)] = g2 * (Z0.x - Z0.y);    // X_M
     __syncwarp();
   }
 };
@@ -212,6 +217,9 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     const double* src = in + L0 * L.nx;
     if ((L.tune & 1) && lane == 0 && g + gstride < ngroups)
       bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
+    // fused update: bring this group's U rows towards L2 now, they are read after the transform
+    if (L.upd && lane == 0)
+      bulk_prefetch_l2(L.upd + L0 * L.nx, (size_t)nl * L.nx * sizeof(double), L.upd + L.nlines * L.nx);
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
@@ -267,6 +275,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
   const int64_t nsl = L.nlines / L.nx;
   const int64_t ngroups = nsl * gx;
   double lmax = 0.0;
+  if (L.stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) __nanosleep(L.stagger_ns);   // see k_time2d_v2
   for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
     const int64_t n = G / gx;
     const int x0 = (int)((G - n * gx) * C);
@@ -317,7 +326,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     }
     cp_async_wait_all();
     __syncthreads();
-    D::transform(xb, L, trig2, lane);
+    D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
     __syncthreads();
     if (c_t < wcols) {
       const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r

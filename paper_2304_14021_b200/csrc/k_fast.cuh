@@ -29,6 +29,9 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   const int64_t ntiles = (P.ns + S - 1) / S;
   const double jbar = P.kind == 2 ? P.st->jbar : 0.0;
   double lmax = 0.0;
+  // two CTAs share an SM; starting the second one late puts their load and compute phases out of
+  // step, so one streams its tile while the other computes
+  if (P.stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) __nanosleep(P.stagger_ns);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t s0 = tile * S;
     if ((P.tune & 4) && tile + gridDim.x < ntiles) {      // (tune bit 2) L2 prefetch of the CTA's next tile (k_dtt.cuh)
@@ -74,7 +77,7 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int t = lane + 32 * e;
-        const double g = __ldg(P.gam + t);
+        const double g = P.gamma_folded ? 1.0 : __ldg(P.gam + t);
         v[p * E + e] = make_double2(sm[t * LD + c] * g, sm[t * LD + c + 1] * g);
       }
     }
@@ -122,9 +125,14 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int t = lane + 32 * e;
-        const double g = __ldg(P.ginv + t);
-        sm[t * LD + c] = v[p * E + e].x * g;
-        sm[t * LD + c + 1] = v[p * E + e].y * g;
+        if (P.gamma_folded) {
+          sm[t * LD + c] = v[p * E + e].x;
+          sm[t * LD + c + 1] = v[p * E + e].y;
+        } else {
+          const double g = __ldg(P.ginv + t);
+          sm[t * LD + c] = v[p * E + e].x * g;
+          sm[t * LD + c + 1] = v[p * E + e].y * g;
+        }
       }
     }
     __syncthreads();

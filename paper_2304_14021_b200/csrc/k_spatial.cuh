@@ -36,6 +36,8 @@ struct LineParams {
   int tune;              // PARADIAG_TUNE bits (A/B switches for measurements; 0 = defaults)
   double* upd;           // k_rows3 only: fused update U += out (out not stored), NULL = off
   unsigned long long* umax;   // with upd: max |U| after the update (bit-pattern max, NaN-safe)
+  const double* oscale;  // k_cols3 only: outputs of slice n scaled by oscale[n] (NULL = 1)
+  int stagger_ns;        // k_cols3: start delay of the second CTA of each SM (phase offset)
 };
 
 // buffer index of stored element e: Neumann x_e = node e; hinged x_{e+1} = interior node e+1

@@ -33,6 +33,8 @@ struct TimeParams {
   unsigned long long* amax;   // optional max |out|
   int tune;                   // PARADIAG_TUNE bits (A/B switches for measurements; 0 = defaults)
   int xoff;                   // column slab (multi-rank): global x of local column 0
+  int gamma_folded;           // k_time2d_v2: Γ_α and Γ_α⁻¹·(normalisation) applied by the y passes
+  int stagger_ns;             // k_time2d_v2: start delay of the second CTA of each SM (phase offset)
 };
 
 PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {

@@ -98,6 +98,7 @@ struct pd_handle {
   double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
   int dtt_ver = 3;                    // line kernels: 3 = k_dtt.cuh, 2 = k_fast.cuh
   int tune = 0;                       // PARADIAG_TUNE: A/B switches for measurements
+  int stagger_ns = 0;                 // PARADIAG_STAGGER: phase offset of co-resident CTAs (ns)
   // slab mode (multi-rank): rows [y0, y0+nyl) for residual / x passes / update,
   // columns [x0, x0+nxl) for the y passes and the time pass; buffers are the caller's
   bool slab = false;
@@ -260,6 +261,8 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.amax = amax;
   L.tune = h->tune;
   L.upd = upd;
+  L.oscale = nullptr;
+  L.stagger_ns = h->stagger_ns;
   L.umax = upd ? &h->st->umax_bits : nullptr;
   return L;
 }
@@ -285,8 +288,9 @@ bool fast_line_any(pd_handle* h, const double* in, double* out, int axis, const 
 }
 
 int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid,
-                 double* upd = nullptr) {
+                 double* upd = nullptr, const double* oscale = nullptr) {
   LineParams L = line_params(h, axis, amax, upd);
+  L.oscale = oscale;
   prof_begin(h, kid);
   const bool fast = h->fast && fast_line_any(h, in, out, axis, L);
   if (!fast) {
@@ -328,6 +332,8 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.lamx = h->lam;
   T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
   T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune; T.xoff = 0;
+  T.gamma_folded = 0;
+  T.stagger_ns = h->stagger_ns;
   return T;
 }
 
@@ -346,16 +352,21 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   unsigned long long* dmax = &h->st->dmax_bits;
   if (h->P.dim == 2) {
     int rc;
+    // when both the v3 column kernel and the register-FFT time pass run, the y passes carry
+    // Γ_α (forward outputs) and Γ_α⁻¹·1/(N_t (2m)²) (inverse outputs) for the time pass
+    const bool fold = h->fast && h->dtt_ver == 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
+                      h->P.nt <= 1024;
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
-    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD))) return rc;
+    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) return rc;
     TimeParams T = time_params(h, nullptr);
+    T.gamma_folded = fold ? 1 : 0;
     const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
     prof_begin(h, K_TIME);
     if (!fast_time_any(h, delta, delta, T))
       k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
     prof_end(h, K_TIME);
     PD_LAUNCHED();
-    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV))) return rc;
+    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) return rc;
     if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
     if ((rc = launch_lines(h, delta, delta, 0, dmax, K_XINV))) return rc;
     return PD_OK;
@@ -642,6 +653,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
+    if (const char* f = std::getenv("PARADIAG_STAGGER")) h->stagger_ns = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
@@ -875,8 +887,10 @@ int paradiag_slab_ypass(pd_handle* h, double* buf) {
   T.ns = L.ns;
   T.nx = h->nxl;
   T.xoff = h->x0;
+  T.gamma_folded = 1;
   const int nm = h->neumann ? 1 : 0;
   auto yline = [&](int kid) {
+    L.oscale = kid == K_YFWD ? h->gam : h->ginv;
     prof_begin(h, kid);
     switch (L.M) {
       case 64: fast_line<1>(nm, 1, buf, buf, L, F); break;
