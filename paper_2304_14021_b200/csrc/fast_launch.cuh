@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "k_dtt.cuh"
+#include "k_dttp.cuh"
 #include "k_fast.cuh"
 
 namespace pd {
@@ -22,7 +23,8 @@ struct FastLaunch {
   int nx;                 // points per row (square grids)
   int64_t ns;             // points per slice
   const double2* trig2;   // k_dtt.cuh split table
-  int dtt_ver;            // 3 = k_dtt.cuh, 2 = k_fast.cuh line kernels
+  const double2* trig2p;  // k_dttp.cuh split table (M = 2048 only)
+  int dtt_ver;            // 4 = k_dttp.cuh (M = 2048), 3 = k_dtt.cuh, 2 = k_fast.cuh line kernels
 };
 
 template <int E>
@@ -42,6 +44,9 @@ inline size_t fast_cols_smem(int E) {
   const size_t nw = fast_col_warps(E);
   return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
 }
+constexpr int kPairsPerRowCta = 2;
+inline size_t dttp_rows_smem() { return (size_t)kPairsPerRowCta * DttPair<1>::BUF * sizeof(double); }
+inline size_t dttp_cols_smem() { return (size_t)8 * DttPair<1>::BUF * sizeof(double); }
 template <int E>
 size_t dtt3_rows_smem() { return (size_t)kFastRowWarps * Dtt3<1, E>::BUF * sizeof(double); }
 template <int E>
@@ -65,6 +70,12 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_cols3<1, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<0, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
+  if (E == 32) {
+    PD_ATTR((k_rows4<1, kPairsPerRowCta>), dttp_rows_smem());
+    PD_ATTR((k_rows4<0, kPairsPerRowCta>), dttp_rows_smem());
+    PD_ATTR((k_cols4<1>), dttp_cols_smem());
+    PD_ATTR((k_cols4<0>), dttp_cols_smem());
+  }
   PD_ATTR((k_cols3<1, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
   PD_ATTR((k_cols3<0, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
   return cudaSuccess;
@@ -75,7 +86,18 @@ template <int NEUMANN, int E>
 void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F) {
   constexpr int NW = fast_col_warps(E);
   const int C = NW * (32 / E);
-  if (F.dtt_ver == 3) {
+  if (E == 32 && F.dtt_ver >= 4 && F.trig2p) {
+    if (axis == 0) {
+      const unsigned grid = (unsigned)std::min<int64_t>((L.nlines + kPairsPerRowCta - 1) / kPairsPerRowCta, 148 * 4);
+      k_rows4<NEUMANN, kPairsPerRowCta><<<grid, kPairsPerRowCta * 64, dttp_rows_smem(), F.stream>>>(in, out, L, F.trig2p);
+    } else {
+      const int64_t groups = (int64_t)F.nt * ((F.nx + 7) / 8);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+      k_cols4<NEUMANN><<<grid, 512, dttp_cols_smem(), F.stream>>>(in, out, L, F.trig2p);
+    }
+    return;
+  }
+  if (F.dtt_ver >= 3) {
     if (axis == 0) {
       const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
       const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);

@@ -96,7 +96,10 @@ struct pd_handle {
   double2* tw = nullptr;
   double2* trig = nullptr;
   double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
-  int dtt_ver = 3;                    // line kernels: 3 = k_dtt.cuh, 2 = k_fast.cuh
+  double2* trig2p = nullptr;         // (cos, sin)(2πk/M) in the [j][t] layout of k_dttp.cuh (M = 2048)
+  // line kernels: 3 = k_dtt.cuh (default), 4 = k_dttp.cuh warp pairs for M = 2048 (opt-in: ncu d5b shows
+  // it shared-memory bound, 12.2 vs 10.6 ms), 2 = k_fast.cuh
+  int dtt_ver = 3;
   int tune = 0;                       // PARADIAG_TUNE: A/B switches for measurements
   int stagger_ns = 0;                 // PARADIAG_STAGGER: phase offset of co-resident CTAs (ns)
   // slab mode (multi-rank): rows [y0, y0+nyl) for residual / x passes / update,
@@ -270,6 +273,7 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
 FastLaunch fast_launch(pd_handle* h) {
   FastLaunch F;
   F.stream = h->stream; F.nt = h->P.nt; F.nx = h->nx; F.ns = h->ns; F.trig2 = h->trig2; F.dtt_ver = h->dtt_ver;
+  F.trig2p = h->trig2p;
   return F;
 }
 
@@ -354,7 +358,7 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     int rc;
     // when both the v3 column kernel and the register-FFT time pass run, the y passes carry
     // Γ_α (forward outputs) and Γ_α⁻¹·1/(N_t (2m)²) (inverse outputs) for the time pass
-    const bool fold = h->fast && h->dtt_ver == 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
+    const bool fold = h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
                       h->P.nt <= 1024;
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) return rc;
@@ -558,6 +562,9 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     const int b = k / 32, j = k % 32;
     trig2[(size_t)j * E2 + b] = trig[std::min(2 * k, M)];
   }
+  // k_dttp.cuh (M = 2048): k = 16t + j stored at j*64 + t
+  std::vector<double2> trig2p(M == 2048 ? 1024 : 0);
+  for (int k = 0; k < (int)trig2p.size(); ++k) trig2p[(size_t)(k % 16) * 64 + k / 16] = trig[2 * k];
 
   // ---- singularity check of d_l + μ (linear kinds): only l = 0 and N_t/2 have real d_l
   if (p->kind != PD_CAHN_HILLIARD) {
@@ -587,6 +594,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
   PD_TRY(dalloc(h, &h->trig2, (size_t)H2));
+  if (!trig2p.empty()) PD_TRY(dalloc(h, &h->trig2p, trig2p.size()));
   PD_TRY(dalloc(h, &h->st, 1));
   {
     cudaError_t e = cudaMallocHost(&h->st_host, sizeof(DevStats));
@@ -602,7 +610,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
       up(h->dl, dl.data(), nt * sizeof(double2)) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
       up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
-      up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)))
+      up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)) ||
+      (!trig2p.empty() && up(h->trig2p, trig2p.data(), trig2p.size() * sizeof(double2))))
     return cleanup(fail(PD_ECUDA, "table upload failed"));
 
   if (p->dim == 1) {

@@ -35,6 +35,9 @@ CASES = {
     "c3_m256_nt64": twin("c3", m=256, nt=64),
     "c4_m64_nt32": twin("c4", m=64, nt=32, t_window=32e-4, n_windows=1),
     "c5_m64_nt256": twin("c5", m=64, nt=256),
+    # c5's line length (M = 2048: the warp-pair transform of k_dttp.cuh), both BCs
+    "c5_m2048_nt4": twin("c5", m=2048, nt=4),
+    "c3_m2048_nt2": twin("c3", m=2048, nt=2),
 }
 
 
@@ -89,6 +92,19 @@ def test_solve_parity(cuda_lib, name):
     if p.fixed_iters is None:
         assert info.converged == int(all(conv_o))
         assert rc == (0 if all(conv_o) else 1)
+
+
+@pytest.mark.parametrize("name", ["c5_m2048_nt4", "c3_m2048_nt2"])
+def test_precond_parity_warp_pair_lines(cuda_lib, name, monkeypatch):
+    """The opt-in warp-pair line transform (PARADIAG_DTT=4, k_dttp.cuh) for M = 2048."""
+    monkeypatch.setenv("PARADIAG_DTT", "4")
+    p = CASES[name]
+    r = _rand_U(p, 12)
+    s = cuda_lib.Solver(p)
+    d = s.empty()
+    s.apply_precond(to_dev(r, p), d, 0.0)
+    d_o, _ = precond.apply_precond(p, r, 0.0)
+    assert rel_err(to_host(d, p), d_o) <= 1e-11
 
 
 def test_solve_host_matches_device(cuda_lib):
