@@ -108,8 +108,8 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
-      const double2 Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
-      const double2 Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
+      const double2 Af = cmul(A, cinv_fast(shifted(d, P.el, l, mua)));
+      const double2 Bf = cmul(B, cinv_fast(shifted(d, P.el, l, mub)));
       if (k2 < 16) v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);       // X_l = Af + i Bf
       T[tpad(pl * NT + m)] = make_double2(Af.x + Bf.y, Bf.x - Af.y);      // X_{N-l}
     }

@@ -1,5 +1,6 @@
 // k_penta.cuh — 1D Step-(2): for every frequency bin l, solve the complex pentadiagonal
-// system (d_l I + A) x = ŝ_l (θ = 1, e_l = 1) by LU without pivoting plus one refinement step whose
+// system (d_l I + e_l A) x = ŝ_l (e_l = θ + (1-θ) z ω^l, = 1 for θ = 1) by LU without pivoting plus
+// one refinement step whose
 // residual uses the nested operator A x = L(L x) or β² L x + ε² L(L x) (R#15; SURVEY probe p10).
 // One thread per bin; bins are the fastest-varying index of spec[x][l] so loads coalesce.
 #pragma once
@@ -15,6 +16,7 @@ struct PentaParams {
   double inv_h2, b2, e2;
   const double* band;    // 5 x n real bands of assembled A: [a2 | a1 | a0 | c1 | c2]
   const double2* dl;     // d_l
+  const double2* el;     // e_l (NULL: θ = 1, e_l = 1)
   double2 *l1, *l2, *iu0, *u1;   // factors [n][nb]
 };
 
@@ -23,6 +25,7 @@ __global__ void k_penta_factor(PentaParams P) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= P.nb) return;
   const double2 d = P.dl[l];
+  const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
   const int n = P.n;
   const double* a2 = P.band;
   const double* a1 = P.band + n;
@@ -30,20 +33,20 @@ __global__ void k_penta_factor(PentaParams P) {
   const double* c1 = P.band + 3 * n;
   const double* c2 = P.band + 4 * n;
   double2 u0m1 = {0, 0}, u0m2 = {0, 0}, u1m1 = {0, 0}, u1m2 = {0, 0};
-  double u2m1 = 0.0, u2m2 = 0.0;
+  double2 u2m1 = {0, 0}, u2m2 = {0, 0};
   for (int i = 0; i < n; ++i) {
     double2 L2 = {0, 0}, L1 = {0, 0};
-    if (i >= 2) L2 = cmul(make_double2(a2[i], 0.0), cinv(u0m2));
+    if (i >= 2) L2 = cmul(cscale(e, a2[i]), cinv(u0m2));
     if (i >= 1) {
-      double2 num = make_double2(a1[i], 0.0);
+      double2 num = cscale(e, a1[i]);
       if (i >= 2) num = csub(num, cmul(L2, u1m2));
       L1 = cmul(num, cinv(u0m1));
     }
-    double2 U0 = make_double2(d.x + a0[i], d.y);
-    if (i >= 2) U0 = csub(U0, cscale(L2, u2m2));
+    double2 U0 = cadd(d, cscale(e, a0[i]));
+    if (i >= 2) U0 = csub(U0, cmul(L2, u2m2));
     if (i >= 1) U0 = csub(U0, cmul(L1, u1m1));
-    double2 U1 = make_double2(c1[i], 0.0);
-    if (i >= 1) U1 = csub(U1, cscale(L1, u2m1));
+    double2 U1 = cscale(e, c1[i]);
+    if (i >= 1) U1 = csub(U1, cmul(L1, u2m1));
     const size_t o = (size_t)i * P.nb + l;
     P.l1[o] = L1;
     P.l2[o] = L2;
@@ -51,7 +54,7 @@ __global__ void k_penta_factor(PentaParams P) {
     P.u1[o] = U1;
     u0m2 = u0m1; u0m1 = U0;
     u1m2 = u1m1; u1m1 = U1;
-    u2m2 = u2m1; u2m1 = c2[i];
+    u2m2 = u2m1; u2m1 = cscale(e, c2[i]);
   }
 }
 
@@ -59,6 +62,7 @@ __global__ void k_penta_factor(PentaParams P) {
 PD_DEV void penta_lu_solve(double2* v, int l, const PentaParams& P) {
   const int n = P.n, nb = P.nb;
   const double* c2 = P.band + 4 * n;
+  const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
   double2 y1 = {0, 0}, y2 = {0, 0};
   for (int i = 0; i < n; ++i) {
     const size_t o = (size_t)i * nb + l;
@@ -73,7 +77,7 @@ PD_DEV void penta_lu_solve(double2* v, int l, const PentaParams& P) {
     const size_t o = (size_t)i * nb + l;
     double2 x = v[o];
     x = csub(x, cmul(P.u1[o], x1));
-    x = csub(x, cscale(x2, c2[i]));
+    x = csub(x, cscale(cmul(e, x2), c2[i]));
     x = cmul(x, P.iu0[o]);
     v[o] = x;
     x2 = x1; x1 = x;
@@ -95,6 +99,7 @@ __global__ void k_penta_solve(double2* spec, double2* w1, double2* w2, PentaPara
   if (l >= P.nb) return;
   const int n = P.n, nb = P.nb;
   const double2 d = P.dl[l];
+  const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
   // x = (LU)^{-1} s
   for (int i = 0; i < n; ++i) w1[(size_t)i * nb + l] = spec[(size_t)i * nb + l];
   penta_lu_solve(w1, l, P);
@@ -119,7 +124,8 @@ __global__ void k_penta_solve(double2* spec, double2* w1, double2* w2, PentaPara
     const size_t o = (size_t)i * nb + l;
     const double2 x = w1[o], s = spec[o];
     const double2 dx = cmul(d, x);
-    w2[o] = make_double2(s.x - (dx.x + Ax.x), s.y - (dx.y + Ax.y));
+    const double2 eAx = P.el ? cmul(e, Ax) : Ax;
+    w2[o] = make_double2(s.x - (dx.x + eAx.x), s.y - (dx.y + eAx.y));
     lm = lc; lc = lp;
   }
   penta_lu_solve(w2, l, P);

@@ -14,6 +14,8 @@ struct ResidualParams {
   double inv_h2;        // m² exactly
   double inv_dt;        // nt / T
   double b2, e2;        // fl(β·β), fl(ε·ε)
+  double theta;         // θ-method: r_n = -(U_n - U_{n-1})/Δt - A(θU_n + (1-θ)U_{n-1}) as
+                        // θ·AU_n + (1-θ)·AU_{n-1} (the oracle's order); 1 = backward Euler
   // row slab of a multi-rank run (k_residual_tile only): local rows are global rows
   // [y0g, y0g + ny); rows y0g-2, y0g-1 come from hlo [nt][2][nx], rows y0g+ny, +1 from hhi.
   // Single GPU: y0g = 0, nyg = ny, no halo buffers.
@@ -99,17 +101,20 @@ k_residual(const double* __restrict__ u0, const double* __restrict__ U, double* 
       out = lv - dtime;
       jloc = 3.0 * uc * uc - 1.0;
     } else {
-      const double lC = lap_at(s, x, y, P);
-      const double lWE = lap_g(s, x - 1, y, P) + lap_g(s, x + 1, y, P);
-      double llap;
-      if (P.dim == 1) {
-        llap = (lWE - 2.0 * lC) * P.inv_h2;
-      } else {
-        const double lSN = lap_g(s, x, y - 1, P) + lap_g(s, x, y + 1, P);
-        llap = ((lWE + lSN) - 4.0 * lC) * P.inv_h2;
-      }
-      const double Au = P.kind == 0 ? llap : P.b2 * lC + P.e2 * llap;
-      out = -dtime - Au;
+      auto applyA = [&](const double* q) {
+        const double lC = lap_at(q, x, y, P);
+        const double lWE = lap_g(q, x - 1, y, P) + lap_g(q, x + 1, y, P);
+        double llap;
+        if (P.dim == 1) {
+          llap = (lWE - 2.0 * lC) * P.inv_h2;
+        } else {
+          const double lSN = lap_g(q, x, y - 1, P) + lap_g(q, x, y + 1, P);
+          llap = ((lWE + lSN) - 4.0 * lC) * P.inv_h2;
+        }
+        return P.kind == 0 ? llap : P.b2 * lC + P.e2 * llap;
+      };
+      const double Au = applyA(s);
+      out = P.theta == 1.0 ? -dtime - Au : -dtime - (P.theta * Au + (1.0 - P.theta) * applyA(sp));
     }
     r[(size_t)n * ns + idx] = out;
   }
@@ -286,6 +291,7 @@ constexpr int kResPer = (kResUN + kResThreads - 1) / kResThreads;
 constexpr int kResOut = kResTY * kResTX / kResThreads;      // outputs per thread
 constexpr size_t kResSmem = (2 * (size_t)kResUY * kResUP + (size_t)kResIY * kResIP) * sizeof(double);
 
+template <bool THETA>     // THETA: θ < 1 (A U_{n-1} term); false compiles the backward-Euler kernel
 __global__ void __launch_bounds__(kResThreads)
 k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
                 ResidualParams P, double* __restrict__ jpart) {
@@ -323,11 +329,12 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     sgn[k] = sy * sg;
   }
   const size_t hstride = 2 * (size_t)P.nx;
-  auto stage = [&](double* dst, int n) {
+  auto stage = [&](double* dst, int n) {           // n = -1: u0 (single-GPU θ-method warm-up)
 #pragma unroll
     for (int k = 0; k < kResPer; ++k)
       if (soff[k] >= 0) {
-        const double* b = ssel[k] == 0 ? U + (size_t)n * ns : (ssel[k] == 1 ? P.hlo : P.hhi) + (size_t)n * hstride;
+        const double* b = ssel[k] == 0 ? (n < 0 ? u0 : U + (size_t)n * ns)
+                                       : (ssel[k] == 1 ? P.hlo : P.hhi) + (size_t)n * hstride;
         cp_async8(dst + dpos[k], b + soff[k]);
       }
     cp_async_commit();
@@ -352,10 +359,17 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     }
   }
   double jloc = 0.0;
-  stage(sU0, n0);
-  for (int n = n0; n < n1; ++n) {
-    double* cur = ((n - n0) & 1) ? sU1 : sU0;
-    double* nxt = ((n - n0) & 1) ? sU0 : sU1;
+  // θ < 1 needs A U_{n-1}: march one extra (output-free) slice n0-1 first; A U_n of every slice
+  // is then carried to the next in registers like U_{n-1}
+  constexpr bool thet = THETA;
+  const int nstart = thet ? n0 - 1 : n0;
+  double prevA[kResOut];
+#pragma unroll
+  for (int j = 0; j < kResOut; ++j) prevA[j] = 0.0;
+  stage(sU0, nstart);
+  for (int n = nstart; n < n1; ++n) {
+    double* cur = ((n - nstart) & 1) ? sU1 : sU0;
+    double* nxt = ((n - nstart) & 1) ? sU0 : sU1;
     cp_async_wait_all();
     fix_signs(cur);
     __syncthreads();                       // cur staged; previous slice done with nxt and sI
@@ -368,7 +382,7 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
       sI[iy * kResIP + ix] = ch ? uc * uc * uc - uc - P.e2 * Lr : Lr;
     }
     __syncthreads();
-    double* rn = r + (size_t)n * ns;
+    double* rn = r + (size_t)max(n, 0) * ns;
 #pragma unroll
     for (int j = 0; j < kResOut; ++j) {
       const int ty = ty0 + j * (kResThreads / kResTX);
@@ -381,12 +395,13 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
         double out;
         if (ch) {
           out = outer - dtime;
-          jloc += 3.0 * uo * uo - 1.0;
+          if (n >= n0) jloc += 3.0 * uo * uo - 1.0;
         } else {
           const double Au = P.kind == 0 ? outer : P.b2 * I[0] + P.e2 * outer;
-          out = -dtime - Au;
+          out = thet ? -dtime - (P.theta * Au + (1.0 - P.theta) * prevA[j]) : -dtime - Au;
+          prevA[j] = Au;
         }
-        rn[(size_t)gy * P.nx + gx] = out;
+        if (n >= n0) rn[(size_t)gy * P.nx + gx] = out;
       }
       prev[j] = uo;
     }

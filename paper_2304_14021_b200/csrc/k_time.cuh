@@ -24,6 +24,7 @@ struct TimeParams {
   const double* gam;     // γ_j
   const double* ginv;    // scale / γ_j
   const double2* dl;     // d_l = (1 - z ω^l)/Δt, l = 0..nt-1
+  const double2* el;     // e_l = θ + (1-θ) z ω^l (θ-method); NULL for θ = 1 (e_l = 1)
   const double* lamx;    // Laplacian eigenvalues along x (and y: same table, square grids)
   int kind;              // 0 biharmonic, 1 linear CH, 2 CH
   double b2, e2;
@@ -36,6 +37,13 @@ struct TimeParams {
   int gamma_folded;           // k_time2d_v2: Γ_α and Γ_α⁻¹·(normalisation) applied by the y passes
   int stagger_ns;             // k_time2d_v2: start delay of the second CTA of each SM (phase offset)
 };
+
+// shifted eigenvalue d_l + e_l μ of the Step-(2) system
+PD_DEV double2 shifted(double2 d, const double2* el, int l, double mu) {
+  if (!el) return make_double2(d.x + mu, d.y);
+  const double2 e = __ldg(el + l);
+  return make_double2(d.x + e.x * mu, d.y + e.y * mu);
+}
 
 PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {
   const int64_t q = s / P.nx, p = s - q * P.nx;
@@ -107,8 +115,8 @@ k_time_solve_2d(const double* in, double* out, TimeParams P) {
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
-      const double2 fa = cinv(make_double2(d.x + mua, d.y));
-      const double2 fb = cinv(make_double2(d.x + mub, d.y));
+      const double2 fa = cinv(shifted(d, P.el, l, mua));
+      const double2 fb = cinv(shifted(d, P.el, l, mub));
       const double2 Af = cmul(A, fa), Bf = cmul(B, fb);
       // X_l = Af + i Bf ; X_{N-l} = conj(Af) + i conj(Bf)
       buf[pl] = make_double2(Af.x - Bf.y, Af.y + Bf.x);

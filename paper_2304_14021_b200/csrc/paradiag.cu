@@ -92,6 +92,7 @@ struct pd_handle {
   double* gam = nullptr;
   double* ginv = nullptr;
   double2* dl = nullptr;
+  double2* el = nullptr;              // e_l = θ + (1-θ) z ω^l (NULL for θ = 1)
   double* lam = nullptr;
   double2* tw = nullptr;
   double2* trig = nullptr;
@@ -175,7 +176,10 @@ int validate(const pd_problem* p) {
     return fail(PD_EINVAL, "2D: m (intervals per axis) must be a power of two in [4, 4096]");
   if (p->dim == 1 && (p->m < 4 || p->m > (1 << 20))) return fail(PD_EINVAL, "1D: m must be in [4, 2^20]");
   if (!(p->alpha > 0.0 && p->alpha < 1.0)) return fail(PD_EINVAL, "alpha must be in (0, 1) (P:308)");
-  if (p->theta != 1.0) return fail(PD_EINVAL, "theta = 1 (backward Euler) only");
+  if (!(p->theta >= 0.5 && p->theta <= 1.0))
+    return fail(PD_EINVAL, "theta must be in [1/2, 1] (theta-method, P:119-126; A-stable range)");
+  if (p->kind == PD_CAHN_HILLIARD && p->theta != 1.0)
+    return fail(PD_EINVAL, "Cahn-Hilliard PinT-I is backward Euler (theta = 1, P:440-451)");
   if (!(p->t_window > 0.0) || !std::isfinite(p->t_window)) return fail(PD_EINVAL, "t_window must be > 0");
   if (!(p->eps >= 0.0)) return fail(PD_EINVAL, "eps must be >= 0");
   if (p->fixed_iters <= 0 && !(p->tol > 0.0)) return fail(PD_EINVAL, "tol must be > 0");
@@ -225,17 +229,18 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
-  R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr;
+  R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr; R.theta = h->P.theta;
   prof_begin(h, K_RESIDUAL);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
   if (h->P.dim == 2) {
-    if (h->tune & 32) {     // previous row-streaming kernel (A/B)
+    if ((h->tune & 32) && h->P.theta == 1.0) {     // previous row-streaming kernel (A/B)
       dim3 grd((h->nx + kResStrip - 1) / kResStrip, h->P.nt);
       k_residual_2d<<<grd, 128, 0, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y;
     } else {
       dim3 grd((h->nx + kResTX - 1) / kResTX, (h->ny + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-      k_residual_tile<<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      if (h->P.theta != 1.0) k_residual_tile<true><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else k_residual_tile<false><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y * grd.z;
     }
   } else {
@@ -333,7 +338,7 @@ bool fast_time_any(pd_handle* h, const double* in, double* out, const TimeParams
 TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   TimeParams T;
   T.nt = h->P.nt; T.log2nt = h->log2nt; T.ns = h->ns; T.nx = h->nx;
-  T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.lamx = h->lam;
+  T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.el = h->el; T.lamx = h->lam;
   T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
   T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune; T.xoff = 0;
   T.gamma_folded = 0;
@@ -384,7 +389,7 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   PD_LAUNCHED();
   PentaParams PP;
   PP.n = h->nx; PP.nb = h->nb; PP.neumann = h->neumann; PP.kind = h->P.kind;
-  PP.inv_h2 = h->inv_h2; PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl;
+  PP.inv_h2 = h->inv_h2; PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl; PP.el = h->el;
   const size_t nf = (size_t)h->nx * h->nb;
   PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
   prof_begin(h, K_PENTA);
@@ -532,7 +537,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   // ---- host tables (closed forms P:156; readings R#1, R#2, R#11)
   const int nt = p->nt;
   std::vector<double> gam(nt), ginv(nt), lam(h->nx);
-  std::vector<double2> dl(nt), tw(size_t(1) << h->twlog), trig(M + 1);
+  std::vector<double2> dl(nt), el(nt), tw(size_t(1) << h->twlog), trig(M + 1);
   const double lna = std::log(p->alpha);
   const double z = std::exp(lna / nt);
   const double spatial_scale = p->dim == 2 ? 1.0 / ((2.0 * M) * (2.0 * M)) : 1.0;
@@ -543,6 +548,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   for (int l = 0; l < nt; ++l) {
     const double ang = 2.0 * M_PI * l / nt;
     dl[l] = make_double2((1.0 - z * std::cos(ang)) * h->inv_dt, (z * std::sin(ang)) * h->inv_dt);
+    el[l] = make_double2(p->theta + (1.0 - p->theta) * z * std::cos(ang), -(1.0 - p->theta) * z * std::sin(ang));
   }
   for (int i = 0; i < h->nx; ++i) {
     const int pidx = h->neumann ? i : i + 1;
@@ -574,7 +580,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
         for (int j = 0; j < (p->dim == 2 ? h->ny : 1); ++j) {
           const double Lam = lam[i] + (p->dim == 2 ? lam[j] : 0.0);
           const double mu = mu_of(p, Lam, h->b2, h->e2);
-          const double den = std::hypot(dl[l].x + mu, dl[l].y) / (std::fabs(dl[l].x) + std::fabs(mu) + 1e-300);
+          const double den = std::hypot(dl[l].x + el[l].x * mu, dl[l].y + el[l].y * mu) /
+                             (std::fabs(dl[l].x) + std::fabs(mu) + 1e-300);
           worst = std::min(worst, den);
         }
     }
@@ -590,6 +597,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   PD_TRY(dalloc(h, &h->gam, nt));
   PD_TRY(dalloc(h, &h->ginv, nt));
   PD_TRY(dalloc(h, &h->dl, nt));
+  if (p->theta != 1.0) PD_TRY(dalloc(h, &h->el, nt));
   PD_TRY(dalloc(h, &h->lam, h->nx));
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
@@ -608,7 +616,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
-      up(h->dl, dl.data(), nt * sizeof(double2)) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
+      up(h->dl, dl.data(), nt * sizeof(double2)) || (h->el && up(h->el, el.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
       up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
       up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)) ||
       (!trig2p.empty() && up(h->trig2p, trig2p.data(), trig2p.size() * sizeof(double2))))
@@ -646,7 +654,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     if (up(h->band, band.data(), band.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "band upload"));
     PentaParams PP;
     PP.n = n; PP.nb = h->nb; PP.neumann = h->neumann; PP.kind = p->kind; PP.inv_h2 = h->inv_h2;
-    PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl;
+    PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl; PP.el = h->el;
     PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
     k_penta_factor<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(PP);
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(PD_ECUDA, "penta factor launch"));
@@ -658,7 +666,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
-    PD_TRY(allow_smem(k_residual_tile, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<false>, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<true>, kResSmem));
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
@@ -814,8 +823,8 @@ int paradiag_init_slab(const pd_problem* p, int device, void* cuda_stream, int64
   *out = nullptr;
   int rc = validate(p);
   if (rc) return rc;
-  if (p->dim != 2 || p->kind == PD_CAHN_HILLIARD)
-    return fail(PD_EINVAL, "slab mode: 2D linear kinds only (CH runs as replicas, DESIGN.md §8)");
+  if (p->dim != 2 || p->kind == PD_CAHN_HILLIARD || p->theta != 1.0)
+    return fail(PD_EINVAL, "slab mode: 2D linear kinds with theta = 1 (CH runs as replicas, DESIGN.md §8)");
   if (p->m < 64 || p->m > 2048 || p->nt < 32 || p->nt > 1024)
     return fail(PD_EINVAL, "slab mode: needs the register-FFT sizes (64 <= m <= 2048, 32 <= nt <= 1024)");
   int nx, ny;
@@ -854,10 +863,10 @@ int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, 
   R.nx = h->nx; R.ny = h->nyl; R.nt = h->P.nt; R.dim = 2;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
-  R.y0g = h->y0; R.nyg = h->ny; R.hlo = halo_lo; R.hhi = halo_hi;
+  R.y0g = h->y0; R.nyg = h->ny; R.hlo = halo_lo; R.hhi = halo_hi; R.theta = 1.0;
   prof_begin(h, K_RESIDUAL);
   dim3 grd((h->nx + kResTX - 1) / kResTX, (h->nyl + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-  k_residual_tile<<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
+  k_residual_tile<false><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
   prof_end(h, K_RESIDUAL);
   PD_LAUNCHED();
   return PD_OK;

@@ -48,13 +48,20 @@ def test_workspace_bytes_all_configs(lib, name):
 
 
 @pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=100), dict(nt=1),
-                                 dict(theta=0.5), dict(m=100), dict(eps=-1.0), dict(t_window=0.0),
+                                 dict(theta=0.4), dict(theta=1.1), dict(m=100), dict(eps=-1.0), dict(t_window=0.0),
                                  dict(kind="cahn_hilliard"), dict(n_windows=0), dict(tol=0.0)])
 def test_invalid_problems_rejected(lib, bad):
     p = pd.make_problem(config("c3"), **bad)
     with pytest.raises(pd.ParadiagError) as e:
         pd.paradiag_workspace_bytes(p)
     assert e.value.code == pd.PD_EINVAL
+
+
+def test_theta_half_accepted_but_not_for_ch(lib):
+    """θ-method: θ ∈ [1/2, 1] for the linear kinds; CH PinT-I is backward Euler."""
+    assert pd.paradiag_workspace_bytes(pd.make_problem(config("c3"), theta=0.5)) > 0
+    with pytest.raises(pd.ParadiagError):
+        pd.paradiag_workspace_bytes(pd.make_problem(config("c4"), theta=0.5))
 
 
 def test_ch_requires_2d_neumann(lib):

@@ -35,6 +35,12 @@ CASES = {
     "c3_m256_nt64": twin("c3", m=256, nt=64),
     "c4_m64_nt32": twin("c4", m=64, nt=32, t_window=32e-4, n_windows=1),
     "c5_m64_nt256": twin("c5", m=64, nt=256),
+    # θ = ½ (trapezoid, NEXT-2): e_l ≠ 1 in Step-(2), (1-θ)A U_{n-1} in the residual
+    "c1_theta": replace(config("c1"), theta=0.5),
+    "c2_theta": twin("c2", m=63, nt=16, theta=0.5),
+    "c3_theta": twin("c3", m=64, nt=32, theta=0.5),
+    "c5_theta": twin("c5", m=64, nt=64, theta=0.5),
+    "c5_theta_nt8": twin("c5", m=16, nt=8, theta=0.5),
     # c5's line length (M = 2048: the warp-pair transform of k_dttp.cuh), both BCs
     "c5_m2048_nt4": twin("c5", m=2048, nt=4),
     "c3_m2048_nt2": twin("c3", m=2048, nt=2),

@@ -28,6 +28,25 @@ def test_c1_closed_form_and_count():
     assert abs((1.0 + (p.t_window / p.nt) * mu1) ** -32 - g["factor_n32"]) <= 1e-16
 
 
+def test_c1_trapezoid_closed_form():
+    """θ = ½ (NEXT-2): sin(πx) stays an eigenvector, so the converged all-at-once solution
+    is u_n = R_{1/2}(Δtμ₁)^n sin(πx) with the trapezoid stability function R_{1/2}(z) =
+    (1 - z/2)/(1 + z/2) — a closed form independent of the circulant machinery."""
+    from dataclasses import replace
+    g = json.load(open(os.path.join(GOLD, "c1_closed_form.json")))
+    p = replace(config("c1"), theta=0.5)
+    m = p.m
+    z = (p.t_window / p.nt) * g["mu1"]
+    R = (1.0 - 0.5 * z) / (1.0 + 0.5 * z)
+    assert 0.0 < R < 1.0
+    U, iters, conv, _ = iterate.solve(p, make_u0(p))
+    assert conv == [True]
+    x = np.arange(1, m) / m
+    n = np.arange(1, p.nt + 1)[:, None]
+    cf = R ** n * np.sin(np.pi * x)[None, :]
+    assert np.abs(U - cf).max() <= 1e-12 * np.abs(cf).max()
+
+
 def test_c2_fixed_point_is_sequential_solution():
     """Converged all-at-once solution = sequential BE: exact mode-wise and banded-LU stepping."""
     p = config("c2")
