@@ -42,9 +42,30 @@ def residual_ch(prob, u0: np.ndarray, U: np.ndarray):
     return r, jbar
 
 
+def residual_ch_eyre(prob, u0: np.ndarray, U: np.ndarray):
+    """PinT-II (NEXT-1): Eyre's splitting treats the convex part u³ implicitly and the
+    concave -u explicitly, u_n - u_{n-1} = Δt(Δ_h u_n³ - Δ_h u_{n-1} - ε²Δ_h² u_n).  The
+    defect of the sequential scheme (= -Q(U) with the α-terms cancelled) in nested form:
+        r_n = (Δ_h(U_n³ - ε²Δ_h U_n) - Δ_h U_{n-1}) - (U_n - U_{n-1})/Δt,   U_0 := u0,
+    and the averaged Jacobian of the implicit part J̄₃ = mean(3U²) (R#8 reading of J̃)."""
+    _, e2 = spatial.coeffs(prob)
+    Uprev = _shift_prev(u0, U)
+    v = U * U * U - e2 * spatial.lap(U, prob.m, prob.bc, prob.dim)
+    r = (spatial.lap(v, prob.m, prob.bc, prob.dim) - spatial.lap(Uprev, prob.m, prob.bc, prob.dim)) - \
+        (U - Uprev) * circulant.inv_dt(prob)
+    jbar = float(np.mean(3.0 * U * U))
+    return r, jbar
+
+
+def is_ch(prob) -> bool:
+    return prob.kind in ("cahn_hilliard", "cahn_hilliard_eyre")
+
+
 def residual(prob, u0, U):
     if prob.kind == "cahn_hilliard":
         return residual_ch(prob, u0, U)
+    if prob.kind == "cahn_hilliard_eyre":
+        return residual_ch_eyre(prob, u0, U)
     return residual_linear(prob, u0, U), 0.0
 
 
@@ -60,7 +81,7 @@ def iterate_once(prob, u0, U):
     r, jbar = residual(prob, u0, U)
     delta, imag = precond.apply_precond(prob, r, jbar)
     dmax = float(np.abs(delta).max())
-    if prob.kind == "cahn_hilliard":
+    if is_ch(prob):
         omega = min(prob.omega, prob.tau / dmax) if dmax > 0 else prob.omega
     else:
         omega = prob.omega

@@ -8,6 +8,11 @@ Cahn-Hilliard PinT-I, P:491-499 (eq. pintiter_CH): Step-(2) matrix
   λ_{1,l} I - Δ_h J̃ + Δ_h + ε²Δ_h²  with J̃ = J̄₃·I (scalar space-time mean of 3u², R#7/R#8),
   i.e. d_l I - J̄ Δ_h + ε² Δ_h² with J̄ = mean(3u² - 1).
 
+Cahn-Hilliard PinT-II (Eyre splitting), P:537-545 (eq. pintiter_CH_eyre): Step-(2) matrix
+  λ_{1,l} I - Δ_h J̃ + λ_{3,l} Δ_h + ε²Δ_h²,  λ_{3,l} = α^{1/N_t} e^{-2πil/N_t} (the eigenvalues of
+  C3^(α) = C2^(α) at θ = 0), J̃ = J̄₃·I with J̄₃ = mean(3u²) (R#8); on the DCT modes the divisor is
+  d_l + z ω^l Λ - J̄₃ Λ + ε² Λ².
+
 Step-(2) solvers (a library primitive may serve as a step):
   1D: banded LU with partial pivoting (LAPACK gbsv via scipy.linalg.solve_banded) of the assembled
       pentadiagonal, then iterative refinement whose residual is evaluated in nested form (R#15)
@@ -34,9 +39,9 @@ def _step2_operator_nested(prob, jbar):
 
 
 def _step2_mu(prob, jbar):
-    """Eigenvalue of A_eff on the mode grid."""
+    """Eigenvalue of A_eff on the mode grid (the l-independent part for PinT-II)."""
     Lam = spatial.Lam_grid(prob)
-    if prob.kind == "cahn_hilliard":
+    if prob.kind in ("cahn_hilliard", "cahn_hilliard_eyre"):
         _, e2 = spatial.coeffs(prob)
         return -jbar * Lam + e2 * (Lam * Lam)
     return spatial.mu(Lam, prob)
@@ -96,6 +101,9 @@ def step2_2d(prob, S1: np.ndarray, jbar: float = 0.0) -> np.ndarray:
     mu = _step2_mu(prob, jbar)                        # [q, p]
     hat = T @ S1 @ T.T                                 # Ty S Txᵀ for every bin
     denom = d[:, None, None] + e[:, None, None] * mu[None, :, :]
+    if prob.kind == "cahn_hilliard_eyre":             # + λ_{3,l} Λ
+        lam3 = circulant.eig_e(nt, prob.alpha, 0.0)    # e_l at θ = 0: z ω^l
+        denom = denom + lam3[:, None, None] * spatial.Lam_grid(prob)[None, :, :]
     hat = hat / denom
     return (T @ hat @ T.T) / (2.0 * prob.m) ** 2
 
@@ -106,6 +114,8 @@ def apply_precond(prob, r: np.ndarray, jbar: float = 0.0):
     Returns (δ, max|Im|/max|Re| after Step-(3)) — the imaginary residue of S:336.
     """
     S1 = circulant.step1(r, prob.alpha)
+    if prob.dim == 1 and prob.kind == "cahn_hilliard_eyre":
+        raise NotImplementedError("PinT-II is exercised in 2D (the library's CH path is 2D Neumann)")
     if prob.dim == 1:
         S2 = step2_1d(prob, S1, jbar)
     else:

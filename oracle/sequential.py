@@ -118,6 +118,43 @@ def dense_precond(prob, r: np.ndarray, jbar: float = 0.0) -> np.ndarray:
     return np.linalg.solve(K, r.reshape(-1)).reshape(r.shape)
 
 
+def dense_precond_eyre(prob, r: np.ndarray, jbar: float) -> np.ndarray:
+    """PinT-II Step-(2) operator as one dense matrix (tiny sizes): C1^(α)⊗I + C3^(α)⊗Δ_h +
+    I⊗(-J̄₃Δ_h + ε²Δ_h²) with C3^(α) = C2^(α) at θ = 0."""
+    nt = prob.nt
+    idt = circulant.inv_dt(prob)
+    L = lap_matrix(prob)
+    _, e2 = spatial.coeffs(prob)
+    ns = L.shape[0]
+    K = np.kron(circulant.C1_dense(nt, prob.alpha, idt), np.eye(ns)) + \
+        np.kron(circulant.C2_dense(nt, prob.alpha, 0.0), L) + np.kron(np.eye(nt), -jbar * L + e2 * (L @ L))
+    return np.linalg.solve(K, r.reshape(-1)).reshape(r.shape)
+
+
+def eyre_newton_stepping(prob, u0: np.ndarray, tol: float = 1e-14, maxit: int = 50) -> np.ndarray:
+    """Sequential Eyre scheme: (u_n - u_{n-1})/Δt = Δ_h u_n³ - Δ_h u_{n-1} - ε²Δ_h² u_n,
+    exact-Jacobian Newton per step (tiny sizes)."""
+    L = lap_matrix(prob)
+    _, e2 = spatial.coeffs(prob)
+    idt = circulant.inv_dt(prob)
+    u = u0.reshape(-1).astype(np.float64).copy()
+    ns = u.size
+    out = np.empty((prob.nt, ns))
+    for n in range(prob.nt):
+        up = u.copy()
+        x = up.copy()
+        for _ in range(maxit):
+            F = (x - up) * idt - L @ (x ** 3 - e2 * (L @ x)) + L @ up
+            J = idt * np.eye(ns) - L @ np.diag(3.0 * x * x) + e2 * (L @ L)
+            dx = np.linalg.solve(J, -F)
+            x = x + dx
+            if np.abs(dx).max() <= tol * max(np.abs(x).max(), 1e-300):
+                break
+        out[n] = x
+        u = x
+    return out.reshape((prob.nt,) + u0.shape)
+
+
 def ch_newton_stepping(prob, u0: np.ndarray, tol: float = 1e-14, maxit: int = 50) -> np.ndarray:
     """Sequential fully implicit BE for CH, exact-Jacobian Newton per step (tiny sizes)."""
     L = lap_matrix(prob)

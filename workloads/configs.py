@@ -11,7 +11,7 @@ from typing import Optional, Tuple
 @dataclass(frozen=True)
 class Problem:
     name: str
-    kind: str            # "biharmonic" | "linear_ch" | "cahn_hilliard"
+    kind: str            # "biharmonic" | "linear_ch" | "cahn_hilliard" (PinT-I) | "cahn_hilliard_eyre" (PinT-II)
     bc: str              # "neumann" | "hinged"
     dim: int             # 1 or 2
     m: int               # intervals per axis, h = 1/m
@@ -72,6 +72,11 @@ CONFIGS = {
     "c5": Problem("c5", "linear_ch", "neumann", 2, m=2048, nt=512, t_window=0.5, alpha=1e-4,
                   beta=0.4, eps=0.01, init="zero", fixed_iters=3,
                   u0_range=(-0.05, 0.05), seed=5),
+    # NEXT-1: c4's physics and windows solved with PinT-II (Eyre convex splitting,
+    # P:502-545) — the scheme the paper runs for its 2D CH experiments
+    "c4e": Problem("c4e", "cahn_hilliard_eyre", "neumann", 2, m=256, nt=64, t_window=64e-4, alpha=1e-3,
+                   eps=0.02, n_windows=4, max_iter=400, omega=0.7, tau=1.0,
+                   u0_range=(-0.1, 0.1), seed=4),
 }
 
 
