@@ -63,6 +63,9 @@ extern "C" {
 #define PD_BIHARMONIC      0   /* u_t = -Δ²u                      A = Δ_h²  */
 #define PD_LINEAR_CH       1   /* u_t = -β²Δu - ε²Δ²u             A = β²Δ_h + ε²Δ_h²  */
 #define PD_CAHN_HILLIARD   2   /* u_t = Δ(u³ - u - ε²Δu), PinT-I           */
+#define PD_CAHN_HILLIARD_EYRE 3 /* same PDE, PinT-II: Eyre convex splitting, u³ implicit, -u lagged
+                                   (P:502-545); Step-(2) divisor d_l + λ_{3,l}Λ - J̄₃Λ + ε²Λ²,
+                                   J̄₃ = mean(3U²)                                                */
 
 /* boundary conditions */
 #define PD_BC_NEUMANN      0   /* ∂u = ∂Δu = 0, paper Δ_h with ghost reflection */
@@ -73,7 +76,7 @@ extern "C" {
 #define PD_INIT_ZERO       1   /* U⁰ = 0                */
 
 typedef struct pd_problem {
-  int32_t kind;          /* PD_BIHARMONIC | PD_LINEAR_CH | PD_CAHN_HILLIARD                     */
+  int32_t kind;          /* PD_BIHARMONIC | PD_LINEAR_CH | PD_CAHN_HILLIARD | PD_CAHN_HILLIARD_EYRE */
   int32_t bc;            /* PD_BC_NEUMANN | PD_BC_HINGED (CH: Neumann only)                */
   int32_t dim;           /* 1 or 2 (CH: 2 only)                                                  */
   int32_t nt;            /* time steps per window, power of two in [2, 4096]                     */

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libparadiag.so")
 
 PD_OK, PD_NOT_CONVERGED = 0, 1
 PD_EINVAL, PD_ESINGULAR, PD_ECUDA, PD_ENCCL, PD_ENOMEM, PD_EDIVERGED = -1, -2, -3, -4, -5, -6
-KINDS = {"biharmonic": 0, "linear_ch": 1, "cahn_hilliard": 2}
+KINDS = {"biharmonic": 0, "linear_ch": 1, "cahn_hilliard": 2, "cahn_hilliard_eyre": 3}
 BCS = {"neumann": 0, "hinged": 1}
 INITS = {"broadcast": 0, "zero": 1}
 MAX_WINDOWS = 64

@@ -27,7 +27,7 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* T = smem2 + (size_t)warp * (kWarpBufD / 2);
   const int64_t ntiles = (P.ns + S - 1) / S;
-  const double jbar = P.kind == 2 ? P.st->jbar : 0.0;
+  const double jbar = P.kind >= 2 ? P.st->jbar : 0.0;
   double lmax = 0.0;
   // two CTAs share an SM; starting the second one late puts their load and compute phases out of
   // step, so one streams its tile while the other computes
@@ -90,6 +90,8 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
     const int64_t sa = s0 + 2 * (warp * PP + pl);
     const double mua = sa < P.ns ? mode_mu(sa, P, jbar) : 0.0;
     const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
+    const double lama = P.l3 && sa < P.ns ? mode_lam(sa, P) : 0.0;            // PinT-II only
+    const double lamb = P.l3 && sa + 1 < P.ns ? mode_lam(sa + 1, P) : lama;
 #pragma unroll
     for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * NT + k1 + E * k2)] = v[k2];
     __syncwarp();
@@ -108,8 +110,8 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
-      const double2 Af = cmul(A, cinv_fast(shifted(d, P.el, l, mua)));
-      const double2 Bf = cmul(B, cinv_fast(shifted(d, P.el, l, mub)));
+      const double2 Af = cmul(A, cinv_fast(shifted(d, P.el, l, mua, P.l3, lama)));
+      const double2 Bf = cmul(B, cinv_fast(shifted(d, P.el, l, mub, P.l3, lamb)));
       if (k2 < 16) v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);       // X_l = Af + i Bf
       T[tpad(pl * NT + m)] = make_double2(Af.x + Bf.y, Bf.x - Af.y);      // X_{N-l}
     }

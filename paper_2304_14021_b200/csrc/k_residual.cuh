@@ -282,16 +282,24 @@ namespace pd {
 //   * inner values L(u) (CH: v = u³ - u - ε²L(u)) on the 1-point-haloed tile go to shared memory,
 //     then the outer stencil and the time difference.  Arithmetic and evaluation order are those of
 //     k_residual_2d.
-constexpr int kResTX = 64, kResTY = 32, kResThreads = 256, kResChunk = 32;
-constexpr int kResUX = kResTX + 4, kResUY = kResTY + 4;     // staged U tile
-constexpr int kResIX = kResTX + 2, kResIY = kResTY + 2;     // inner-value tile
+constexpr int kResTX = 62, kResTY = 32, kResThreads = 256, kResChunk = 32;
+constexpr int kResUX = kResTX + 4, kResUY = kResTY + 4;     // staged U tile (66 x 36)
+constexpr int kResIX = kResTX + 2, kResIY = kResTY + 2;     // inner-value tile (64 x 34)
 constexpr int kResUP = kResUX + 1, kResIP = kResIX + 1;     // pitches (odd: conflict-free columns)
 constexpr int kResUN = kResUY * kResUX;                     // staged elements
 constexpr int kResPer = (kResUN + kResThreads - 1) / kResThreads;
-constexpr int kResOut = kResTY * kResTX / kResThreads;      // outputs per thread
+constexpr int kResGroups = kResThreads / kResIX;            // 4 row groups of the 64 inner columns
+constexpr int kResOut = kResTY / kResGroups;                // 8 consecutive output rows per thread
 constexpr size_t kResSmem = (2 * (size_t)kResUY * kResUP + (size_t)kResIY * kResIP) * sizeof(double);
+static_assert(kResIX * kResGroups == kResThreads, "one thread per inner column and row group");
 
-template <bool THETA>     // THETA: θ < 1 (A U_{n-1} term); false compiles the backward-Euler kernel
+// MODE 0: backward Euler (linear, CH PinT-I); 1: θ-method (A U_{n-1} term, NEXT-2); 2: CH PinT-II
+// (Eyre, NEXT-1: inner v = U³ - ε²L(U), r = (L(v) - L(U_{n-1})) - (U_n - U_{n-1})/Δt, Σ 3U²).
+// Modes 1 and 2 carry a previous-slice quantity (A U_{n-1} / L U_{n-1}) in registers.
+// Threads stream down vertical strips (thread = one column x one row group) so the vertical
+// neighbours of both stencils stay in registers: 3 shared loads per inner value, 3-4 per output
+// (ncu r01c: the 2D-loop version spent 2.9 warp instructions per point).
+template <int MODE>
 __global__ void __launch_bounds__(kResThreads)
 k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
                 ResidualParams P, double* __restrict__ jpart) {
@@ -304,7 +312,9 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
   const int x0 = blockIdx.x * kResTX, y0 = blockIdx.y * kResTY;
   const int n0 = blockIdx.z * kResChunk, n1 = min(n0 + kResChunk, P.nt);
   const size_t ns = (size_t)P.nx * P.ny;
-  const bool ch = P.kind == 2;
+  const bool ch = P.kind >= 2;
+  constexpr bool eyre = MODE == 2;
+  const bool halos = P.hlo != nullptr || P.hhi != nullptr;
   // staging map (slice independent): element k of this thread -> smem slot, source buffer
   // (0: U, 1: lower halo, 2: upper halo) and offset within its slice, extension sign
   int soff[kResPer], dpos[kResPer], ssel[kResPer];
@@ -329,14 +339,20 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     sgn[k] = sy * sg;
   }
   const size_t hstride = 2 * (size_t)P.nx;
-  auto stage = [&](double* dst, int n) {           // n = -1: u0 (single-GPU θ-method warm-up)
+  auto stage = [&](double* dst, int n) {           // n = -1: u0 (single-GPU warm-up slice)
+    const double* b0 = n < 0 ? u0 : U + (size_t)n * ns;
+    if (!halos) {
 #pragma unroll
-    for (int k = 0; k < kResPer; ++k)
-      if (soff[k] >= 0) {
-        const double* b = ssel[k] == 0 ? (n < 0 ? u0 : U + (size_t)n * ns)
-                                       : (ssel[k] == 1 ? P.hlo : P.hhi) + (size_t)n * hstride;
-        cp_async8(dst + dpos[k], b + soff[k]);
-      }
+      for (int k = 0; k < kResPer; ++k)
+        if (soff[k] >= 0) cp_async8(dst + dpos[k], b0 + soff[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kResPer; ++k)
+        if (soff[k] >= 0) {
+          const double* b = ssel[k] == 0 ? b0 : (ssel[k] == 1 ? P.hlo : P.hhi) + (size_t)n * hstride;
+          cp_async8(dst + dpos[k], b + soff[k]);
+        }
+    }
     cp_async_commit();
   };
   auto fix_signs = [&](double* dst) {     // hinged: odd extension (own elements only)
@@ -346,22 +362,26 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
         if (soff[k] >= 0) dst[dpos[k]] *= sgn[k];
     }
   };
-  // outputs of this thread: column tx, rows ty = tid / TX + 4j
-  const int tx = tid % kResTX, ty0 = tid / kResTX;
+  // inner strip: inner column ix = tid % 64, rows [ir0, ir1) of the 34 inner rows
+  const int ix = tid % kResIX, grp = tid / kResIX;
+  const int ir0 = (grp * kResIY) / kResGroups, ir1 = ((grp + 1) * kResIY) / kResGroups;
+  // output strip: column tx = ix (< TX), rows ty0 .. ty0+7
+  const int tx = ix, ty0 = grp * kResOut;
   const int gx = x0 + tx;
+  const bool xout = tx < kResTX && gx < P.nx;
   double prev[kResOut];
   {
     const double* sp = n0 == 0 ? u0 : U + (size_t)(n0 - 1) * ns;
 #pragma unroll
     for (int j = 0; j < kResOut; ++j) {
-      const int gy = y0 + ty0 + j * (kResThreads / kResTX);
-      prev[j] = (gx < P.nx && gy < P.ny) ? __ldg(sp + (size_t)gy * P.nx + gx) : 0.0;
+      const int gy = y0 + ty0 + j;
+      prev[j] = (xout && gy < P.ny) ? __ldg(sp + (size_t)gy * P.nx + gx) : 0.0;
     }
   }
   double jloc = 0.0;
-  // θ < 1 needs A U_{n-1}: march one extra (output-free) slice n0-1 first; A U_n of every slice
-  // is then carried to the next in registers like U_{n-1}
-  constexpr bool thet = THETA;
+  // θ < 1 / PinT-II need A U_{n-1} / L U_{n-1}: march one extra (output-free) slice n0-1 first;
+  // the quantity of every slice is then carried to the next in registers like U_{n-1}
+  constexpr bool thet = MODE != 0;
   const int nstart = thet ? n0 - 1 : n0;
   double prevA[kResOut];
 #pragma unroll
@@ -374,36 +394,52 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     fix_signs(cur);
     __syncthreads();                       // cur staged; previous slice done with nxt and sI
     if (n + 1 < n1) stage(nxt, n + 1);
-    for (int i = tid; i < kResIY * kResIX; i += kResThreads) {
-      const int iy = i / kResIX, ix = i - iy * kResIX;
-      const double* c = cur + (iy + 1) * kResUP + (ix + 1);
-      const double uc = c[0];
-      const double Lr = ((c[-1] + c[1]) + (c[-kResUP] + c[kResUP]) - 4.0 * uc) * P.inv_h2;
-      sI[iy * kResIP + ix] = ch ? uc * uc * uc - uc - P.e2 * Lr : Lr;
+    // ---- inner values down the strip: u rows stream through registers
+    {
+      const double* c = cur + (ir0 + 1) * kResUP + (ix + 1);
+      double ua = c[-kResUP], uc = c[0];
+      double* out = sI + ir0 * kResIP + ix;
+      for (int iy = ir0; iy < ir1; ++iy, c += kResUP, out += kResIP) {
+        const double ub = c[kResUP];
+        const double Lr = ((c[-1] + c[1]) + (ua + ub) - 4.0 * uc) * P.inv_h2;
+        *out = eyre ? uc * uc * uc - P.e2 * Lr : (ch ? uc * uc * uc - uc - P.e2 * Lr : Lr);
+        ua = uc;
+        uc = ub;
+      }
     }
     __syncthreads();
+    // ---- outer stencil + time difference down the output strip
     double* rn = r + (size_t)max(n, 0) * ns;
+    if (tx < kResTX) {
+      const double* I = sI + (ty0 + 1) * kResIP + (tx + 1);
+      const double* cu = cur + (ty0 + 2) * kResUP + (tx + 2);
+      double Ia = I[-kResIP], Ic = I[0];
 #pragma unroll
-    for (int j = 0; j < kResOut; ++j) {
-      const int ty = ty0 + j * (kResThreads / kResTX);
-      const int gy = y0 + ty;
-      const double* I = sI + (ty + 1) * kResIP + (tx + 1);
-      const double uo = cur[(ty + 2) * kResUP + (tx + 2)];
-      if (gx < P.nx && gy < P.ny) {
-        const double outer = ((I[-1] + I[1]) + (I[-kResIP] + I[kResIP]) - 4.0 * I[0]) * P.inv_h2;
+      for (int j = 0; j < kResOut; ++j, I += kResIP, cu += kResUP) {
+        const double Ib = I[kResIP];
+        const int gy = y0 + ty0 + j;
+        const double uo = cu[0];
+        const double outer = ((I[-1] + I[1]) + (Ia + Ib) - 4.0 * Ic) * P.inv_h2;
         const double dtime = (uo - prev[j]) * P.inv_dt;
-        double out;
-        if (ch) {
-          out = outer - dtime;
-          if (n >= n0) jloc += 3.0 * uo * uo - 1.0;
+        double outv;
+        if (eyre) {
+          const double Lc = ((cu[-1] + cu[1]) + (cu[-kResUP] + cu[kResUP]) - 4.0 * uo) * P.inv_h2;
+          outv = (outer - prevA[j]) - dtime;
+          prevA[j] = Lc;
+          if (n >= n0 && gx < P.nx && gy < P.ny) jloc += 3.0 * uo * uo;
+        } else if (ch) {
+          outv = outer - dtime;
+          if (n >= n0 && gx < P.nx && gy < P.ny) jloc += 3.0 * uo * uo - 1.0;
         } else {
-          const double Au = P.kind == 0 ? outer : P.b2 * I[0] + P.e2 * outer;
-          out = thet ? -dtime - (P.theta * Au + (1.0 - P.theta) * prevA[j]) : -dtime - Au;
-          prevA[j] = Au;
+          const double Au = P.kind == 0 ? outer : P.b2 * Ic + P.e2 * outer;
+          outv = thet ? -dtime - (P.theta * Au + (1.0 - P.theta) * prevA[j]) : -dtime - Au;
+          if (thet) prevA[j] = Au;
         }
-        if (n >= n0) rn[(size_t)gy * P.nx + gx] = out;
+        if (n >= n0 && gx < P.nx && gy < P.ny) rn[(size_t)gy * P.nx + gx] = outv;
+        prev[j] = uo;
+        Ia = Ic;
+        Ic = Ib;
       }
-      prev[j] = uo;
     }
   }
   if (ch) {

@@ -25,6 +25,7 @@ struct TimeParams {
   const double* ginv;    // scale / γ_j
   const double2* dl;     // d_l = (1 - z ω^l)/Δt, l = 0..nt-1
   const double2* el;     // e_l = θ + (1-θ) z ω^l (θ-method); NULL for θ = 1 (e_l = 1)
+  const double2* l3;     // λ_{3,l} = z ω^l (PinT-II): divisor gains λ_{3,l}·Λ; NULL otherwise
   const double* lamx;    // Laplacian eigenvalues along x (and y: same table, square grids)
   int kind;              // 0 biharmonic, 1 linear CH, 2 CH
   double b2, e2;
@@ -38,11 +39,28 @@ struct TimeParams {
   int stagger_ns;             // k_time2d_v2: start delay of the second CTA of each SM (phase offset)
 };
 
-// shifted eigenvalue d_l + e_l μ of the Step-(2) system
-PD_DEV double2 shifted(double2 d, const double2* el, int l, double mu) {
-  if (!el) return make_double2(d.x + mu, d.y);
-  const double2 e = __ldg(el + l);
-  return make_double2(d.x + e.x * mu, d.y + e.y * mu);
+// shifted eigenvalue d_l + e_l μ of the Step-(2) system; PinT-II adds λ_{3,l}Λ
+// — pass lam = Λ of the mode with l3 != NULL
+PD_DEV double2 shifted(double2 d, const double2* el, int l, double mu, const double2* l3 = nullptr,
+                       double lam = 0.0) {
+  double2 s;
+  if (!el) {
+    s = make_double2(d.x + mu, d.y);
+  } else {
+    const double2 e = __ldg(el + l);
+    s = make_double2(d.x + e.x * mu, d.y + e.y * mu);
+  }
+  if (l3) {
+    const double2 w = __ldg(l3 + l);
+    s = make_double2(s.x + w.x * lam, s.y + w.y * lam);
+  }
+  return s;
+}
+
+// Laplacian eigenvalue Λ = λ_p + λ_q of spatial mode s
+PD_DEV double mode_lam(int64_t s, const TimeParams& P) {
+  const int64_t q = s / P.nx, p = s - q * P.nx;
+  return __ldg(P.lamx + P.xoff + p) + (P.nx == P.ns ? 0.0 : __ldg(P.lamx + q));
 }
 
 PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {
@@ -50,7 +68,7 @@ PD_DEV double mode_mu(int64_t s, const TimeParams& P, double jbar) {
   const double Lam = __ldg(P.lamx + P.xoff + p) + (P.nx == P.ns ? 0.0 : __ldg(P.lamx + q));
   if (P.kind == 0) return Lam * Lam;
   if (P.kind == 1) return P.b2 * Lam + P.e2 * (Lam * Lam);
-  return -jbar * Lam + P.e2 * (Lam * Lam);
+  return -jbar * Lam + P.e2 * (Lam * Lam);          // CH PinT-I (J̄ = mean(3U²-1)) / PinT-II (J̄₃)
 }
 
 // Stage the tile's pencil pairs in shared memory with cp.async (natural time order; the
@@ -103,7 +121,7 @@ k_time_solve_2d(const double* in, double* out, TimeParams P) {
   const int64_t sa = s0 + 2 * warp;
   if (sa < P.ns) {
     warp_fft_dif<-1>(buf, P.log2nt, P.tw, P.twlog, lane, P.gam);
-    const double jbar = P.kind == 2 ? P.st->jbar : 0.0;
+    const double jbar = P.kind >= 2 ? P.st->jbar : 0.0;
     const double mua = mode_mu(sa, P, jbar);
     const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
     const int N = P.nt, half = N >> 1;
@@ -115,8 +133,8 @@ k_time_solve_2d(const double* in, double* out, TimeParams P) {
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(P.dl + l);
-      const double2 fa = cinv(shifted(d, P.el, l, mua));
-      const double2 fb = cinv(shifted(d, P.el, l, mub));
+      const double2 fa = cinv(shifted(d, P.el, l, mua, P.l3, P.l3 ? mode_lam(sa, P) : 0.0));
+      const double2 fb = cinv(shifted(d, P.el, l, mub, P.l3, P.l3 && sa + 1 < P.ns ? mode_lam(sa + 1, P) : 0.0));
       const double2 Af = cmul(A, fa), Bf = cmul(B, fb);
       // X_l = Af + i Bf ; X_{N-l} = conj(Af) + i conj(Bf)
       buf[pl] = make_double2(Af.x - Bf.y, Af.y + Bf.x);

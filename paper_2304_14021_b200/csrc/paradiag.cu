@@ -93,6 +93,7 @@ struct pd_handle {
   double* ginv = nullptr;
   double2* dl = nullptr;
   double2* el = nullptr;              // e_l = θ + (1-θ) z ω^l (NULL for θ = 1)
+  double2* l3 = nullptr;              // λ_{3,l} = z ω^l (PinT-II only)
   double* lam = nullptr;
   double2* tw = nullptr;
   double2* trig = nullptr;
@@ -164,12 +165,14 @@ int dalloc(pd_handle* h, T** p, size_t count) {
   return PD_OK;
 }
 
+bool is_ch(int kind) { return kind == PD_CAHN_HILLIARD || kind == PD_CAHN_HILLIARD_EYRE; }
+
 int validate(const pd_problem* p) {
   if (!p) return fail(PD_EINVAL, "problem is NULL");
-  if (p->kind < 0 || p->kind > 2) return fail(PD_EINVAL, "unknown kind");
+  if (p->kind < 0 || p->kind > 3) return fail(PD_EINVAL, "unknown kind");
   if (p->bc < 0 || p->bc > 1) return fail(PD_EINVAL, "unknown bc");
   if (p->dim != 1 && p->dim != 2) return fail(PD_EINVAL, "dim must be 1 or 2");
-  if (p->kind == PD_CAHN_HILLIARD && (p->dim != 2 || p->bc != PD_BC_NEUMANN))
+  if (is_ch(p->kind) && (p->dim != 2 || p->bc != PD_BC_NEUMANN))
     return fail(PD_EINVAL, "Cahn-Hilliard is supported in 2D with Neumann BCs (P:59)");
   if (!is_pow2(p->nt) || p->nt < 2 || p->nt > 4096) return fail(PD_EINVAL, "nt must be a power of two in [2, 4096]");
   if (p->dim == 2 && (!is_pow2(p->m) || p->m < 4 || p->m > 4096))
@@ -178,14 +181,14 @@ int validate(const pd_problem* p) {
   if (!(p->alpha > 0.0 && p->alpha < 1.0)) return fail(PD_EINVAL, "alpha must be in (0, 1) (P:308)");
   if (!(p->theta >= 0.5 && p->theta <= 1.0))
     return fail(PD_EINVAL, "theta must be in [1/2, 1] (theta-method, P:119-126; A-stable range)");
-  if (p->kind == PD_CAHN_HILLIARD && p->theta != 1.0)
+  if (is_ch(p->kind) && p->theta != 1.0)
     return fail(PD_EINVAL, "Cahn-Hilliard PinT-I is backward Euler (theta = 1, P:440-451)");
   if (!(p->t_window > 0.0) || !std::isfinite(p->t_window)) return fail(PD_EINVAL, "t_window must be > 0");
   if (!(p->eps >= 0.0)) return fail(PD_EINVAL, "eps must be >= 0");
   if (p->fixed_iters <= 0 && !(p->tol > 0.0)) return fail(PD_EINVAL, "tol must be > 0");
   if (p->n_windows < 1 || p->n_windows > PD_MAX_WINDOWS) return fail(PD_EINVAL, "n_windows out of range");
   if (p->fixed_iters <= 0 && p->max_iter < 1) return fail(PD_EINVAL, "max_iter must be >= 1");
-  if (p->kind == PD_CAHN_HILLIARD && !(p->omega > 0.0 && p->tau > 0.0))
+  if (is_ch(p->kind) && !(p->omega > 0.0 && p->tau > 0.0))
     return fail(PD_EINVAL, "CH damping needs omega > 0 and tau > 0");
   if (p->init != PD_INIT_BROADCAST && p->init != PD_INIT_ZERO) return fail(PD_EINVAL, "unknown init");
   return PD_OK;
@@ -233,14 +236,18 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   prof_begin(h, K_RESIDUAL);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
   if (h->P.dim == 2) {
-    if ((h->tune & 32) && h->P.theta == 1.0) {     // previous row-streaming kernel (A/B)
+    if ((h->tune & 32) && h->P.theta == 1.0 && h->P.kind != PD_CAHN_HILLIARD_EYRE) {     // previous row-streaming kernel (A/B)
       dim3 grd((h->nx + kResStrip - 1) / kResStrip, h->P.nt);
       k_residual_2d<<<grd, 128, 0, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y;
     } else {
       dim3 grd((h->nx + kResTX - 1) / kResTX, (h->ny + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-      if (h->P.theta != 1.0) k_residual_tile<true><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
-      else k_residual_tile<false><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      if (h->P.kind == PD_CAHN_HILLIARD_EYRE)
+        k_residual_tile<2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else if (h->P.theta != 1.0)
+        k_residual_tile<1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else
+        k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y * grd.z;
     }
   } else {
@@ -250,7 +257,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
   }
   prof_end(h, K_RESIDUAL);
   PD_LAUNCHED();
-  if (h->P.kind == PD_CAHN_HILLIARD) {
+  if (is_ch(h->P.kind)) {
     prof_begin(h, K_JBAR);
     k_jbar_finalize<<<1, 1024, 0, h->stream>>>(h->jpart, nparts, 1.0 / (double)h->total, h->st);
     prof_end(h, K_JBAR);
@@ -338,7 +345,7 @@ bool fast_time_any(pd_handle* h, const double* in, double* out, const TimeParams
 TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   TimeParams T;
   T.nt = h->P.nt; T.log2nt = h->log2nt; T.ns = h->ns; T.nx = h->nx;
-  T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.el = h->el; T.lamx = h->lam;
+  T.gam = h->gam; T.ginv = h->ginv; T.dl = h->dl; T.el = h->el; T.l3 = h->l3; T.lamx = h->lam;
   T.kind = h->P.kind; T.b2 = h->b2; T.e2 = h->e2; T.st = h->st;
   T.tw = h->tw; T.twlog = h->twlog; T.amax = amax; T.tune = h->tune; T.xoff = 0;
   T.gamma_folded = 0;
@@ -351,7 +358,7 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
 bool can_fuse_update(const pd_handle* h) {
   // measured (d3f/d3g): the epilogue's U loads are exposed in the latency-bound line kernel, so the
   // fused pass (20.4 ms) loses to x-inverse + streaming update (10.3 + 8.2 ms) — opt-in (tune 16)
-  return (h->tune & 16) && h->P.dim == 2 && h->P.kind != PD_CAHN_HILLIARD && h->fast && h->dtt_ver == 3 && h->P.m >= 64 &&
+  return (h->tune & 16) && h->P.dim == 2 && !is_ch(h->P.kind) && h->fast && h->dtt_ver == 3 && h->P.m >= 64 &&
          h->P.m <= 2048;
 }
 
@@ -405,7 +412,7 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
 }
 
 int launch_update(pd_handle* h, double* U, const double* delta) {
-  const int damped = h->P.kind == PD_CAHN_HILLIARD;
+  const int damped = is_ch(h->P.kind);
   prof_begin(h, K_UPDATE);
   k_update<<<148 * 8, 256, 0, h->stream>>>(U, delta, (size_t)h->total, h->st, damped, h->P.omega, h->P.tau);
   prof_end(h, K_UPDATE);
@@ -440,7 +447,7 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   info->delta_max = dmax;
   info->u_max = umax;
   info->rel = umax > 0 ? dmax / umax : 0.0;
-  info->jbar = h->P.kind == PD_CAHN_HILLIARD ? h->st_host->jbar : 0.0;
+  info->jbar = is_ch(h->P.kind) ? h->st_host->jbar : 0.0;
   info->omega = h->st_host->omega;
   if (!std::isfinite(dmax) || !std::isfinite(umax)) return fail(PD_EDIVERGED, "non-finite increment or iterate");
   return PD_OK;
@@ -573,7 +580,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   for (int k = 0; k < (int)trig2p.size(); ++k) trig2p[(size_t)(k % 16) * 64 + k / 16] = trig[2 * k];
 
   // ---- singularity check of d_l + μ (linear kinds): only l = 0 and N_t/2 have real d_l
-  if (p->kind != PD_CAHN_HILLIARD) {
+  if (!is_ch(p->kind)) {
     double worst = INFINITY;
     for (int l : {0, nt / 2}) {
       for (int i = 0; i < h->nx; ++i)
@@ -598,6 +605,9 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   PD_TRY(dalloc(h, &h->ginv, nt));
   PD_TRY(dalloc(h, &h->dl, nt));
   if (p->theta != 1.0) PD_TRY(dalloc(h, &h->el, nt));
+  std::vector<double2> l3(nt);
+  for (int l = 0; l < nt; ++l) l3[l] = make_double2(z * std::cos(2.0 * M_PI * l / nt), -z * std::sin(2.0 * M_PI * l / nt));
+  if (p->kind == PD_CAHN_HILLIARD_EYRE) PD_TRY(dalloc(h, &h->l3, nt));
   PD_TRY(dalloc(h, &h->lam, h->nx));
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
@@ -608,7 +618,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     cudaError_t e = cudaMallocHost(&h->st_host, sizeof(DevStats));
     if (e != cudaSuccess) return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
   }
-  if (p->kind == PD_CAHN_HILLIARD) {
+  if (is_ch(p->kind)) {
     h->njpart = std::max((size_t)((h->nx + kResStrip - 1) / kResStrip) * nt,
                          (size_t)((h->nx + kResTX - 1) / kResTX) * ((h->ny + kResTY - 1) / kResTY) *
                              ((nt + kResChunk - 1) / kResChunk));
@@ -616,7 +626,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
-      up(h->dl, dl.data(), nt * sizeof(double2)) || (h->el && up(h->el, el.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
+      up(h->dl, dl.data(), nt * sizeof(double2)) || (h->el && up(h->el, el.data(), nt * sizeof(double2))) ||
+      (h->l3 && up(h->l3, l3.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
       up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
       up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)) ||
       (!trig2p.empty() && up(h->trig2p, trig2p.data(), trig2p.size() * sizeof(double2))))
@@ -666,8 +677,9 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
-    PD_TRY(allow_smem(k_residual_tile<false>, kResSmem));
-    PD_TRY(allow_smem(k_residual_tile<true>, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<1>, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<2>, kResSmem));
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
@@ -689,7 +701,7 @@ int paradiag_residual(pd_handle* h, const double* u0, const double* U, double* r
   if (jbar_out) {
     PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
     PD_CUDA(cudaStreamSynchronize(h->stream));
-    *jbar_out = h->P.kind == PD_CAHN_HILLIARD ? h->st_host->jbar : 0.0;
+    *jbar_out = is_ch(h->P.kind) ? h->st_host->jbar : 0.0;
   }
   return PD_OK;
 }
@@ -698,7 +710,7 @@ int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double 
   int rc = check_handle(h);
   if (rc) return rc;
   if (!r || !delta) return fail(PD_EINVAL, "NULL buffer");
-  if (h->P.kind == PD_CAHN_HILLIARD) {
+  if (is_ch(h->P.kind)) {
     k_set_jbar<<<1, 1, 0, h->stream>>>(h->st, jbar);
     PD_LAUNCHED();
   }
@@ -784,7 +796,7 @@ int paradiag_launches_per_iteration(const pd_handle* h) {
   if (!h) return 0;
   int n = 1 /*reset*/ + 1 /*residual*/ + (can_fuse_update(h) ? 0 : 1) /*update*/;
   n += h->P.dim == 2 ? 5 : 3;
-  if (h->P.kind == PD_CAHN_HILLIARD) n += 1;
+  if (is_ch(h->P.kind)) n += 1;
   return n;
 }
 
@@ -823,7 +835,7 @@ int paradiag_init_slab(const pd_problem* p, int device, void* cuda_stream, int64
   *out = nullptr;
   int rc = validate(p);
   if (rc) return rc;
-  if (p->dim != 2 || p->kind == PD_CAHN_HILLIARD || p->theta != 1.0)
+  if (p->dim != 2 || is_ch(p->kind) || p->theta != 1.0)
     return fail(PD_EINVAL, "slab mode: 2D linear kinds with theta = 1 (CH runs as replicas, DESIGN.md §8)");
   if (p->m < 64 || p->m > 2048 || p->nt < 32 || p->nt > 1024)
     return fail(PD_EINVAL, "slab mode: needs the register-FFT sizes (64 <= m <= 2048, 32 <= nt <= 1024)");
@@ -866,7 +878,7 @@ int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, 
   R.y0g = h->y0; R.nyg = h->ny; R.hlo = halo_lo; R.hhi = halo_hi; R.theta = 1.0;
   prof_begin(h, K_RESIDUAL);
   dim3 grd((h->nx + kResTX - 1) / kResTX, (h->nyl + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-  k_residual_tile<false><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
+  k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
   prof_end(h, K_RESIDUAL);
   PD_LAUNCHED();
   return PD_OK;

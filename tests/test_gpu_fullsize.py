@@ -41,9 +41,12 @@ def test_c3_full(cuda_lib):
     assert np.abs(got - modespace.sample(p, gm, c0, pts)).max() <= 1e-10 * umax
 
 
-def test_c4_full(cuda_lib):
-    p = config("c4")
-    g = json.load(open(os.path.join(GOLD, "c4_full.json")))
+@pytest.mark.parametrize("name", ["c4", "c4e"])
+def test_c4_full(cuda_lib, name):
+    """BJ.c4 (PinT-I) and its PinT-II twin c4e (NEXT-1): per-window iteration counts, sampled values
+    of the last window, conserved mass and the end energy against the oracle's golden run."""
+    p = config(name)
+    g = json.load(open(os.path.join(GOLD, f"{name}_full.json")))
     u0 = make_u0(p)
     s = cuda_lib.Solver(p)
     U = s.empty()

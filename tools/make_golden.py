@@ -1,6 +1,6 @@
 """Write tests/golden/*_full.json from the ORACLE only (no CUDA path involved).
 
-  python tools/make_golden.py c3 c4        (c4 takes ~2-3 min on 8 cores)
+  python tools/make_golden.py c3 c4 c4e    (c4 / c4e take a few minutes each on 8 cores)
 
 Each file records the oracle's per-window iteration counts, increments, and the iterate at a
 fixed set of sample points (drawn from a seeded RNG), plus mass/energy for CH.
@@ -39,14 +39,14 @@ def run(name):
                "rel": [h["rel"] for h in hist[h0:]],
                "points": pts, "values": [float(U[n, iy, ix]) for n, iy, ix in pts],
                "u_max": float(np.abs(U).max())}
-        if p.kind == "cahn_hilliard":
+        if p.kind.startswith("cahn_hilliard"):
             win["mass_end"] = diagnostics.mass(p, U[-1])
             win["energy_end"] = diagnostics.energy(p, U[-1])
             win["jbar_last"] = hist[-1]["jbar"]
         out["windows"].append(win)
         u = U[-1].copy()
         print(name, "window", w, "iters", k, flush=True)
-    if p.kind == "cahn_hilliard":
+    if p.kind.startswith("cahn_hilliard"):
         out["mass_u0"] = diagnostics.mass(p, u0)
         out["energy_u0"] = diagnostics.energy(p, u0)
     out["oracle_seconds"] = time.time() - t
