@@ -11,9 +11,12 @@ PD_DEV double stats_omega(const DevStats* st, int damped, double omega_cap, doub
 }
 
 // U += ω δ over n doubles; ‖U‖∞ reduced into st->umax_bits.  Vectorised by double2 when aligned.
+// Usrc == U: in place.  Otherwise U = Usrc + ω δ (the pipelined solve's last update lands in the
+// caller's buffer from the alternate one).
 __global__ void __launch_bounds__(256)
-k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, DevStats* st,
-         int damped, double omega_cap, double tau) {
+k_update(double* U, const double* delta, size_t n, DevStats* st, int damped, double omega_cap, double tau,
+         const double* Usrc = nullptr) {
+  if (!Usrc) Usrc = U;
   const double w = stats_omega(st, damped, omega_cap, tau);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->omega = w;
   // ‖U‖∞ as a max over |u| bit patterns: NaN sorts above +inf, so a non-finite iterate always
@@ -22,9 +25,10 @@ k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, Dev
   const unsigned long long absmask = 0x7fffffffffffffffull;
   const size_t n2 = n / 2;
   double2* U2 = reinterpret_cast<double2*>(U);
+  const double2* S2 = reinterpret_cast<const double2*>(Usrc);
   const double2* D2 = reinterpret_cast<const double2*>(delta);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
-    double2 u = U2[i];
+    double2 u = S2[i];
     const double2 d = __ldg(D2 + i);
     u.x += w * d.x;
     u.y += w * d.y;
@@ -34,7 +38,7 @@ k_update(double* __restrict__ U, const double* __restrict__ delta, size_t n, Dev
     lbits = max(lbits, max(bx, by));
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const double u = U[n - 1] + w * delta[n - 1];
+    const double u = Usrc[n - 1] + w * delta[n - 1];
     U[n - 1] = u;
     lbits = max(lbits, (unsigned long long)__double_as_longlong(u) & absmask);
   }

@@ -22,6 +22,11 @@ struct ResidualParams {
   int y0g, nyg;
   const double* hlo;
   const double* hhi;
+  // pipelined solve (k_residual_tile<.., true>): the iterate is U_new = U + dU, formed while staging;
+  // U_new is written to unew at the tile's outputs and max |U_new| folded into umax
+  const double* dU;
+  double* unew;
+  unsigned long long* umax;
 };
 
 // Reflect an out-of-range Neumann index back onto the node grid (ghost u_{-1} = u_1).
@@ -291,6 +296,7 @@ constexpr int kResPer = (kResUN + kResThreads - 1) / kResThreads;
 constexpr int kResGroups = kResThreads / kResIX;            // 4 row groups of the 64 inner columns
 constexpr int kResOut = kResTY / kResGroups;                // 8 consecutive output rows per thread
 constexpr size_t kResSmem = (2 * (size_t)kResUY * kResUP + (size_t)kResIY * kResIP) * sizeof(double);
+constexpr size_t kResSmemUpd = (4 * (size_t)kResUY * kResUP + (size_t)kResIY * kResIP) * sizeof(double);
 static_assert(kResIX * kResGroups == kResThreads, "one thread per inner column and row group");
 
 // MODE 0: backward Euler (linear, CH PinT-I); 1: θ-method (A U_{n-1} term, NEXT-2); 2: CH PinT-II
@@ -299,7 +305,10 @@ static_assert(kResIX * kResGroups == kResThreads, "one thread per inner column a
 // Threads stream down vertical strips (thread = one column x one row group) so the vertical
 // neighbours of both stencils stay in registers: 3 shared loads per inner value, 3-4 per output
 // (ncu r01c: the 2D-loop version spent 2.9 warp instructions per point).
-template <int MODE>
+// UPD (pipelined solve, linear kinds): the previous iteration's update is applied here — the
+// staged tile is U + dU, the outputs also write U_new to P.unew (a different buffer: neighbouring
+// tiles still read the old iterate as their halo) and reduce ‖U_new‖∞.
+template <int MODE, bool UPD = false>
 __global__ void __launch_bounds__(kResThreads)
 k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
                 ResidualParams P, double* __restrict__ jpart) {
@@ -307,6 +316,9 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
   double* const sU0 = reinterpret_cast<double*>(smem2);
   double* const sU1 = sU0 + kResUY * kResUP;
   double* const sI = sU1 + kResUY * kResUP;
+  double* const sD0 = sI + kResIY * kResIP;            // UPD: staged dU tiles
+  double* const sD1 = sD0 + kResUY * kResUP;
+  unsigned long long ubits = 0ull;
   __shared__ double wsum[kResThreads / 32];
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * kResTX, y0 = blockIdx.y * kResTY;
@@ -341,6 +353,13 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
   const size_t hstride = 2 * (size_t)P.nx;
   auto stage = [&](double* dst, int n) {           // n = -1: u0 (single-GPU warm-up slice)
     const double* b0 = n < 0 ? u0 : U + (size_t)n * ns;
+    if (UPD && n >= 0) {                              // the dU tile of the same slice
+      double* dd = dst == sU0 ? sD0 : sD1;
+      const double* d0 = P.dU + (size_t)n * ns;
+#pragma unroll
+      for (int k = 0; k < kResPer; ++k)
+        if (soff[k] >= 0) cp_async8(dd + dpos[k], d0 + soff[k]);
+    }
     if (!halos) {
 #pragma unroll
       for (int k = 0; k < kResPer; ++k)
@@ -355,7 +374,13 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     }
     cp_async_commit();
   };
-  auto fix_signs = [&](double* dst) {     // hinged: odd extension (own elements only)
+  auto fix_signs = [&](double* dst, int n) {     // U + dU (UPD), then the hinged odd extension
+    if (UPD && n >= 0) {
+      const double* dd = dst == sU0 ? sD0 : sD1;
+#pragma unroll
+      for (int k = 0; k < kResPer; ++k)
+        if (soff[k] >= 0) dst[dpos[k]] += dd[dpos[k]];
+    }
     if (!P.neumann) {
 #pragma unroll
       for (int k = 0; k < kResPer; ++k)
@@ -375,7 +400,9 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
 #pragma unroll
     for (int j = 0; j < kResOut; ++j) {
       const int gy = y0 + ty0 + j;
-      prev[j] = (xout && gy < P.ny) ? __ldg(sp + (size_t)gy * P.nx + gx) : 0.0;
+      const size_t o = (size_t)gy * P.nx + gx;
+      prev[j] = (xout && gy < P.ny) ? __ldg(sp + o) + (UPD && n0 > 0 ? __ldg(P.dU + (size_t)(n0 - 1) * ns + o) : 0.0)
+                                    : 0.0;
     }
   }
   double jloc = 0.0;
@@ -391,7 +418,7 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     double* cur = ((n - nstart) & 1) ? sU1 : sU0;
     double* nxt = ((n - nstart) & 1) ? sU0 : sU1;
     cp_async_wait_all();
-    fix_signs(cur);
+    fix_signs(cur, n);
     __syncthreads();                       // cur staged; previous slice done with nxt and sI
     if (n + 1 < n1) stage(nxt, n + 1);
     // ---- inner values down the strip: u rows stream through registers
@@ -435,12 +462,22 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
           outv = thet ? -dtime - (P.theta * Au + (1.0 - P.theta) * prevA[j]) : -dtime - Au;
           if (thet) prevA[j] = Au;
         }
-        if (n >= n0 && gx < P.nx && gy < P.ny) rn[(size_t)gy * P.nx + gx] = outv;
+        if (n >= n0 && gx < P.nx && gy < P.ny) {
+          rn[(size_t)gy * P.nx + gx] = outv;
+          if (UPD) {
+            P.unew[(size_t)n * ns + (size_t)gy * P.nx + gx] = uo;
+            ubits = max(ubits, (unsigned long long)__double_as_longlong(uo) & 0x7fffffffffffffffull);
+          }
+        }
         prev[j] = uo;
         Ia = Ic;
         Ic = Ib;
       }
     }
+  }
+  if (UPD) {
+    ubits = warp_max_u64(ubits);
+    if ((tid & 31) == 0 && ubits) atomicMax(P.umax, ubits);
   }
   if (ch) {
     const double v = warp_sum(jloc);

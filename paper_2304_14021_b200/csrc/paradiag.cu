@@ -52,10 +52,11 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
-                K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, PD_NKERNELS };
+                K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
-                                         "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update"};
+                                         "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update",
+                                         "residual_update"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr int kTime1DWarps = 4;
@@ -116,6 +117,11 @@ struct pd_handle {
   size_t njpart = 0;
   double* u0buf = nullptr;
   double* Uint = nullptr;             // solve_host's iterate
+  // pipelined solve (linear 2D): iteration k's update U += δ is applied inside iteration k+1's
+  // residual, which writes the new iterate to the other U buffer and r to the other workspace
+  double* Ub = nullptr;
+  double* work2 = nullptr;
+  bool pipe = true;                   // PARADIAG_PIPELINE=0 disables
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -166,6 +172,7 @@ int dalloc(pd_handle* h, T** p, size_t count) {
 }
 
 bool is_ch(int kind) { return kind == PD_CAHN_HILLIARD || kind == PD_CAHN_HILLIARD_EYRE; }
+bool can_pipeline(const pd_handle* h);
 
 int validate(const pd_problem* p) {
   if (!p) return fail(PD_EINVAL, "problem is NULL");
@@ -227,13 +234,16 @@ int setup_fast_attrs(pd_handle* h) {
   return PD_OK;
 }
 
-int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) {
+int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, const double* dU = nullptr,
+                    double* unew = nullptr) {
   ResidualParams R;
   R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
   R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr; R.theta = h->P.theta;
-  prof_begin(h, K_RESIDUAL);
+  R.dU = dU; R.unew = unew; R.umax = &h->st->umax_bits;
+  const int kid = dU ? K_RESUPD : K_RESIDUAL;
+  prof_begin(h, kid);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
   if (h->P.dim == 2) {
     if ((h->tune & 32) && h->P.theta == 1.0 && h->P.kind != PD_CAHN_HILLIARD_EYRE) {     // previous row-streaming kernel (A/B)
@@ -242,7 +252,11 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
       nparts = (size_t)grd.x * grd.y;
     } else {
       dim3 grd((h->nx + kResTX - 1) / kResTX, (h->ny + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-      if (h->P.kind == PD_CAHN_HILLIARD_EYRE)
+      if (dU && h->P.theta != 1.0)
+        k_residual_tile<1, true><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
+      else if (dU)
+        k_residual_tile<0, true><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
+      else if (h->P.kind == PD_CAHN_HILLIARD_EYRE)
         k_residual_tile<2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.theta != 1.0)
         k_residual_tile<1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
@@ -255,7 +269,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r) 
     dim3 grd((h->nx + blk.x - 1) / blk.x, 1, h->P.nt);
     k_residual<<<grd, blk, 0, h->stream>>>(u0, U, r, R, h->jpart);
   }
-  prof_end(h, K_RESIDUAL);
+  prof_end(h, kid);
   PD_LAUNCHED();
   if (is_ch(h->P.kind)) {
     prof_begin(h, K_JBAR);
@@ -453,6 +467,79 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   return PD_OK;
 }
 
+bool can_pipeline(const pd_handle* h) {
+  return h->pipe && !h->slab && h->P.dim == 2 && !is_ch(h->P.kind) && h->fast && h->P.m >= 64 && h->P.m <= 2048 &&
+         h->P.nt >= 32 && h->P.nt <= 1024;
+}
+
+int read_stats(pd_handle* h, double* dmax, double* umax) {
+  PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  std::memcpy(dmax, &h->st_host->dmax_bits, sizeof(double));
+  std::memcpy(umax, &h->st_host->umax_bits, sizeof(double));
+  return PD_OK;
+}
+
+// One window of the pipelined solve (can_pipeline): the same iterates as the plain loop —
+//   step 1:  r = b - K U⁰, δ_1 = P⁻¹ r
+//   step k:  U^{k-1} = U^{k-2} + δ_{k-1} (inside the residual, written to the other U buffer),
+//            r = b - K U^{k-1}, δ_k = P⁻¹ r
+//   end:     U^K = U^{K-1} + δ_K into the caller's buffer
+// which saves the separate update pass (24 B/dof).  The stop test of iteration k-1 (needs ‖U^{k-1}‖)
+// runs after step k; on convergence step k's δ is discarded.
+int solve_window_pipelined(pd_handle* h, const double* u0, double* U, int* iters, bool* conv, double* rel) {
+  if (!h->Ub) {
+    int rc;
+    if ((rc = dalloc(h, &h->Ub, (size_t)h->total)) || (rc = dalloc(h, &h->work2, (size_t)h->total))) return rc;
+  }
+  double* Ubuf[2] = {U, h->Ub};
+  double* Wbuf[2] = {h->work, h->work2};
+  int cu = 0, cw = 0, rc;
+  const bool fixed = h->P.fixed_iters > 0;
+  const int kmax = fixed ? h->P.fixed_iters : h->P.max_iter;
+  if ((rc = init_iterate(h, U, u0))) return rc;
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  if ((rc = launch_residual(h, u0, U, Wbuf[0]))) return rc;
+  if ((rc = precond(h, Wbuf[0], Wbuf[0]))) return rc;
+  double dmax = 0, umax = 0, dprev = 0;
+  if ((rc = read_stats(h, &dprev, &umax))) return rc;
+  if (!std::isfinite(dprev)) return fail(PD_EDIVERGED, "non-finite increment");
+  *conv = false;
+  for (int k = 2; k <= kmax; ++k) {
+    k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+    PD_LAUNCHED();
+    if ((rc = launch_residual(h, u0, Ubuf[cu], Wbuf[1 - cw], Wbuf[cw], Ubuf[1 - cu]))) return rc;
+    cu = 1 - cu;
+    cw = 1 - cw;
+    if ((rc = precond(h, Wbuf[cw], Wbuf[cw]))) return rc;
+    if ((rc = read_stats(h, &dmax, &umax))) return rc;          // ‖δ_k‖, ‖U^{k-1}‖
+    if (!std::isfinite(dmax) || !std::isfinite(umax)) return fail(PD_EDIVERGED, "non-finite increment or iterate");
+    if (!fixed && dprev <= h->P.tol * umax) {                   // iteration k-1 converged
+      *conv = true;
+      *iters = k - 1;
+      *rel = umax > 0 ? dprev / umax : 0.0;
+      if (Ubuf[cu] != U)
+        PD_CUDA(cudaMemcpyAsync(U, Ubuf[cu], (size_t)h->total * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      return PD_OK;
+    }
+    dprev = dmax;
+  }
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  prof_begin(h, K_UPDATE);
+  k_update<<<148 * 8, 256, 0, h->stream>>>(U, Wbuf[cw], (size_t)h->total, h->st, 0, 1.0, 1.0, Ubuf[cu]);
+  prof_end(h, K_UPDATE);
+  PD_LAUNCHED();
+  if ((rc = read_stats(h, &dmax, &umax))) return rc;
+  if (!std::isfinite(umax)) return fail(PD_EDIVERGED, "non-finite iterate");
+  *iters = kmax;
+  *rel = umax > 0 ? dprev / umax : 0.0;
+  *conv = !fixed && dprev <= h->P.tol * umax;
+  return PD_OK;
+}
+
 int check_handle(pd_handle* h) {
   if (!h) return fail(PD_EINVAL, "handle is NULL");
   PD_CUDA(cudaSetDevice(h->device));
@@ -492,6 +579,8 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
+  if (p->dim == 2 && !is_ch(p->kind) && p->m >= 64 && p->m <= 2048 && p->nt >= 32 && p->nt <= 1024)
+    b += 2 * total * sizeof(double);      // pipelined solve: alternate iterate and workspace
   *bytes = b;
   return PD_OK;
 }
@@ -680,6 +769,13 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<1>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<2>, kResSmem));
+    PD_TRY(allow_smem(k_residual_tile<0, true>, kResSmemUpd));
+    PD_TRY(allow_smem(k_residual_tile<1, true>, kResSmemUpd));
+    if (const char* f = std::getenv("PARADIAG_PIPELINE")) h->pipe = std::atoi(f) != 0;
+    if (can_pipeline(h)) {              // the pipelined solve's second iterate / workspace buffers
+      PD_TRY(dalloc(h, &h->Ub, (size_t)h->total));
+      PD_TRY(dalloc(h, &h->work2, (size_t)h->total));
+    }
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
@@ -743,6 +839,26 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
   int status = PD_OK;
   bool all_conv = true;
   for (int w = 0; w < h->P.n_windows; ++w) {
+    if (can_pipeline(h)) {
+      int iters = 0;
+      bool conv = false;
+      double rel = 0.0;
+      if ((rc = solve_window_pipelined(h, cur_u0, U, &iters, &conv, &rel))) {
+        info->windows_done = w;
+        return rc;
+      }
+      info->iters[w] = iters;
+      info->last_rel[w] = rel;
+      info->windows_done = w + 1;
+      all_conv = all_conv && conv;
+      if (!conv && h->P.fixed_iters <= 0) status = PD_NOT_CONVERGED;
+      if (w + 1 < h->P.n_windows) {
+        PD_CUDA(cudaMemcpyAsync(h->u0buf, U + (size_t)(h->P.nt - 1) * h->ns, h->ns * sizeof(double),
+                                cudaMemcpyDeviceToDevice, h->stream));
+        cur_u0 = h->u0buf;
+      }
+      continue;
+    }
     if ((rc = init_iterate(h, U, cur_u0))) return rc;
     const int kmax = h->P.fixed_iters > 0 ? h->P.fixed_iters : h->P.max_iter;
     bool conv = false;

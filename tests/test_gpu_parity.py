@@ -117,6 +117,23 @@ def test_precond_parity_warp_pair_lines(cuda_lib, name, monkeypatch):
     assert rel_err(to_host(d, p), d_o) <= 1e-11
 
 
+@pytest.mark.parametrize("name", ["c3_m256_nt64", "c5_m64", "c3_theta", "c5_m128_nt128"])
+def test_pipelined_solve_matches_plain_loop(cuda_lib, name, monkeypatch):
+    """The pipelined engine (update applied inside the next residual) reproduces the
+    plain residual / P_α⁻¹ / update loop: same iteration counts, iterates equal to rounding."""
+    p = CASES[name]
+    u0 = make_u0(p)
+    s = cuda_lib.Solver(p)
+    Ua = s.empty()
+    rca, ia = s.solve(to_dev(u0), Ua)
+    monkeypatch.setenv("PARADIAG_PIPELINE", "0")
+    s2 = cuda_lib.Solver(p)
+    Ub = s2.empty()
+    rcb, ib = s2.solve(to_dev(u0), Ub)
+    assert rca == rcb and list(ia.iters[:1]) == list(ib.iters[:1])
+    assert rel_err(to_host(Ua), to_host(Ub)) <= 1e-12
+
+
 def test_solve_host_matches_device(cuda_lib):
     p = CASES["c3_m32"]
     u0 = make_u0(p)
