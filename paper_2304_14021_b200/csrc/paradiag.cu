@@ -121,7 +121,7 @@ struct pd_handle {
   // residual, which writes the new iterate to the other U buffer and r to the other workspace
   double* Ub = nullptr;
   double* work2 = nullptr;
-  bool pipe = true;                   // PARADIAG_PIPELINE=0 disables
+  bool pipe = false;                  // PARADIAG_PIPELINE=1 enables (≈ neutral on c5, +2 arrays)
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -579,8 +579,7 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
-  if (p->dim == 2 && !is_ch(p->kind) && p->m >= 64 && p->m <= 2048 && p->nt >= 32 && p->nt <= 1024)
-    b += 2 * total * sizeof(double);      // pipelined solve: alternate iterate and workspace
+  // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
   *bytes = b;
   return PD_OK;
 }

@@ -123,6 +123,7 @@ def test_pipelined_solve_matches_plain_loop(cuda_lib, name, monkeypatch):
     plain residual / P_α⁻¹ / update loop: same iteration counts, iterates equal to rounding."""
     p = CASES[name]
     u0 = make_u0(p)
+    monkeypatch.setenv("PARADIAG_PIPELINE", "1")
     s = cuda_lib.Solver(p)
     Ua = s.empty()
     rca, ia = s.solve(to_dev(u0), Ua)
