@@ -59,6 +59,7 @@ const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finali
                                          "residual_update"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
+constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per CTA (sm_100a)
 constexpr int kTime1DWarps = 4;
 constexpr int kLineWarps = 4;   // spatial DTT rows: one warp per row, 4 rows per CTA
 #ifndef PD_COLW
@@ -390,10 +391,18 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) return rc;
     TimeParams T = time_params(h, nullptr);
     T.gamma_folded = fold ? 1 : 0;
-    const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
     prof_begin(h, K_TIME);
-    if (!fast_time_any(h, delta, delta, T))
-      k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
+    if (!fast_time_any(h, delta, delta, T)) {
+      // generic time pass (N_t outside the register-FFT sizes): one pencil pair per warp, fewer
+      // warps per CTA when the pencils are long (N_t = 2048/4096 need 35/70 KB per warp)
+      if (time_smem(h->P.nt, kTimeWarps) <= kSmemMax) {
+        const unsigned grid = (unsigned)((h->ns + 2 * kTimeWarps - 1) / (2 * kTimeWarps));
+        k_time_solve_2d<kTimeWarps><<<grid, kTimeWarps * 32, time_smem(h->P.nt, kTimeWarps), h->stream>>>(delta, delta, T);
+      } else {
+        const unsigned grid = (unsigned)((h->ns + 1) / 2);
+        k_time_solve_2d<1><<<grid, 32, time_smem(h->P.nt, 1), h->stream>>>(delta, delta, T);
+      }
+    }
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) return rc;
@@ -402,10 +411,13 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     return PD_OK;
   }
   TimeParams T = time_params(h, nullptr);
-  const unsigned grid = (unsigned)((h->ns + 2 * kTime1DWarps - 1) / (2 * kTime1DWarps));
-  const size_t smem = time_smem(h->P.nt, kTime1DWarps);
+  const bool w4 = time_smem(h->P.nt, kTime1DWarps) <= kSmemMax;     // else one warp per CTA (N_t = 4096)
+  const int nw = w4 ? kTime1DWarps : 1;
+  const unsigned grid = (unsigned)((h->ns + 2 * nw - 1) / (2 * nw));
+  const size_t smem = time_smem(h->P.nt, nw);
   prof_begin(h, K_TFWD1D);
-  k_time_fwd_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(r, h->spec, T);
+  if (w4) k_time_fwd_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(r, h->spec, T);
+  else k_time_fwd_1d<1><<<grid, 32, smem, h->stream>>>(r, h->spec, T);
   prof_end(h, K_TFWD1D);
   PD_LAUNCHED();
   PentaParams PP;
@@ -419,7 +431,8 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   PD_LAUNCHED();
   T.amax = dmax;
   prof_begin(h, K_TINV1D);
-  k_time_inv_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(h->spec, delta, T);
+  if (w4) k_time_inv_1d<kTime1DWarps><<<grid, kTime1DWarps * 32, smem, h->stream>>>(h->spec, delta, T);
+  else k_time_inv_1d<1><<<grid, 32, smem, h->stream>>>(h->spec, delta, T);
   prof_end(h, K_TINV1D);
   PD_LAUNCHED();
   return PD_OK;
@@ -757,10 +770,16 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
     k_penta_factor<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(PP);
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(PD_ECUDA, "penta factor launch"));
-    PD_TRY(allow_smem(k_time_fwd_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
-    PD_TRY(allow_smem(k_time_inv_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
+    if (time_smem(nt, kTime1DWarps) <= kSmemMax) {
+      PD_TRY(allow_smem(k_time_fwd_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
+      PD_TRY(allow_smem(k_time_inv_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
+    } else {
+      PD_TRY(allow_smem(k_time_fwd_1d<1>, time_smem(nt, 1)));
+      PD_TRY(allow_smem(k_time_inv_1d<1>, time_smem(nt, 1)));
+    }
   } else {
-    PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
+    if (time_smem(nt, kTimeWarps) <= kSmemMax) PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
+    else PD_TRY(allow_smem(k_time_solve_2d<1>, time_smem(nt, 1)));
     PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));

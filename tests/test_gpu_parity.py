@@ -45,6 +45,10 @@ CASES = {
     "c4e_m32": twin("c4e", m=32, nt=16, t_window=16e-4, n_windows=2),
     "c4e_m64_nt32": twin("c4e", m=64, nt=32, t_window=32e-4, n_windows=1),
     "c4e_m16_nt8": twin("c4e", m=16, nt=8, t_window=8e-4, n_windows=1),
+    # largest N_t (4096, the validated maximum): one warp per CTA in the generic time kernels
+    "c2_nt4096": twin("c2", m=31, nt=4096, t_window=4.0),
+    "c3_nt4096": twin("c3", m=8, nt=4096, t_window=0.4),
+    "c1_nt2048": replace(config("c1"), nt=2048, t_window=6.4),
     # c5's line length (M = 2048: the warp-pair transform of k_dttp.cuh), both BCs
     "c5_m2048_nt4": twin("c5", m=2048, nt=4),
     "c3_m2048_nt2": twin("c3", m=2048, nt=2),
