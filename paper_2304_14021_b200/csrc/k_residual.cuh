@@ -139,6 +139,29 @@ k_residual(const double* __restrict__ u0, const double* __restrict__ U, double* 
   }
 }
 
+// 1D linear residual, one thread per space-time point over the flattened [N_t][N_x] index
+// (grid-stride): the same per-point arithmetic as k_residual with a dense thread map, so short
+// rows (N_x = 63 at N_t = 2^20, NEXT-3) do not leave most of every block idle.
+__global__ void __launch_bounds__(256)
+k_residual_1d(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
+              ResidualParams P) {
+  const size_t total = (size_t)P.nx * P.nt;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / P.nx), x = (int)(i - (size_t)n * P.nx);
+    const double* s = U + (size_t)n * P.nx;
+    const double* sp = n == 0 ? u0 : U + (size_t)(n - 1) * P.nx;
+    const double uc = __ldg(s + x);
+    const double dtime = (uc - __ldg(sp + x)) * P.inv_dt;
+    auto applyA = [&](const double* q) {
+      const double lC = lap_at(q, x, 0, P);
+      const double llap = ((lap_g(q, x - 1, 0, P) + lap_g(q, x + 1, 0, P)) - 2.0 * lC) * P.inv_h2;
+      return P.kind == 0 ? llap : P.b2 * lC + P.e2 * llap;
+    };
+    const double Au = applyA(s);
+    r[i] = P.theta == 1.0 ? -dtime - Au : -dtime - (P.theta * Au + (1.0 - P.theta) * applyA(sp));
+  }
+}
+
 // J̄ = Σ partials / (N_t N_s), summed by one block in a fixed order.
 __global__ void k_jbar_finalize(const double* __restrict__ jpart, size_t np, double inv_count,
                                 DevStats* st) {

@@ -1,0 +1,267 @@
+// k_tlong.cuh — Steps (1)-(3) along time for long windows (N_t > 4096; SURVEY §8(f) NEXT-3:
+// "Δt = 10⁻⁶, i.e. N_t = 10⁶ ... four iterations").
+//
+// A pencil of N_t = 2^20 complex values (16 MB) does not fit on chip, so the time DFT runs as a
+// four-step FFT over HBM: N = N1·N2, n = N2·n1 + n2, k = k1 + N1·k2,
+//   X[k1 + N1 k2] = Σ_{n2} W_{N2}^{n2 k2} · W_N^{n2 k1} · Σ_{n1} W_{N1}^{n1 k1} x[N2 n1 + n2].
+// Pass A does the length-N1 transforms (stride N2 rows) and the W_N^{n2 k1} twiddle, pass B the
+// length-N2 transforms; both are the register-resident warp FFT of fft4.cuh (N1, N2 ≤ 1024).
+// Every pass stages a [transform length][8 pencil pairs] tile in shared memory so that HBM is
+// touched in 128-byte row segments (8 complex pencils side by side), never pencil by pencil.
+//
+// Data (all row-major, time slowest):
+//   in/out  real    [N][ns]       spatially transformed residual / correction (ns = N_x·N_y modes)
+//   Y       complex [N1][N2][P]   after pass A (forward) / before pass A (inverse), P = ⌈ns/2⌉
+//   X       complex [N][P]        the spectrum, bin-major; Step (2) divides it in place
+// Two real pencils (modes 2p, 2p+1) share one complex pencil z = γ_j (r_j[2p] + i r_j[2p+1]) as in
+// k_time.cuh; the divide kernel separates the Hermitian pair from bins k and N−k (both rows of X),
+// divides each by its mode's shifted eigenvalue and recombines.
+// Inverse: pass B with conjugate roots and W_N^{-n2 k1}, then pass A with conjugate roots and the
+// Γ_α⁻¹·(1/N_t)·(spatial normalisation) scale.
+#pragma once
+#include "common.cuh"
+#include "fft4.cuh"
+#include "k_time.cuh"
+
+namespace pd {
+
+constexpr int kTlPairs = 8;                  // pencil pairs per CTA = warps per CTA
+constexpr int kTlThreads = kTlPairs * 32;
+constexpr int kTlRowD = 2 * kTlPairs + 2;    // staged row pitch in doubles (16 + 2 pad: 144 B)
+constexpr int kTlRowC = kTlRowD / 2;         // ... in complex slots
+constexpr size_t kTlSmem = (size_t)1024 * kTlRowD * sizeof(double);   // 147456 B ≥ 8 × kWarpScratch slots
+
+struct TlongParams {
+  int N, log2N;            // N_t
+  int N1, N2;              // N = N1·N2, both in [32, 1024]
+  int log2N1, log2N2;
+  int64_t ns;              // real columns per time row
+  int64_t P;               // complex pencil pairs = ⌈ns/2⌉ (row pitch of Y and X)
+  int64_t nch;             // pair chunks = ⌈P/8⌉
+  const double2* tw;       // tw[j] = exp(-2πi j / 2^twlog)
+  int twlog;
+  TimeParams T;            // Step-(2) divisor tables (dl, el, l3, lamx, kind, b2, e2, st, nx, ns, gam, ginv)
+};
+
+#ifdef PD_TLONG_KERNELS     // defined only in tlong.cu (the engine sees TlongParams alone)
+PD_DEV double2 tl_tw(const TlongParams& Q, int e) {
+  return __ldg(Q.tw + ((size_t)(e & (Q.N - 1)) << (Q.twlog - Q.log2N)));
+}
+
+// Pass A forward: rows n = N2·n1 + n2a + g (g < G), columns 16·chunk .. +16 of the real input;
+// z = γ_n (r[2p] + i r[2p+1]); length-N1 DFT over n1; × W_N^{n2 k}; store Y[k][n2][p].
+template <int E>
+__global__ void __launch_bounds__(kTlThreads, 1)
+k_tl_a_fwd(const double* __restrict__ in, double2* __restrict__ Y, TlongParams Q) {
+  constexpr int G = 32 / E, L = 32 * E;
+  extern __shared__ double2 sm[];
+  double* sd = reinterpret_cast<double*>(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = blockIdx.x % Q.nch;
+  const int n2a = (int)(blockIdx.x / Q.nch) * G;
+  const int64_t c0 = chunk * (2 * kTlPairs);
+  for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
+    const int c = idx & 15, row = idx >> 4;            // row = n1·G + g: consecutive g are adjacent rows
+    const int g = row % G, n1 = row / G;
+    const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+    double* d = sd + (g * L + n1) * kTlRowD + c;
+    if (c0 + c < Q.ns) cp_async8(d, in + n * Q.ns + c0 + c);
+    else *d = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  double2 v[32];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int n1 = lane + 32 * e;
+      const double2 z = *reinterpret_cast<const double2*>(sd + (g * L + n1) * kTlRowD + 2 * warp);
+      const double s = __ldg(Q.T.gam + (int64_t)Q.N2 * n1 + n2a + g);
+      v[g * E + e] = make_double2(z.x * s, z.y * s);
+    }
+  __syncthreads();                                      // the FFT scratch overlaps the staged tile
+  fft4_s1_to_s2<E, -1>(v, sm + warp * kWarpScratch, Q.log2N1, Q.tw, Q.twlog, lane);
+  __syncthreads();
+  {
+    const int g = lane / E, k1 = lane % E, n2 = n2a + g;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int k = k1 + E * r;
+      sm[(g * L + k) * kTlRowC + warp] = cmul(v[r], tl_tw(Q, n2 * k));
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int g = row % G, k = row / G;
+    const int64_t p = chunk * kTlPairs + w;
+    if (p < Q.P) Y[((int64_t)k * Q.N2 + n2a + g) * Q.P + p] = sm[(g * L + k) * kTlRowC + w];
+  }
+}
+
+// Pass B forward: Y rows (k1a + g)·N2 + n2; length-N2 DFT over n2; store X[(k1a + g) + N1·k2][p].
+template <int E>
+__global__ void __launch_bounds__(kTlThreads, 1)
+k_tl_b_fwd(const double2* __restrict__ Y, double2* __restrict__ X, TlongParams Q) {
+  constexpr int G = 32 / E, L = 32 * E;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = blockIdx.x % Q.nch;
+  const int k1a = (int)(blockIdx.x / Q.nch) * G;
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int n2 = row % L, g = row / L;                // consecutive n2 are adjacent rows of Y
+    const int64_t p = chunk * kTlPairs + w;
+    double2* d = sm + (g * L + n2) * kTlRowC + w;
+    if (p < Q.P) cp_async16(d, Y + ((int64_t)(k1a + g) * Q.N2 + n2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  double2 v[32];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[g * E + e] = sm[(g * L + lane + 32 * e) * kTlRowC + warp];
+  __syncthreads();
+  fft4_s1_to_s2<E, -1>(v, sm + warp * kWarpScratch, Q.log2N2, Q.tw, Q.twlog, lane);
+  __syncthreads();
+  {
+    const int g = lane / E, ka = lane % E;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) sm[(g * L + ka + E * r) * kTlRowC + warp] = v[r];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int g = row % G, k2 = row / G;                // consecutive g are adjacent bins
+    const int64_t p = chunk * kTlPairs + w;
+    if (p < Q.P) X[((int64_t)(k1a + g) + (int64_t)Q.N1 * k2) * Q.P + p] = sm[(g * L + k2) * kTlRowC + w];
+  }
+}
+
+// Step (2): separate the packed pair from bins k and N−k, divide each by its mode's shifted
+// eigenvalue (d_k + e_k μ_s [+ λ_{3,k} Λ_s]; CH: J̄ from the device stats), recombine in place.
+__global__ void __launch_bounds__(256)
+k_tl_divide(double2* __restrict__ X, TlongParams Q) {
+  const int64_t half = Q.N >> 1, total = (half + 1) * Q.P;
+  const double jbar = Q.T.kind >= 2 ? Q.T.st->jbar : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / Q.P, p = i - k * Q.P;
+    const int64_t km = (Q.N - k) & (Q.N - 1);
+    const double2 Zl = X[k * Q.P + p], Zm = X[km * Q.P + p];
+    const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
+    const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
+    const int64_t sa = 2 * p, sb = sa + 1;
+    const bool hb = sb < Q.ns;
+    const double2 d = __ldg(Q.T.dl + k);
+    const double mua = mode_mu(sa, Q.T, jbar);
+    const double mub = hb ? mode_mu(sb, Q.T, jbar) : mua;
+    const double2 fa = cinv(shifted(d, Q.T.el, (int)k, mua, Q.T.l3, Q.T.l3 ? mode_lam(sa, Q.T) : 0.0));
+    const double2 fb = cinv(shifted(d, Q.T.el, (int)k, mub, Q.T.l3, Q.T.l3 && hb ? mode_lam(sb, Q.T) : 0.0));
+    const double2 Af = cmul(A, fa), Bf = cmul(B, fb);
+    X[k * Q.P + p] = make_double2(Af.x - Bf.y, Af.y + Bf.x);
+    if (km != k) X[km * Q.P + p] = make_double2(Af.x + Bf.y, Bf.x - Af.y);
+  }
+}
+
+// Pass B inverse: X rows (k1a + g) + N1·k2; length-N2 inverse DFT over k2; × W_N^{-n2 k1};
+// store Y[k1][n2][p].
+template <int E>
+__global__ void __launch_bounds__(kTlThreads, 1)
+k_tl_b_inv(const double2* __restrict__ X, double2* __restrict__ Y, TlongParams Q) {
+  constexpr int G = 32 / E, L = 32 * E;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = blockIdx.x % Q.nch;
+  const int k1a = (int)(blockIdx.x / Q.nch) * G;
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int g = row % G, k2 = row / G;
+    const int64_t p = chunk * kTlPairs + w;
+    double2* d = sm + (g * L + k2) * kTlRowC + w;
+    if (p < Q.P) cp_async16(d, X + ((int64_t)(k1a + g) + (int64_t)Q.N1 * k2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  double2 v[32];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[g * E + e] = sm[(g * L + lane + 32 * e) * kTlRowC + warp];
+  __syncthreads();
+  fft4_s1_to_s2<E, +1>(v, sm + warp * kWarpScratch, Q.log2N2, Q.tw, Q.twlog, lane);
+  __syncthreads();
+  {
+    const int g = lane / E, na = lane % E, k1 = k1a + g;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int n2 = na + E * r;
+      sm[(g * L + n2) * kTlRowC + warp] = cmul(v[r], cconj(tl_tw(Q, n2 * k1)));
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int n2 = row % L, g = row / L;
+    const int64_t p = chunk * kTlPairs + w;
+    if (p < Q.P) Y[((int64_t)(k1a + g) * Q.N2 + n2) * Q.P + p] = sm[(g * L + n2) * kTlRowC + w];
+  }
+}
+
+// Pass A inverse: Y rows k1·N2 + n2a + g; length-N1 inverse DFT over k1; × ginv[n] (Γ_α⁻¹ and all
+// normalisations); real part → column 2p, imaginary part → 2p+1 of row n = N2·n1 + n2a + g.
+template <int E>
+__global__ void __launch_bounds__(kTlThreads, 1)
+k_tl_a_inv(const double2* __restrict__ Y, double* __restrict__ out, TlongParams Q) {
+  constexpr int G = 32 / E, L = 32 * E;
+  extern __shared__ double2 sm[];
+  double* sd = reinterpret_cast<double*>(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = blockIdx.x % Q.nch;
+  const int n2a = (int)(blockIdx.x / Q.nch) * G;
+  const int64_t c0 = chunk * (2 * kTlPairs);
+  for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+    const int w = idx & 7, row = idx >> 3;
+    const int g = row % G, k1 = row / G;
+    const int64_t p = chunk * kTlPairs + w;
+    double2* d = sm + (g * L + k1) * kTlRowC + w;
+    if (p < Q.P) cp_async16(d, Y + ((int64_t)k1 * Q.N2 + n2a + g) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  double2 v[32];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[g * E + e] = sm[(g * L + lane + 32 * e) * kTlRowC + warp];
+  __syncthreads();
+  fft4_s1_to_s2<E, +1>(v, sm + warp * kWarpScratch, Q.log2N1, Q.tw, Q.twlog, lane);
+  __syncthreads();
+  {
+    const int g = lane / E, na = lane % E;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int n1 = na + E * r;
+      const double s = __ldg(Q.T.ginv + (int64_t)Q.N2 * n1 + n2a + g);
+      *reinterpret_cast<double2*>(sd + (g * L + n1) * kTlRowD + 2 * warp) = make_double2(v[r].x * s, v[r].y * s);
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
+    const int c = idx & 15, row = idx >> 4;
+    const int g = row % G, n1 = row / G;
+    const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+    if (c0 + c < Q.ns) out[n * Q.ns + c0 + c] = sd[(g * L + n1) * kTlRowD + c];
+  }
+}
+#endif  // PD_TLONG_KERNELS
+
+}  // namespace pd

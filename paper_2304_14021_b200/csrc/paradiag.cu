@@ -24,6 +24,7 @@
 #include "k_spatial.cuh"
 #include "k_time.cuh"
 #include "fast_launch.cuh"
+#include "tlong.h"
 
 using namespace pd;
 
@@ -52,14 +53,18 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
-                K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, PD_NKERNELS };
+                K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI,
+                PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
                                          "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update",
-                                         "residual_update"};
+                                         "residual_update", "tlong_a_fwd", "tlong_b_fwd", "tlong_divide",
+                                         "tlong_b_inv", "tlong_a_inv"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per CTA (sm_100a)
+constexpr int kMaxNtShort = 4096;         // one pencil per warp on chip; longer windows: k_tlong.cuh
+constexpr int kMaxNt = 1 << 20;           // four-step factors N1, N2 <= 1024
 constexpr int kTime1DWarps = 4;
 constexpr int kLineWarps = 4;   // spatial DTT rows: one warp per row, 4 rows per CTA
 #ifndef PD_COLW
@@ -123,6 +128,11 @@ struct pd_handle {
   double* Ub = nullptr;
   double* work2 = nullptr;
   bool pipe = false;                  // PARADIAG_PIPELINE=1 enables (≈ neutral on c5, +2 arrays)
+  // long windows (N_t > 4096, or PARADIAG_TLONG=1 from N_t = 1024): four-step time pass over HBM
+  // (k_tlong.cuh); Y = spec, X = w1, each [N_t][⌈N_s/2⌉] complex.  1D then solves Step (2) in the
+  // DST-I/DCT-I eigenbasis like 2D (x passes + per-mode divide) instead of the pentadiagonal LU.
+  bool tlong = false;
+  int log2n1 = 0, log2n2 = 0;
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -182,7 +192,9 @@ int validate(const pd_problem* p) {
   if (p->dim != 1 && p->dim != 2) return fail(PD_EINVAL, "dim must be 1 or 2");
   if (is_ch(p->kind) && (p->dim != 2 || p->bc != PD_BC_NEUMANN))
     return fail(PD_EINVAL, "Cahn-Hilliard is supported in 2D with Neumann BCs (P:59)");
-  if (!is_pow2(p->nt) || p->nt < 2 || p->nt > 4096) return fail(PD_EINVAL, "nt must be a power of two in [2, 4096]");
+  if (!is_pow2(p->nt) || p->nt < 2 || p->nt > kMaxNt) return fail(PD_EINVAL, "nt must be a power of two in [2, 2^20]");
+  if (p->nt > kMaxNtShort && p->dim == 1 && (!is_pow2(p->m) || p->m > 4096))
+    return fail(PD_EINVAL, "1D with nt > 4096 (spectral long-window path): m must be a power of two <= 4096");
   if (p->dim == 2 && (!is_pow2(p->m) || p->m < 4 || p->m > 4096))
     return fail(PD_EINVAL, "2D: m (intervals per axis) must be a power of two in [4, 4096]");
   if (p->dim == 1 && (p->m < 4 || p->m > (1 << 20))) return fail(PD_EINVAL, "1D: m must be in [4, 2^20]");
@@ -266,9 +278,9 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
       nparts = (size_t)grd.x * grd.y * grd.z;
     }
   } else {
-    dim3 blk(256, 1);
-    dim3 grd((h->nx + blk.x - 1) / blk.x, 1, h->P.nt);
-    k_residual<<<grd, blk, 0, h->stream>>>(u0, U, r, R, h->jpart);
+    // 1D (linear kinds only): flattened grid-stride map
+    const unsigned grid = (unsigned)std::min<int64_t>((h->total + 255) / 256, 148 * 16);
+    k_residual_1d<<<grid, 256, 0, h->stream>>>(u0, U, r, R);
   }
   prof_end(h, kid);
   PD_LAUNCHED();
@@ -368,6 +380,28 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
   return T;
 }
 
+// Long-window time pass (k_tlong.cuh) on spatially transformed data: in → Y → X (divided) → Y → out.
+int tlong_time(pd_handle* h, const double* in, double* out) {
+  TlongParams Q;
+  Q.N = h->P.nt; Q.log2N = h->log2nt;
+  Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = 1 << h->log2n1; Q.N2 = 1 << h->log2n2;
+  Q.ns = h->ns; Q.P = (h->ns + 1) / 2; Q.nch = (Q.P + kTlPairs - 1) / kTlPairs;
+  Q.tw = h->tw; Q.twlog = h->twlog;
+  Q.T = time_params(h, nullptr);
+  double2* Y = h->spec;
+  double2* X = h->w1;
+  const int kid[5] = {K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI};
+  const void* ins[5] = {in, Y, nullptr, X, Y};
+  void* outs[5] = {Y, X, X, Y, out};
+  for (int stage = 0; stage < 5; ++stage) {
+    prof_begin(h, kid[stage]);
+    if (!tlong_launch(stage, ins[stage], outs[stage], Q, h->stream)) return fail(PD_EINVAL, "tlong: unsupported N_t split");
+    prof_end(h, kid[stage]);
+    PD_LAUNCHED();
+  }
+  return PD_OK;
+}
+
 // The last 2D pass (x-inverse, rows) can apply the update U += δ itself (k_rows3 epilogue): only
 // the register-FFT v3 line kernels implement it.
 bool can_fuse_update(const pd_handle* h) {
@@ -385,12 +419,15 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     int rc;
     // when both the v3 column kernel and the register-FFT time pass run, the y passes carry
     // Γ_α (forward outputs) and Γ_α⁻¹·1/(N_t (2m)²) (inverse outputs) for the time pass
-    const bool fold = h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
+    const bool fold = !h->tlong && h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
                       h->P.nt <= 1024;
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) return rc;
     TimeParams T = time_params(h, nullptr);
     T.gamma_folded = fold ? 1 : 0;
+    if (h->tlong) {
+      if ((rc = tlong_time(h, delta, delta))) return rc;
+    } else {
     prof_begin(h, K_TIME);
     if (!fast_time_any(h, delta, delta, T)) {
       // generic time pass (N_t outside the register-FFT sizes): one pencil pair per warp, fewer
@@ -405,10 +442,17 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     }
     prof_end(h, K_TIME);
     PD_LAUNCHED();
+    }
     if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) return rc;
     if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
     if ((rc = launch_lines(h, delta, delta, 0, dmax, K_XINV))) return rc;
     return PD_OK;
+  }
+  if (h->tlong) {     // 1D long window: DST-I/DCT-I along x, four-step time pass with divide, inverse
+    int rc;
+    if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
+    if ((rc = tlong_time(h, delta, delta))) return rc;
+    return launch_lines(h, delta, delta, 0, dmax, K_XINV);
   }
   TimeParams T = time_params(h, nullptr);
   const bool w4 = time_smem(h->P.nt, kTime1DWarps) <= kSmemMax;     // else one warp per CTA (N_t = 4096)
@@ -589,7 +633,9 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   geometry(p, &nx, &ny);
   const size_t ns = (size_t)nx * ny, total = ns * p->nt, nb = p->nt / 2 + 1;
   size_t b = total * sizeof(double) + ns * sizeof(double);
-  if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
+  const bool tl = p->nt > kMaxNtShort;
+  if (tl) b += 2 * (size_t)p->nt * ((ns + 1) / 2) * sizeof(double2);       // Y, X of k_tlong.cuh
+  else if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
@@ -633,7 +679,13 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   h->b2 = p->beta * p->beta;
   h->e2 = p->eps * p->eps;
   const int M = (int)p->m;
-  h->log2h = p->dim == 2 ? ilog2(M) - 1 : 0;
+  {
+    const char* f = std::getenv("PARADIAG_TLONG");
+    const bool force = f && std::atoi(f) != 0;
+    h->tlong = p->nt > kMaxNtShort || (force && p->nt >= 1024 && (p->dim == 2 || (is_pow2(M) && M <= 4096)));
+    tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
+  }
+  h->log2h = (p->dim == 2 || h->tlong) ? ilog2(M) - 1 : 0;
   h->twlog = std::max(h->log2nt, h->log2h);
 
   auto cleanup = [&](int code) {
@@ -648,7 +700,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   std::vector<double2> dl(nt), el(nt), tw(size_t(1) << h->twlog), trig(M + 1);
   const double lna = std::log(p->alpha);
   const double z = std::exp(lna / nt);
-  const double spatial_scale = p->dim == 2 ? 1.0 / ((2.0 * M) * (2.0 * M)) : 1.0;
+  const double spatial_scale = p->dim == 2 ? 1.0 / ((2.0 * M) * (2.0 * M)) : h->tlong ? 1.0 / (2.0 * M) : 1.0;
   for (int j = 0; j < nt; ++j) {
     gam[j] = std::exp(j * lna / nt);
     ginv[j] = std::exp(-j * lna / nt) * (spatial_scale / nt);
@@ -734,7 +786,18 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       (!trig2p.empty() && up(h->trig2p, trig2p.data(), trig2p.size() * sizeof(double2))))
     return cleanup(fail(PD_ECUDA, "table upload failed"));
 
-  if (p->dim == 1) {
+  if (h->tlong) {
+    const size_t nc = (size_t)nt * (size_t)((h->ns + 1) / 2);
+    PD_TRY(dalloc(h, &h->spec, nc));
+    PD_TRY(dalloc(h, &h->w1, nc));
+    if (tlong_attrs() != cudaSuccess) return cleanup(fail(PD_ECUDA, "tlong kernel attributes"));
+  }
+  if (p->dim == 1 && h->tlong) {
+    PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));
+    PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
+    if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
+    PD_TRY(setup_fast_attrs(h));
+  } else if (p->dim == 1) {
     const size_t nf = (size_t)h->nx * h->nb;
     PD_TRY(dalloc(h, &h->spec, nf));
     PD_TRY(dalloc(h, &h->w1, nf));
@@ -778,8 +841,12 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       PD_TRY(allow_smem(k_time_inv_1d<1>, time_smem(nt, 1)));
     }
   } else {
-    if (time_smem(nt, kTimeWarps) <= kSmemMax) PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
-    else PD_TRY(allow_smem(k_time_solve_2d<1>, time_smem(nt, 1)));
+    if (h->tlong) {
+    } else if (time_smem(nt, kTimeWarps) <= kSmemMax) {
+      PD_TRY(allow_smem(k_time_solve_2d<kTimeWarps>, time_smem(nt, kTimeWarps)));
+    } else {
+      PD_TRY(allow_smem(k_time_solve_2d<1>, time_smem(nt, 1)));
+    }
     PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));

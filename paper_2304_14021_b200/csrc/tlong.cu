@@ -1,0 +1,74 @@
+// tlong.cu — launch wrappers of the long-window time pass (k_tlong.cuh), one instantiation per
+// transform length 32·E of each four-step factor.  paradiag.cu sees only tlong.h.
+#define PD_TLONG_KERNELS
+#include "tlong.h"
+
+#include <algorithm>
+
+namespace pd {
+
+namespace {
+
+template <int E>
+cudaError_t attrs_e() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_tl_a_fwd<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  if ((e = cudaFuncSetAttribute(k_tl_b_fwd<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  if ((e = cudaFuncSetAttribute(k_tl_b_inv<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  return cudaFuncSetAttribute(k_tl_a_inv<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem);
+}
+
+// CTAs of a pass over transform length L = 32·E: (N / L) / (32 / E) groups × chunks
+unsigned grid_of(int L, const TlongParams& Q) {
+  const int64_t groups = (int64_t)(Q.N / L) / (1024 / L);
+  return (unsigned)(groups * Q.nch);
+}
+
+template <int E>
+void launch_e(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s) {
+  constexpr int L = 32 * E;
+  const unsigned grid = grid_of(L, Q);
+  switch (stage) {
+    case 0: k_tl_a_fwd<E><<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double*>(in), static_cast<double2*>(out), Q); break;
+    case 1: k_tl_b_fwd<E><<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
+    case 3: k_tl_b_inv<E><<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
+    case 4: k_tl_a_inv<E><<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double*>(out), Q); break;
+    default: break;
+  }
+}
+
+}  // namespace
+
+void tlong_split(int log2N, int* log2N1, int* log2N2) {
+  *log2N1 = (log2N + 1) / 2;
+  *log2N2 = log2N - *log2N1;
+}
+
+cudaError_t tlong_attrs() {
+  cudaError_t e;
+  if ((e = attrs_e<1>()) || (e = attrs_e<2>()) || (e = attrs_e<4>()) || (e = attrs_e<8>()) || (e = attrs_e<16>()) ||
+      (e = attrs_e<32>()))
+    return e;
+  return cudaSuccess;
+}
+
+bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s) {
+  if (stage == 2) {
+    const int64_t total = (int64_t)(Q.N / 2 + 1) * Q.P;
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    k_tl_divide<<<grid, 256, 0, s>>>(static_cast<double2*>(out), Q);
+    return true;
+  }
+  const int L = (stage == 0 || stage == 4) ? Q.N1 : Q.N2;
+  switch (L) {
+    case 32: launch_e<1>(stage, in, out, Q, s); return true;
+    case 64: launch_e<2>(stage, in, out, Q, s); return true;
+    case 128: launch_e<4>(stage, in, out, Q, s); return true;
+    case 256: launch_e<8>(stage, in, out, Q, s); return true;
+    case 512: launch_e<16>(stage, in, out, Q, s); return true;
+    case 1024: launch_e<32>(stage, in, out, Q, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace pd

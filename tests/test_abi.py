@@ -47,7 +47,7 @@ def test_workspace_bytes_all_configs(lib, name):
     assert b >= p.dofs * 8
 
 
-@pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=100), dict(nt=1), dict(nt=8192),
+@pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=100), dict(nt=1), dict(nt=1 << 21),
                                  dict(theta=0.4), dict(theta=1.1), dict(m=100), dict(eps=-1.0), dict(t_window=0.0),
                                  dict(kind="cahn_hilliard"), dict(n_windows=0), dict(tol=0.0)])
 def test_invalid_problems_rejected(lib, bad):
@@ -60,6 +60,17 @@ def test_invalid_problems_rejected(lib, bad):
 def test_max_nt_accepted(lib):
     """N_t = 4096 is the documented maximum (include/paradiag.h); the GPU parity suite runs it."""
     assert pd.paradiag_workspace_bytes(pd.make_problem(config("c2"), nt=4096)) > 0
+
+
+def test_long_window_limits(lib):
+    """N_t > 4096 takes the four-step time pass (k_tlong.cuh): up to 2^20 (c6, NEXT-3); in 1D it
+    solves Step (2) in the DST/DCT eigenbasis, so m must be a power of two there."""
+    b = pd.paradiag_workspace_bytes(pd.make_problem(config("c6")))
+    p = config("c6")
+    assert b >= 3 * p.dofs * 8                       # U-sized work + Y + X (complex, ⌈N_s/2⌉ pairs each)
+    with pytest.raises(pd.ParadiagError):
+        pd.paradiag_workspace_bytes(pd.make_problem(config("c6"), m=100))
+    assert pd.paradiag_workspace_bytes(pd.make_problem(config("c6"), m=100, nt=4096)) > 0
 
 
 def test_theta_half_accepted_but_not_for_ch(lib):

@@ -77,6 +77,12 @@ CONFIGS = {
     "c4e": Problem("c4e", "cahn_hilliard_eyre", "neumann", 2, m=256, nt=64, t_window=64e-4, alpha=1e-3,
                    eps=0.02, n_windows=4, max_iter=400, omega=0.7, tau=1.0,
                    u0_range=(-0.1, 0.1), seed=4),
+    # NEXT-3: the long-window 1D run "Δt = 10⁻⁶, i.e. N_t = 10⁶ ... four
+    # iterations", h = 1/64, T = 1, α = 10⁻³ (Fig. 3).  Power-of-two stand-in N_t = 2^20
+    # (Δt = 2^-20 ≈ 9.5e-7; reading R#24); u = u_xx = 0 (the c1 operator); the paper's
+    # random start is read as noise on top of the c1 sine.
+    "c6": Problem("c6", "biharmonic", "hinged", 1, m=64, nt=1 << 20, t_window=1.0, alpha=1e-3,
+                  u0_kind="sine_plus_noise", u0_range=(-0.01, 0.01), seed=6),
 }
 
 
