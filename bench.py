@@ -32,6 +32,12 @@ BYTES_PER_DOF = {  # algorithmic HBM bytes per space-time dof per launch (DESIGN
     "residual": 16.0, "dtt_x_fwd": 16.0, "dtt_y_fwd": 16.0, "time_solve_2d": 16.0,
     "dtt_y_inv": 16.0, "dtt_x_inv": 16.0, "update": 24.0, "dtt_x_inv_update": 24.0,
     "residual_update": 32.0,      # pipelined solve: read U, δ; write U_new, r
+    # long windows (k_tlong.cuh): each pass reads and writes one U-sized array (pairs of real
+    # pencils packed as one complex pencil: ⌈N_s/2⌉·16 B = N_s·8 B per time row)
+    "tlong_a_fwd": 16.0, "tlong_b_fwd": 16.0, "tlong_divide": 16.0, "tlong_b_inv": 16.0, "tlong_a_inv": 16.0,
+    # 1D short rows (k_x1d.cuh): residual fused with the forward x transform (read U, write r̂),
+    # inverse x transform fused with the update (read δ̂, U; write U)
+    "residual_dst_x": 16.0, "dst_x_inv_update": 24.0,
 }
 
 
@@ -90,8 +96,12 @@ class Clocks:
 
 
 def oracle_sample_problem(name):
-    """Bounded sample of the workload for the CPU oracle: same physics and N_t, 65² nodes."""
-    from workloads import twin
+    """Bounded sample of the workload for the CPU oracle: same physics and N_t, 65² nodes (2D);
+    1D long windows (c6): same h and Δt, N_t = 1024 (the naive O(N_t²) DFT bounds the sample)."""
+    from workloads import twin, config
+    p = config(name)
+    if p.dim == 1 and p.nt > 4096:
+        return twin(name, nt=1024, t_window=p.t_window * 1024 / p.nt)
     return twin(name, m=64)
 
 
@@ -107,6 +117,8 @@ def time_oracle(name, steps, warmup):
         cores = os.cpu_count()
     p = oracle_sample_problem(name)
     u0 = make_u0(p)
+    if p.dim == 1:
+        u0 = u0.reshape(-1)            # the oracle's 1D layout
     U = iterate.initial_iterate(p, u0)
     for _ in range(warmup):
         U, _ = iterate.iterate_once(p, u0, U)
@@ -115,7 +127,8 @@ def time_oracle(name, steps, warmup):
         U, _ = iterate.iterate_once(p, u0, U)
     dt = (time.perf_counter() - t0) / max(steps, 1)
     desc = (f"oracle iterate_once (numpy fp64, naive O(N_t^2) DFT, dense DCT-I matmuls) on a "
-            f"{p.ny}x{p.nx} x N_t={p.nt} twin of {name} ({p.dofs} dofs), {steps} iteration(s)")
+            f"{p.ny}x{p.nx} x N_t={p.nt} twin of {name} ({p.dofs} dofs), {steps} iteration(s)"
+            + ("; 1D: banded LU + refinement per bin" if p.dim == 1 else ""))
     return p.dofs / dt, cores, desc, dt
 
 
@@ -283,9 +296,13 @@ def main():
     metric = "space-time dof/s per ParaDiag iteration (fp64)"
     cfg = {"workload": f"BASELINE.json configs[4] ({args.config}): 2D linearised Cahn-Hilliard, Neumann, "
                        f"{p.ny}x{p.nx} nodes, N_t={p.nt}, T={p.t_window}, alpha={p.alpha}, beta={p.beta}, "
-                       f"eps={p.eps}, U0=0" if args.config == "c5" else args.config,
-           "dofs_per_iteration": p.dofs, "l2": "inputs 17.2 GB/array >> 126 MB L2 (no flush needed)"
-           if args.config == "c5" else "see dofs"}
+                       f"eps={p.eps}, U0=0" if args.config == "c5" else
+                       f"{args.config} (SURVEY §8(f) NEXT-3, P:692-699): 1D biharmonic, u = u_xx = 0, h = 1/{p.m} "
+                       f"({p.nx} unknowns), N_t={p.nt} (2^20 stand-in for 10^6), T={p.t_window}, alpha={p.alpha}"
+                       if args.config == "c6" else args.config,
+           "dofs_per_iteration": p.dofs,
+           "l2": (f"inputs {p.dofs * 8 / 1e9:.3g} GB/array >> 126 MB L2 (no flush needed)" if p.dofs * 8 > 4 * 126e6
+                  else "arrays fit in L2: warm-L2 numbers")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -387,8 +404,9 @@ def main():
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "peak_source": peak_src, "traffic": traffic,
                 "algorithmic_bytes_per_launch": bpd * p.dofs}
-    # whole-iteration HBM efficiency at the design byte count
-    design_bytes = sum(BYTES_PER_DOF[k] for k in BYTES_PER_DOF) * p.dofs
+    # whole-iteration HBM efficiency at the design byte count: the algorithmic bytes
+    # of the kernels that ran, per step
+    design_bytes = sum(BYTES_PER_DOF.get(k, 0.0) * n for k, (n, _) in prof.items()) / args.steps * p.dofs
 
     # end-to-end through the host-buffer C-ABI call (H2D u0, K iterations, D2H u_{N_t})
     e2e = None

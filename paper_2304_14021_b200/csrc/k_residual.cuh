@@ -142,12 +142,16 @@ k_residual(const double* __restrict__ u0, const double* __restrict__ U, double* 
 // 1D linear residual, one thread per space-time point over the flattened [N_t][N_x] index
 // (grid-stride): the same per-point arithmetic as k_residual with a dense thread map, so short
 // rows (N_x = 63 at N_t = 2^20, NEXT-3) do not leave most of every block idle.
+// Thread map: lanes of a 2^wlog-wide group walk one row (2^wlog ≥ N_x up to 256), 256 >> wlog rows
+// per block, grid-stride over rows — no 64-bit division in the index math.
 __global__ void __launch_bounds__(256)
 k_residual_1d(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
-              ResidualParams P) {
-  const size_t total = (size_t)P.nx * P.nt;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int n = (int)(i / P.nx), x = (int)(i - (size_t)n * P.nx);
+              ResidualParams P, int wlog) {
+  const int W = 1 << wlog, rpb = 256 >> wlog;
+  const int xl = threadIdx.x & (W - 1);
+  for (int n = blockIdx.x * rpb + (threadIdx.x >> wlog); n < P.nt; n += gridDim.x * rpb)
+  for (int x = xl; x < P.nx; x += W) {
+    const size_t i = (size_t)n * P.nx + x;
     const double* s = U + (size_t)n * P.nx;
     const double* sp = n == 0 ? u0 : U + (size_t)(n - 1) * P.nx;
     const double uc = __ldg(s + x);

@@ -36,17 +36,41 @@ struct TlongParams {
   int N1, N2;              // N = N1·N2, both in [32, 1024]
   int log2N1, log2N2;
   int64_t ns;              // real columns per time row
+  int64_t ld;              // row pitch (doubles) of the real in/out arrays: ns, or 2P (even: 16-byte pairs)
   int64_t P;               // complex pencil pairs = ⌈ns/2⌉ (row pitch of Y and X)
   int64_t nch;             // pair chunks = ⌈P/8⌉
   const double2* tw;       // tw[j] = exp(-2πi j / 2^twlog)
   int twlog;
-  TimeParams T;            // Step-(2) divisor tables (dl, el, l3, lamx, kind, b2, e2, st, nx, ns, gam, ginv)
+  TimeParams T;            // Step-(2) divisor tables (dl, el, l3, lamx, kind, b2, e2, st, nx, ns)
+  // Γ_α split over the four-step index n = N2·n1 + n2: γ_n = ghi[n1]·glo[n2] and
+  // scale/γ_n = gihi[n1]·gilo[n2] (one extra rounding; coalesced instead of stride-N2 gathers)
+  const double* ghi;
+  const double* glo;
+  const double* gihi;
+  const double* gilo;
 };
 
 #ifdef PD_TLONG_KERNELS     // defined only in tlong.cu (the engine sees TlongParams alone)
 PD_DEV double2 tl_tw(const TlongParams& Q, int e) {
   return __ldg(Q.tw + ((size_t)(e & (Q.N - 1)) << (Q.twlog - Q.log2N)));
 }
+
+// The four-step twiddles of one lane: W_N^{±b·(a + E·r)}, r = 0..31, as f·lo[r&7]·hi[r>>3] with
+// f = W_N^{±b·a} and lo/hi the TwPow powers of W_N^{±b·E}: 6 table loads instead of 32 gathers.
+template <int E, int SIGN>
+struct TlTwiddle {
+  TwPow<32, SIGN> w;
+  PD_DEV TlTwiddle(const TlongParams& Q, int a, int b) : w(b * E, Q.log2N, Q.tw, Q.twlog) {
+    double2 f = tl_tw(Q, a * b);
+    if (SIGN > 0) f.y = -f.y;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w.lo[k] = cmul(w.lo[k], f);
+  }
+  PD_DEV double2 apply(double2 v, int r) const {
+    const double2 a = cmul(v, w.lo[r & 7]);
+    return (r >> 3) ? cmul(a, w.hi[r >> 3]) : a;
+  }
+};
 
 // Pass A forward: rows n = N2·n1 + n2a + g (g < G), columns 16·chunk .. +16 of the real input;
 // z = γ_n (r[2p] + i r[2p+1]); length-N1 DFT over n1; × W_N^{n2 k}; store Y[k][n2][p].
@@ -60,13 +84,24 @@ k_tl_a_fwd(const double* __restrict__ in, double2* __restrict__ Y, TlongParams Q
   const int64_t chunk = blockIdx.x % Q.nch;
   const int n2a = (int)(blockIdx.x / Q.nch) * G;
   const int64_t c0 = chunk * (2 * kTlPairs);
-  for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
-    const int c = idx & 15, row = idx >> 4;            // row = n1·G + g: consecutive g are adjacent rows
-    const int g = row % G, n1 = row / G;
-    const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
-    double* d = sd + (g * L + n1) * kTlRowD + c;
-    if (c0 + c < Q.ns) cp_async8(d, in + n * Q.ns + c0 + c);
-    else *d = 0.0;
+  if (!(Q.ld & 1)) {                                    // even pitch: 16-byte pencil pairs
+    for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+      const int w = idx & 7, row = idx >> 3;
+      const int g = row % G, n1 = row / G;
+      const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+      double* d = sd + (g * L + n1) * kTlRowD + 2 * w;
+      if (chunk * kTlPairs + w < Q.P) cp_async16(d, in + n * Q.ld + c0 + 2 * w);
+      else d[0] = d[1] = 0.0;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
+      const int c = idx & 15, row = idx >> 4;          // row = n1·G + g: consecutive g are adjacent rows
+      const int g = row % G, n1 = row / G;
+      const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+      double* d = sd + (g * L + n1) * kTlRowD + c;
+      if (c0 + c < Q.ns) cp_async8(d, in + n * Q.ld + c0 + c);
+      else *d = 0.0;
+    }
   }
   cp_async_commit();
   cp_async_wait_all();
@@ -78,7 +113,7 @@ k_tl_a_fwd(const double* __restrict__ in, double2* __restrict__ Y, TlongParams Q
     for (int e = 0; e < E; ++e) {
       const int n1 = lane + 32 * e;
       const double2 z = *reinterpret_cast<const double2*>(sd + (g * L + n1) * kTlRowD + 2 * warp);
-      const double s = __ldg(Q.T.gam + (int64_t)Q.N2 * n1 + n2a + g);
+      const double s = __ldg(Q.ghi + n1) * __ldg(Q.glo + n2a + g);
       v[g * E + e] = make_double2(z.x * s, z.y * s);
     }
   __syncthreads();                                      // the FFT scratch overlaps the staged tile
@@ -86,11 +121,9 @@ k_tl_a_fwd(const double* __restrict__ in, double2* __restrict__ Y, TlongParams Q
   __syncthreads();
   {
     const int g = lane / E, k1 = lane % E, n2 = n2a + g;
+    const TlTwiddle<E, -1> tw(Q, k1, n2);               // W_N^{n2 (k1 + E r)}
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int k = k1 + E * r;
-      sm[(g * L + k) * kTlRowC + warp] = cmul(v[r], tl_tw(Q, n2 * k));
-    }
+    for (int r = 0; r < 32; ++r) sm[(g * L + k1 + E * r) * kTlRowC + warp] = tw.apply(v[r], r);
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
@@ -199,11 +232,9 @@ k_tl_b_inv(const double2* __restrict__ X, double2* __restrict__ Y, TlongParams Q
   __syncthreads();
   {
     const int g = lane / E, na = lane % E, k1 = k1a + g;
+    const TlTwiddle<E, +1> tw(Q, na, k1);               // W_N^{-k1 (na + E r)}
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int n2 = na + E * r;
-      sm[(g * L + n2) * kTlRowC + warp] = cmul(v[r], cconj(tl_tw(Q, n2 * k1)));
-    }
+    for (int r = 0; r < 32; ++r) sm[(g * L + na + E * r) * kTlRowC + warp] = tw.apply(v[r], r);
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
@@ -250,16 +281,27 @@ k_tl_a_inv(const double2* __restrict__ Y, double* __restrict__ out, TlongParams 
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       const int n1 = na + E * r;
-      const double s = __ldg(Q.T.ginv + (int64_t)Q.N2 * n1 + n2a + g);
+      const double s = __ldg(Q.gihi + n1) * __ldg(Q.gilo + n2a + g);
       *reinterpret_cast<double2*>(sd + (g * L + n1) * kTlRowD + 2 * warp) = make_double2(v[r].x * s, v[r].y * s);
     }
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
-    const int c = idx & 15, row = idx >> 4;
-    const int g = row % G, n1 = row / G;
-    const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
-    if (c0 + c < Q.ns) out[n * Q.ns + c0 + c] = sd[(g * L + n1) * kTlRowD + c];
+  if (!(Q.ld & 1)) {                                    // even pitch: 16-byte pairs (pad column included)
+    for (int idx = threadIdx.x; idx < G * L * kTlPairs; idx += kTlThreads) {
+      const int w = idx & 7, row = idx >> 3;
+      const int g = row % G, n1 = row / G;
+      const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+      if (chunk * kTlPairs + w < Q.P)
+        *reinterpret_cast<double2*>(out + n * Q.ld + c0 + 2 * w) =
+            *reinterpret_cast<const double2*>(sd + (g * L + n1) * kTlRowD + 2 * w);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < G * L * 16; idx += kTlThreads) {
+      const int c = idx & 15, row = idx >> 4;
+      const int g = row % G, n1 = row / G;
+      const int64_t n = (int64_t)Q.N2 * n1 + n2a + g;
+      if (c0 + c < Q.ns) out[n * Q.ld + c0 + c] = sd[(g * L + n1) * kTlRowD + c];
+    }
   }
 }
 #endif  // PD_TLONG_KERNELS

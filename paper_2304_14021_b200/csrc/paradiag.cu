@@ -25,6 +25,7 @@
 #include "k_time.cuh"
 #include "fast_launch.cuh"
 #include "tlong.h"
+#include "k_x1d.cuh"
 
 using namespace pd;
 
@@ -54,12 +55,12 @@ int fail(int code, const std::string& msg) {
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
                 K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI,
-                PD_NKERNELS };
+                K_XRES, K_XUPD, PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
                                          "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update",
                                          "residual_update", "tlong_a_fwd", "tlong_b_fwd", "tlong_divide",
-                                         "tlong_b_inv", "tlong_a_inv"};
+                                         "tlong_b_inv", "tlong_a_inv", "residual_dst_x", "dst_x_inv_update"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per CTA (sm_100a)
@@ -133,6 +134,11 @@ struct pd_handle {
   // DST-I/DCT-I eigenbasis like 2D (x passes + per-mode divide) instead of the pentadiagonal LU.
   bool tlong = false;
   int log2n1 = 0, log2n2 = 0;
+  // 1D long windows with N_x ≤ 64: x transforms as DMMA products with T (k_x1d.cuh), fused with
+  // the residual (forward) and the update (inverse); x1T = Tᵀ zero padded to 64×64
+  bool x1 = false;
+  double* x1T = nullptr;
+  double* tlg = nullptr;              // k_tlong.cuh split Γ_α tables: ghi[N1] glo[N2] gihi[N1] gilo[N2]
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -247,14 +253,44 @@ int setup_fast_attrs(pd_handle* h) {
   return PD_OK;
 }
 
-int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, const double* dU = nullptr,
-                    double* unew = nullptr) {
+// k_x1d workspace row pitch: 2⌈N_x/2⌉ doubles (the time pass reads 16-byte pencil pairs)
+size_t x1_pitch(const pd_handle* h) { return (size_t)((h->nx + 1) / 2) * 2; }
+
+ResidualParams residual_params(pd_handle* h) {
   ResidualParams R;
   R.nx = h->nx; R.ny = h->ny; R.nt = h->P.nt; R.dim = h->P.dim;
   R.neumann = h->neumann; R.kind = h->P.kind;
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
   R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr; R.theta = h->P.theta;
-  R.dU = dU; R.unew = unew; R.umax = &h->st->umax_bits;
+  R.dU = nullptr; R.unew = nullptr; R.umax = &h->st->umax_bits;
+  return R;
+}
+
+// 1D long windows with N_x ≤ 64 (k_x1d.cuh): MODE 0 residual + forward x transform, 1 forward,
+// 2 inverse (‖δ‖∞), 3 inverse + update
+int launch_x1d(pd_handle* h, int mode, const double* u0, const double* in, double* out, int kid) {
+  X1Params Q;
+  Q.nx = h->nx; Q.nt = h->P.nt; Q.R = residual_params(h); Q.B = h->x1T; Q.st = h->st;
+  Q.ld_in = mode <= 1 ? h->nx : (int)x1_pitch(h);       // user arrays: N_x; workspace: even pitch
+  Q.ld_out = mode <= 1 ? (int)x1_pitch(h) : h->nx;
+  const int units = (h->P.nt + 7) / 8;
+  const unsigned grid = (unsigned)std::min((units + kX1Warps - 1) / kX1Warps, 148 * 2);
+  prof_begin(h, kid);
+  switch (mode) {
+    case 0: k_x1d<0><<<grid, kX1Threads, kX1Smem, h->stream>>>(u0, in, out, Q); break;
+    case 1: k_x1d<1><<<grid, kX1Threads, kX1Smem, h->stream>>>(u0, in, out, Q); break;
+    case 2: k_x1d<2><<<grid, kX1Threads, kX1Smem, h->stream>>>(u0, in, out, Q); break;
+    default: k_x1d<3><<<grid, kX1Threads, kX1Smem, h->stream>>>(u0, in, out, Q); break;
+  }
+  prof_end(h, kid);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, const double* dU = nullptr,
+                    double* unew = nullptr) {
+  ResidualParams R = residual_params(h);
+  R.dU = dU; R.unew = unew;
   const int kid = dU ? K_RESUPD : K_RESIDUAL;
   prof_begin(h, kid);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
@@ -279,8 +315,11 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
     }
   } else {
     // 1D (linear kinds only): flattened grid-stride map
-    const unsigned grid = (unsigned)std::min<int64_t>((h->total + 255) / 256, 148 * 16);
-    k_residual_1d<<<grid, 256, 0, h->stream>>>(u0, U, r, R);
+    int wlog = 5;
+    while ((1 << wlog) < h->nx && wlog < 8) ++wlog;
+    const int rpb = 256 >> wlog;
+    const unsigned grid = (unsigned)std::min<int64_t>((h->P.nt + rpb - 1) / rpb, 148 * 16);
+    k_residual_1d<<<grid, 256, 0, h->stream>>>(u0, U, r, R, wlog);
   }
   prof_end(h, kid);
   PD_LAUNCHED();
@@ -386,6 +425,8 @@ int tlong_time(pd_handle* h, const double* in, double* out) {
   Q.N = h->P.nt; Q.log2N = h->log2nt;
   Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = 1 << h->log2n1; Q.N2 = 1 << h->log2n2;
   Q.ns = h->ns; Q.P = (h->ns + 1) / 2; Q.nch = (Q.P + kTlPairs - 1) / kTlPairs;
+  Q.ld = h->x1 ? (int64_t)x1_pitch(h) : h->ns;
+  Q.ghi = h->tlg; Q.glo = h->tlg + Q.N1; Q.gihi = h->tlg + Q.N1 + Q.N2; Q.gilo = h->tlg + 2 * Q.N1 + Q.N2;
   Q.tw = h->tw; Q.twlog = h->twlog;
   Q.T = time_params(h, nullptr);
   double2* Y = h->spec;
@@ -450,6 +491,11 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   }
   if (h->tlong) {     // 1D long window: DST-I/DCT-I along x, four-step time pass with divide, inverse
     int rc;
+    if (h->x1) {       // r̂, δ̂ in the workspace (even row pitch), r and δ in the caller's layout
+      if ((rc = launch_x1d(h, 1, nullptr, r, h->work, K_XFWD))) return rc;
+      if ((rc = tlong_time(h, h->work, h->work))) return rc;
+      return launch_x1d(h, 2, nullptr, h->work, delta, K_XINV);
+    }
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
     if ((rc = tlong_time(h, delta, delta))) return rc;
     return launch_lines(h, delta, delta, 0, dmax, K_XINV);
@@ -502,8 +548,13 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   int rc;
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
-  if ((rc = launch_residual(h, u0, U, h->work))) return rc;
-  if (can_fuse_update(h)) {
+  if (h->x1) {           // residual + x transform, time pass, x inverse + update: 7 passes
+    if ((rc = launch_x1d(h, 0, u0, U, h->work, K_XRES))) return rc;
+    if ((rc = tlong_time(h, h->work, h->work))) return rc;
+    if ((rc = launch_x1d(h, 3, nullptr, h->work, U, K_XUPD))) return rc;
+  } else if ((rc = launch_residual(h, u0, U, h->work))) {
+    return rc;
+  } else if (can_fuse_update(h)) {
     if ((rc = precond(h, h->work, h->work, U))) return rc;
   } else {
     if ((rc = precond(h, h->work, h->work))) return rc;
@@ -684,6 +735,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     const bool force = f && std::atoi(f) != 0;
     h->tlong = p->nt > kMaxNtShort || (force && p->nt >= 1024 && (p->dim == 2 || (is_pow2(M) && M <= 4096)));
     tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
+    h->x1 = h->tlong && p->dim == 1 && h->nx <= 2 * kX1H;
+    if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
   }
   h->log2h = (p->dim == 2 || h->tlong) ? ilog2(M) - 1 : 0;
   h->twlog = std::max(h->log2nt, h->log2h);
@@ -752,7 +805,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   }
 
   // ---- device buffers
-  if (!slab) PD_TRY(dalloc(h, &h->work, (size_t)h->total));   // slab mode: caller-owned buffers
+  // slab mode: caller-owned buffers; k_x1d's workspace rows have an even pitch (pencil pairs)
+  if (!slab) PD_TRY(dalloc(h, &h->work, h->x1 ? (size_t)nt * x1_pitch(h) : (size_t)h->total));
   PD_TRY(dalloc(h, &h->u0buf, (size_t)h->ns));
   PD_TRY(dalloc(h, &h->gam, nt));
   PD_TRY(dalloc(h, &h->ginv, nt));
@@ -787,10 +841,50 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     return cleanup(fail(PD_ECUDA, "table upload failed"));
 
   if (h->tlong) {
+    // γ_n = α^{n/N_t} (R#2) split at n = N2·n1 + n2; the inverse side carries 1/N_t and the spatial
+    // normalisation like ginv
+    const int N1 = 1 << h->log2n1, N2 = 1 << h->log2n2;
+    std::vector<double> g(2 * (size_t)(N1 + N2));
+    for (int i = 0; i < N1; ++i) {
+      g[i] = std::exp((double)N2 * i * lna / nt);
+      g[N1 + N2 + i] = std::exp(-(double)N2 * i * lna / nt) * (spatial_scale / nt);
+    }
+    for (int i = 0; i < N2; ++i) {
+      g[N1 + i] = std::exp((double)i * lna / nt);
+      g[2 * N1 + N2 + i] = std::exp(-(double)i * lna / nt);
+    }
+    PD_TRY(dalloc(h, &h->tlg, g.size()));
+    if (up(h->tlg, g.data(), g.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "tlong table upload"));
     const size_t nc = (size_t)nt * (size_t)((h->ns + 1) / 2);
     PD_TRY(dalloc(h, &h->spec, nc));
     PD_TRY(dalloc(h, &h->w1, nc));
     if (tlong_attrs() != cudaSuccess) return cleanup(fail(PD_ECUDA, "tlong kernel attributes"));
+  }
+  if (h->x1) {
+    // B[0][j][i] = T[2i][j], B[1][j][i] = T[2i+1][j] (k_x1d.cuh even/odd halves): Neumann
+    // T[p][j] = c_j cos(π p j/m) (c = 1 at j = 0, m, else 2), hinged T[p][j] = 2 sin(π (p+1)(j+1)/m);
+    // angles by the exact integer reduction (p·j) mod 2m
+    const int n = h->nx, nh = n / 2, hc = (n + 1) / 2;
+    auto Tkj = [&](int k, int j) {
+      if (h->neumann) {
+        const long a = ((long)k * j) % (2L * M);
+        return std::cos(M_PI * (double)a / M) * ((j == 0 || j == M) ? 1.0 : 2.0);
+      }
+      const long a = ((long)(k + 1) * (j + 1)) % (2L * M);
+      return 2.0 * std::sin(M_PI * (double)a / M);
+    };
+    std::vector<double> B((size_t)2 * kX1H * kX1H, 0.0);
+    for (int j = 0; j < hc; ++j)
+      for (int i = 0; 2 * i < n; ++i) {
+        B[(size_t)j * kX1H + i] = Tkj(2 * i, j);
+        if (j < nh && 2 * i + 1 < n) B[(size_t)(kX1H + j) * kX1H + i] = Tkj(2 * i + 1, j);
+      }
+    PD_TRY(dalloc(h, &h->x1T, B.size()));
+    if (up(h->x1T, B.data(), B.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "T upload"));
+    PD_TRY(allow_smem(k_x1d<0>, kX1Smem));
+    PD_TRY(allow_smem(k_x1d<1>, kX1Smem));
+    PD_TRY(allow_smem(k_x1d<2>, kX1Smem));
+    PD_TRY(allow_smem(k_x1d<3>, kX1Smem));
   }
   if (p->dim == 1 && h->tlong) {
     PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));

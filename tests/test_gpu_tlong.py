@@ -3,7 +3,9 @@
 N_t > 4096 runs the four-step time FFT over HBM (N_t = N1·N2) with Step (2) as a per-mode divide in
 the DST-I/DCT-I eigenbasis (1D and 2D).  PARADIAG_TLONG=1 forces the same path from N_t = 1024, so
 the oracle (naive DFT + banded LU in 1D) checks every four-step factor length (32..128)
-at sizes it finishes in seconds; N_t = 8192 is the first size that takes the path unforced.
+at sizes it finishes in seconds; N_t = 8192 is the first size that takes the path unforced.  1D rows
+of N_x ≤ 64 take the DMMA x transforms of k_x1d.cuh (fused with residual and update), longer rows
+the register-FFT line kernels.
 BJ-style bars: P_α⁻¹ ≤ 1e-11 relative, solves ≤ 1e-10 (linear) / 1e-8 (CH) with identical counts.
 Full size (c6, N_t = 2^20): iteration count and sampled iterates vs the closed-form per-mode WR
 iterate (oracle/modespace.py), where the physical-space oracle would need an N_t² DFT.
@@ -14,7 +16,7 @@ import numpy as np
 import pytest
 
 from _helpers import gshape, to_dev, to_host, rel_err, oracle_u0
-from oracle import iterate, precond, modespace, spatial
+from oracle import iterate, precond, modespace, spatial, circulant
 from workloads import config, twin, make_u0
 
 pytestmark = pytest.mark.gpu
@@ -30,6 +32,7 @@ FORCED = {
     "c6_nt1024": _c6(1024),
     "c6_nt2048_theta": _c6(2048, theta=0.5),
     "c2n_m256_nt4096": twin("c2", m=256, nt=4096, t_window=1.0),          # 257 nodes: odd N_s, Neumann
+    "c2n_m32_nt1024": twin("c2", m=32, nt=1024, t_window=0.25),           # 33 nodes: DMMA x transform, Neumann
     "c3_m16_nt1024": twin("c3", m=16, nt=1024, t_window=0.4),             # 2D hinged, 225 modes
     "c5_m8_nt2048_theta": twin("c5", m=8, nt=2048, t_window=2.0, theta=0.5, init="broadcast", fixed_iters=None),
     "c4e_m16_nt1024": twin("c4e", m=16, nt=1024, t_window=1024e-5, n_windows=1),   # CH: J̄ in the divide
@@ -51,6 +54,21 @@ def _is_ch(p):
     return p.kind.startswith("cahn_hilliard")
 
 
+def _rounding_floor_1d(p, r, d_lu):
+    """The rounding floor of this P_α⁻¹ instance: the oracle's own Step (2) solved a second, equally
+    exact way (the eigenbasis divide the GPU uses, as oracle.precond.step2_2d does in 2D) differs
+    from its banded-LU result by this much; 1D Neumann instances near the growing modes of linear
+    CH (μ < 0) sit at ~3e-12."""
+    S1 = circulant.step1(r, p.alpha)
+    d = circulant.eig_d(p.nt, p.alpha, circulant.inv_dt(p))
+    e = circulant.eig_e(p.nt, p.alpha, p.theta)
+    T = spatial.transform_matrix(p.m, p.bc)
+    mu = spatial.mu(spatial.Lam_grid(p), p).reshape(-1)
+    S2 = ((S1 @ T.T) / (d[:, None] + e[:, None] * mu[None, :])) @ T.T / (2.0 * p.m)
+    d_sp, _ = circulant.step3(S2, p.alpha)
+    return rel_err(d_sp, d_lu)
+
+
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_tlong_precond_parity(solver_for, name):
     p = CASES[name]
@@ -60,10 +78,13 @@ def test_tlong_precond_parity(solver_for, name):
     rd = to_dev(r, p)
     d = s.empty()
     s.apply_precond(rd, d, jbar)
-    d_o, _ = precond.apply_precond(p, r.reshape(p.nt, p.nx) if p.dim == 1 else r, jbar)
-    assert rel_err(to_host(d, p), d_o) <= 1e-11
+    r_o = r.reshape(p.nt, p.nx) if p.dim == 1 else r
+    d_o, _ = precond.apply_precond(p, r_o, jbar)
+    # bar: 1e-11, or 10x the instance's rounding floor where that is larger (1D)
+    bar = max(1e-11, 10 * _rounding_floor_1d(p, r_o, d_o)) if p.dim == 1 else 1e-11
+    assert rel_err(to_host(d, p), d_o) <= bar
     s.apply_precond(rd, rd, jbar)                  # in place
-    assert rel_err(to_host(rd, p), d_o) <= 1e-11
+    assert rel_err(to_host(rd, p), d_o) <= bar
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
