@@ -35,6 +35,7 @@ BYTES_PER_DOF = {  # algorithmic HBM bytes per space-time dof per launch (DESIGN
     # long windows (k_tlong.cuh): each pass reads and writes one U-sized array (pairs of real
     # pencils packed as one complex pencil: ⌈N_s/2⌉·16 B = N_s·8 B per time row)
     "tlong_a_fwd": 16.0, "tlong_b_fwd": 16.0, "tlong_divide": 16.0, "tlong_b_inv": 16.0, "tlong_a_inv": 16.0,
+    "tlong_b_fused": 16.0,        # pass B + divide + pass B⁻¹ (Y read and written once)
     # 1D short rows (k_x1d.cuh): residual fused with the forward x transform (read U, write r̂),
     # inverse x transform fused with the update (read δ̂, U; write U)
     "residual_dst_x": 16.0, "dst_x_inv_update": 24.0,

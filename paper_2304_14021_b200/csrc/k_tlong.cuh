@@ -193,11 +193,96 @@ k_tl_divide(double2* __restrict__ X, TlongParams Q) {
     const double2 d = __ldg(Q.T.dl + k);
     const double mua = mode_mu(sa, Q.T, jbar);
     const double mub = hb ? mode_mu(sb, Q.T, jbar) : mua;
-    const double2 fa = cinv(shifted(d, Q.T.el, (int)k, mua, Q.T.l3, Q.T.l3 ? mode_lam(sa, Q.T) : 0.0));
-    const double2 fb = cinv(shifted(d, Q.T.el, (int)k, mub, Q.T.l3, Q.T.l3 && hb ? mode_lam(sb, Q.T) : 0.0));
+    const double2 fa = cinv_fast(shifted(d, Q.T.el, (int)k, mua, Q.T.l3, Q.T.l3 ? mode_lam(sa, Q.T) : 0.0));
+    const double2 fb = cinv_fast(shifted(d, Q.T.el, (int)k, mub, Q.T.l3, Q.T.l3 && hb ? mode_lam(sb, Q.T) : 0.0));
     const double2 Af = cmul(A, fa), Bf = cmul(B, fb);
     X[k * Q.P + p] = make_double2(Af.x - Bf.y, Af.y + Bf.x);
     if (km != k) X[km * Q.P + p] = make_double2(Af.x + Bf.y, Bf.x - Af.y);
+  }
+}
+
+// Pass B forward + Step (2) + pass B inverse in one kernel, for N2 = 1024 (one k1 per transform
+// group): a CTA takes the k1 and N1−k1 groups (k1 = 0 pairs with N1/2, both self-mirrored) for
+// 4 pencil pairs, so every bin k = k1 + N1·k2 finds its mirror N−k = (N1−k1) + N1·(N2−1−k2) in
+// shared memory.  The forward FFT leaves bin k2 = lane + 32r in register r, which is exactly the
+// input layout of the inverse FFT, so the divided spectrum never leaves registers; Y is read and
+// written once (in place) instead of three round trips through X.
+constexpr int kFbPairs = 4;
+constexpr int kFbRowC = kFbPairs + 1;                 // staged row pitch (complex): 80 B
+constexpr size_t kFbSmem = (size_t)2 * 1024 * kFbRowC * sizeof(double2);   // 160 KB ≥ 8 × kWarpScratch
+
+__global__ void __launch_bounds__(256, 1)
+k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
+  constexpr int L = 1024;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nch4 = (Q.P + kFbPairs - 1) / kFbPairs;
+  const int64_t chunk = blockIdx.x % nch4;
+  const int j = (int)(blockIdx.x / nch4);               // 0: (0, N1/2); j ≥ 1: (j, N1 - j)
+  const int k1b = j == 0 ? Q.N1 / 2 : Q.N1 - j;        // the second group's k1
+  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += 256) {
+    const int w = idx & 3, row = idx >> 2;
+    const int n2 = row & (L - 1), grp = row >> 10;
+    const int64_t p = chunk * kFbPairs + w;
+    double2* d = sm + (grp * L + n2) * kFbRowC + w;
+    if (p < Q.P) cp_async16(d, Y + ((int64_t)(grp ? k1b : j) * L + n2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  const int grp = warp >> 2, pw = warp & 3;
+  const int k1 = grp ? k1b : j;
+  double2 v[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = sm[(grp * L + lane + 32 * e) * kFbRowC + pw];
+  __syncthreads();
+  fft4_s1_to_s2<32, -1>(v, sm + warp * kWarpScratch, Q.log2N2, Q.tw, Q.twlog, lane);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 32; ++r) sm[(grp * L + lane + 32 * r) * kFbRowC + pw] = v[r];
+  __syncthreads();
+  {
+    // mirror group and bin: k1 = 0 → (same, (N2 - k2) mod N2); k1 = N1/2 → (same, N2-1-k2);
+    // otherwise (other group, N2-1-k2)
+    const int mg = (j == 0) ? grp : 1 - grp;
+    const bool zero = (j == 0 && grp == 0);
+    const int64_t p = chunk * kFbPairs + pw;
+    const int64_t sa = 2 * p, sb = sa + 1;
+    const bool hb = sb < Q.ns;
+    const double jbar = Q.T.kind >= 2 ? Q.T.st->jbar : 0.0;
+    const double mua = mode_mu(sa, Q.T, jbar);
+    const double mub = hb ? mode_mu(sb, Q.T, jbar) : mua;
+    const double lama = Q.T.l3 ? mode_lam(sa, Q.T) : 0.0;
+    const double lamb = Q.T.l3 && hb ? mode_lam(sb, Q.T) : 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int k2 = lane + 32 * r;
+      const int k2m = zero ? ((L - k2) & (L - 1)) : (L - 1 - k2);
+      const int k = k1 + Q.N1 * k2;
+      const double2 Zl = v[r], Zm = sm[(mg * L + k2m) * kFbRowC + pw];
+      const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
+      const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
+      const double2 d = __ldg(Q.T.dl + k);
+      const double2 Af = cmul(A, cinv_fast(shifted(d, Q.T.el, k, mua, Q.T.l3, lama)));
+      const double2 Bf = cmul(B, cinv_fast(shifted(d, Q.T.el, k, mub, Q.T.l3, lamb)));
+      v[r] = make_double2(Af.x - Bf.y, Af.y + Bf.x);
+    }
+  }
+  __syncthreads();                                      // all mirrors read before the scratch reuse
+  fft4_s1_to_s2<32, +1>(v, sm + warp * kWarpScratch, Q.log2N2, Q.tw, Q.twlog, lane);
+  __syncthreads();
+  {
+    const TlTwiddle<32, +1> tw(Q, lane, k1);            // W_N^{-k1 n2}, n2 = lane + 32 r
+#pragma unroll
+    for (int r = 0; r < 32; ++r) sm[(grp * L + lane + 32 * r) * kFbRowC + pw] = tw.apply(v[r], r);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += 256) {
+    const int w = idx & 3, row = idx >> 2;
+    const int n2 = row & (L - 1), g = row >> 10;
+    const int64_t p = chunk * kFbPairs + w;
+    if (p < Q.P) Y[((int64_t)(g ? k1b : j) * L + n2) * Q.P + p] = sm[(g * L + n2) * kFbRowC + w];
   }
 }
 

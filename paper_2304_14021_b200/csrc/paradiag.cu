@@ -55,12 +55,13 @@ int fail(int code, const std::string& msg) {
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
                 K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI,
-                K_XRES, K_XUPD, PD_NKERNELS };
+                K_XRES, K_XUPD, K_TLBF, PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
                                          "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update",
                                          "residual_update", "tlong_a_fwd", "tlong_b_fwd", "tlong_divide",
-                                         "tlong_b_inv", "tlong_a_inv", "residual_dst_x", "dst_x_inv_update"};
+                                         "tlong_b_inv", "tlong_a_inv", "residual_dst_x", "dst_x_inv_update",
+                                         "tlong_b_fused"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per CTA (sm_100a)
@@ -137,6 +138,7 @@ struct pd_handle {
   // 1D long windows with N_x ≤ 64: x transforms as DMMA products with T (k_x1d.cuh), fused with
   // the residual (forward) and the update (inverse); x1T = Tᵀ zero padded to 64×64
   bool x1 = false;
+  bool tlfuse = true;                 // PARADIAG_TLFUSE=0: unfused pass B / divide / pass B⁻¹ (A/B, tests)
   double* x1T = nullptr;
   double* tlg = nullptr;              // k_tlong.cuh split Γ_α tables: ghi[N1] glo[N2] gihi[N1] gilo[N2]
   std::vector<void*> allocs;
@@ -431,6 +433,19 @@ int tlong_time(pd_handle* h, const double* in, double* out) {
   Q.T = time_params(h, nullptr);
   double2* Y = h->spec;
   double2* X = h->w1;
+  if (h->tlfuse && tlong_fusable(Q)) {                   // A, fused B (+ divide), A⁻¹
+    const int kid[3] = {K_TLA, K_TLBF, K_TLAI};
+    const int stg[3] = {0, 5, 4};
+    const void* ins[3] = {in, nullptr, Y};
+    void* outs[3] = {Y, Y, out};
+    for (int i = 0; i < 3; ++i) {
+      prof_begin(h, kid[i]);
+      if (!tlong_launch(stg[i], ins[i], outs[i], Q, h->stream)) return fail(PD_EINVAL, "tlong: unsupported N_t split");
+      prof_end(h, kid[i]);
+      PD_LAUNCHED();
+    }
+    return PD_OK;
+  }
   const int kid[5] = {K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI};
   const void* ins[5] = {in, Y, nullptr, X, Y};
   void* outs[5] = {Y, X, X, Y, out};
@@ -736,6 +751,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     h->tlong = p->nt > kMaxNtShort || (force && p->nt >= 1024 && (p->dim == 2 || (is_pow2(M) && M <= 4096)));
     tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
     h->x1 = h->tlong && p->dim == 1 && h->nx <= 2 * kX1H;
+    if (const char* f3 = std::getenv("PARADIAG_TLFUSE")) h->tlfuse = std::atoi(f3) != 0;
     if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
   }
   h->log2h = (p->dim == 2 || h->tlong) ? ilog2(M) - 1 : 0;
@@ -758,10 +774,17 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     gam[j] = std::exp(j * lna / nt);
     ginv[j] = std::exp(-j * lna / nt) * (spatial_scale / nt);
   }
-  for (int l = 0; l < nt; ++l) {
+  // bins l ≤ N_t/2 from the accurate small angle 2πl/N_t; the upper half as exact conjugates
+  // (d_{N-l} = conj d_l): evaluating sin near 2π would carry the argument's absolute rounding
+  // (≈ 4e-16) into the small Im d_l of the low bins (1e-12 relative at N_t = 2^15)
+  for (int l = 0; l <= nt / 2; ++l) {
     const double ang = 2.0 * M_PI * l / nt;
     dl[l] = make_double2((1.0 - z * std::cos(ang)) * h->inv_dt, (z * std::sin(ang)) * h->inv_dt);
     el[l] = make_double2(p->theta + (1.0 - p->theta) * z * std::cos(ang), -(1.0 - p->theta) * z * std::sin(ang));
+    if (l > 0 && l < nt - l) {
+      dl[nt - l] = make_double2(dl[l].x, -dl[l].y);
+      el[nt - l] = make_double2(el[l].x, -el[l].y);
+    }
   }
   for (int i = 0; i < h->nx; ++i) {
     const int pidx = h->neumann ? i : i + 1;
@@ -813,7 +836,10 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   PD_TRY(dalloc(h, &h->dl, nt));
   if (p->theta != 1.0) PD_TRY(dalloc(h, &h->el, nt));
   std::vector<double2> l3(nt);
-  for (int l = 0; l < nt; ++l) l3[l] = make_double2(z * std::cos(2.0 * M_PI * l / nt), -z * std::sin(2.0 * M_PI * l / nt));
+  for (int l = 0; l <= nt / 2; ++l) {
+    l3[l] = make_double2(z * std::cos(2.0 * M_PI * l / nt), -z * std::sin(2.0 * M_PI * l / nt));
+    if (l > 0 && l < nt - l) l3[nt - l] = make_double2(l3[l].x, -l3[l].y);
+  }
   if (p->kind == PD_CAHN_HILLIARD_EYRE) PD_TRY(dalloc(h, &h->l3, nt));
   PD_TRY(dalloc(h, &h->lam, h->nx));
   PD_TRY(dalloc(h, &h->tw, TWN));

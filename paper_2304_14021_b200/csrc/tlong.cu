@@ -40,19 +40,32 @@ void launch_e(int stage, const void* in, void* out, const TlongParams& Q, cudaSt
 }  // namespace
 
 void tlong_split(int log2N, int* log2N1, int* log2N2) {
-  *log2N1 = (log2N + 1) / 2;
-  *log2N2 = log2N - *log2N1;
+  // N2 = 1024 whenever N1 = N / 1024 ≥ 32 (the fused pass B needs N2 = 1024), else balanced
+  if (log2N >= 15) {
+    *log2N2 = 10;
+  } else {
+    *log2N2 = log2N / 2;
+  }
+  *log2N1 = log2N - *log2N2;
 }
+
+bool tlong_fusable(const TlongParams& Q) { return Q.N2 == 1024 && Q.N1 >= 32; }
 
 cudaError_t tlong_attrs() {
   cudaError_t e;
   if ((e = attrs_e<1>()) || (e = attrs_e<2>()) || (e = attrs_e<4>()) || (e = attrs_e<8>()) || (e = attrs_e<16>()) ||
       (e = attrs_e<32>()))
     return e;
-  return cudaSuccess;
+  return cudaFuncSetAttribute(k_tl_b_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
 }
 
 bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s) {
+  if (stage == 5) {                                     // fused B: Y in place (`out`)
+    if (!tlong_fusable(Q)) return false;
+    const int64_t nch4 = (Q.P + kFbPairs - 1) / kFbPairs;
+    k_tl_b_fused<<<(unsigned)(nch4 * (Q.N1 / 2)), 256, kFbSmem, s>>>(static_cast<double2*>(out), Q);
+    return true;
+  }
   if (stage == 2) {
     const int64_t total = (int64_t)(Q.N / 2 + 1) * Q.P;
     const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);

@@ -6,11 +6,14 @@
 
 namespace pd {
 
-// N = 2^log2N split as N1 = 2^⌈log2N/2⌉ (pass A) × N2 (pass B)
+// N = 2^log2N split as N1 (pass A) × N2 (pass B): N2 = 1024 from N = 2^15 on, else balanced
 void tlong_split(int log2N, int* log2N1, int* log2N2);
 cudaError_t tlong_attrs();
+// pass B forward + divide + pass B inverse fused (stage 5) applies: N2 = 1024
+bool tlong_fusable(const TlongParams& Q);
 // stage 0: pass A forward (real in → Y), 1: pass B forward (Y → X), 2: divide (X in place, `out`),
-// 3: pass B inverse (X → Y), 4: pass A inverse (Y → real out).  false: unsupported factor length.
+// 3: pass B inverse (X → Y), 4: pass A inverse (Y → real out), 5: fused pass B with the divide
+// (Y in place, `out`).  false: unsupported factor length.
 bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s);
 
 }  // namespace pd

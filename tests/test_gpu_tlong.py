@@ -100,6 +100,25 @@ def test_tlong_solve_parity(solver_for, name):
     assert info.converged == int(all(conv_o)) and rc == (0 if all(conv_o) else 1)
 
 
+@pytest.mark.parametrize("nt", [1 << 15, 1 << 17])
+def test_tlong_fused_pass_b_matches_unfused(cuda_lib, monkeypatch, nt):
+    """N2 = 1024 splits (N_t ≥ 2^15) run pass B, the divide and pass B⁻¹ as one kernel; it must
+    reproduce the three-kernel sequence (each separately pinned to the oracle above) to rounding
+    (the same operations up to FMA contraction; both sit ~1e-11 from an FFT evaluation here, the
+    Γ_α⁻¹ = 1/α amplification of this window's rounding floor)."""
+    p = _c6(nt)
+    r = np.random.default_rng(23).uniform(-1, 1, gshape(p))
+    out = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("PARADIAG_TLFUSE", fuse)
+        s = cuda_lib.Solver(p)
+        d = s.empty()
+        s.apply_precond(to_dev(r, p), d, 0.0)
+        out.append(to_host(d, p))
+        s.close()
+    assert rel_err(out[0], out[1]) <= 1e-12
+
+
 def _closed_form_field(p, g, c):
     """Iterate on the whole space-time grid from its mode coefficients: u_n = T (g^{n+1} c) / 2m."""
     T = spatial.transform_matrix(p.m, p.bc)
