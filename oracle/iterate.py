@@ -8,6 +8,7 @@ because b^{k-1} = b + (P_α - K) U^{k-1}.
 Cahn-Hilliard PinT-I with one quasi-Newton step per WR step (R#6):
     U^k = U^{k-1} + ω_k P̃⁻¹ (-G(U^{k-1})),  -G(U)_n = -(U_n - U_{n-1})/Δt + Δ_h(U_n³ - U_n - ε²Δ_h U_n)
 (P:460-463 with the α-terms cancelled as above), P̃ with the scalar J̄ = mean(3U² - 1) (R#7, R#8),
+or (jacobian = "time_avg", NEXT-4) with the paper's time-only average J̃ = diag(mean_n 3U_n²),
 ω_k = min(omega, tau/‖δ_k‖∞) (R#9; linear problems ω = 1).
 
 Stopping (R#4): ‖δ^k‖∞ ≤ tol·‖U^k‖∞ with the undamped δ; c5 runs a fixed K (R#16).
@@ -76,10 +77,16 @@ def initial_iterate(prob, u0: np.ndarray) -> np.ndarray:
     return np.broadcast_to(u0.reshape(shape[1:]), shape).copy()
 
 
+def time_avg_jacobian(U: np.ndarray) -> np.ndarray:
+    """jt = (1/N_t) Σ_n 3 u_n² per grid point: the diagonal of J̃ = (1/N_t) Σ_n J_s(u_n) (R#7)."""
+    return 3.0 * np.mean(U * U, axis=0)
+
+
 def iterate_once(prob, u0, U):
     """One ParaDiag iteration.  Returns (U_new, info dict)."""
     r, jbar = residual(prob, u0, U)
-    delta, imag = precond.apply_precond(prob, r, jbar)
+    jt = time_avg_jacobian(U) if is_ch(prob) and getattr(prob, "jacobian", "scalar") == "time_avg" else None
+    delta, imag = precond.apply_precond(prob, r, jbar, jt)
     dmax = float(np.abs(delta).max())
     if is_ch(prob):
         omega = min(prob.omega, prob.tau / dmax) if dmax > 0 else prob.omega

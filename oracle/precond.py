@@ -108,12 +108,47 @@ def step2_2d(prob, S1: np.ndarray, jbar: float = 0.0) -> np.ndarray:
     return (T @ hat @ T.T) / (2.0 * prob.m) ** 2
 
 
-def apply_precond(prob, r: np.ndarray, jbar: float = 0.0):
-    """δ = P_α⁻¹ r, r shaped [N_t, N_x] (1D) or [N_t, N_y, N_x] (2D).
+def step2_2d_timeavg(prob, S1: np.ndarray, jt: np.ndarray) -> np.ndarray:
+    """Step-(2) with the paper's time-only averaged Jacobian (NEXT-4):
+    J̃ = (1/N_t) Σ_n J_s(u_n) = diag(jt), jt = mean_n 3u_n² (R#7), spatially varying, so Step-(2)
+    is not DCT-diagonalisable.  Per bin l the sparse system of P:495 (PinT-I)
+        (λ_{1,l} I - Δ_h diag(jt) + Δ_h + ε²Δ_h²) x = S1_l
+    or of P:545 (PinT-II, Eyre)
+        (λ_{1,l} I - Δ_h diag(jt) + λ_{3,l} Δ_h + ε²Δ_h²) x = S1_l
+    is assembled from the paper's Δ_h (Kronecker form P:284) and solved directly
+    (scipy.sparse.linalg.spsolve, a library LU).  jt shaped [N_y, N_x]."""
+    import scipy.sparse as sp
+    from scipy.sparse.linalg import spsolve
+    nt = S1.shape[0]
+    d = circulant.eig_d(nt, prob.alpha, circulant.inv_dt(prob))
+    _, e2 = spatial.coeffs(prob)
+    D = sp.csr_matrix(spatial.lap_matrix_1d(prob.m, prob.bc))
+    I1 = sp.identity(D.shape[0], format="csr")
+    L = (sp.kron(D, I1) + sp.kron(I1, D)).tocsr()               # row-major [y, x]: Δ_y⊗I + I⊗Δ_x
+    ns = L.shape[0]
+    LJ = L @ sp.diags(jt.reshape(-1))
+    base = -LJ + e2 * (L @ L)
+    if prob.kind == "cahn_hilliard_eyre":
+        c = circulant.eig_e(nt, prob.alpha, 0.0)                # λ_{3,l} = z ω^l (P:545)
+    else:
+        c = np.ones(nt)                                          # + Δ_h (P:495)
+    I = sp.identity(ns, format="csr")
+    out = np.empty(S1.shape, dtype=np.complex128)
+    for l in range(nt):
+        M = (d[l] * I + c[l] * L + base).tocsc()
+        out[l] = spsolve(M, S1[l].reshape(-1).astype(np.complex128)).reshape(S1.shape[1:])
+    return out
+
+
+def apply_precond(prob, r: np.ndarray, jbar: float = 0.0, jt: np.ndarray = None):
+    """δ = P_α⁻¹ r, r shaped [N_t, N_x] (1D) or [N_t, N_y, N_x] (2D).  With jt (CH, 2D): the
+    time-averaged Jacobian J̃ = diag(jt) of P:486 in Step-(2) (NEXT-4) instead of the scalar J̄.
 
     Returns (δ, max|Im|/max|Re| after Step-(3)) — the imaginary residue of S:336.
     """
     S1 = circulant.step1(r, prob.alpha)
+    if jt is not None:
+        return circulant.step3(step2_2d_timeavg(prob, S1, jt), prob.alpha)
     if prob.dim == 1 and prob.kind == "cahn_hilliard_eyre":
         raise NotImplementedError("PinT-II is exercised in 2D (the library's CH path is 2D Neumann)")
     if prob.dim == 1:

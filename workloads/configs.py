@@ -31,6 +31,7 @@ class Problem:
     u0_kind: str = "uniform"
     u0_range: Tuple[float, float] = (0.0, 0.0)
     seed: int = 0
+    jacobian: str = "scalar"         # CH: "scalar" J̄ (R#8) | "time_avg" J̃ = diag(mean_n 3u_n²) (NEXT-4)
 
     @property
     def n(self) -> int:
@@ -83,6 +84,12 @@ CONFIGS = {
     # random start is read as noise on top of the c1 sine.
     "c6": Problem("c6", "biharmonic", "hinged", 1, m=64, nt=1 << 20, t_window=1.0, alpha=1e-3,
                   u0_kind="sine_plus_noise", u0_range=(-0.01, 0.01), seed=6),
+    # NEXT-4: c4's PinT-I with the paper's time-only averaged Jacobian
+    # J̃ = I_t ⊗ (1/N_t) Σ_n J_s(u_n) — spatially varying, Step-(2) solved by an inner Krylov
+    # iteration preconditioned by the scalar-J̄ spectral solve
+    "c4t": Problem("c4t", "cahn_hilliard", "neumann", 2, m=256, nt=64, t_window=64e-4, alpha=1e-3,
+                   eps=0.02, n_windows=4, max_iter=400, omega=0.7, tau=1.0,
+                   u0_range=(-0.1, 0.1), seed=4, jacobian="time_avg"),
 }
 
 
