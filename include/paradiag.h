@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PARADIAG_ABI_VERSION 2
+#define PARADIAG_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define PD_API __attribute__((visibility("default")))
@@ -74,16 +74,18 @@ extern "C" {
 /* initial iterate U⁰ (R#5) */
 #define PD_INIT_BROADCAST  0   /* U⁰_n = u0 for every n */
 #define PD_INIT_ZERO       1   /* U⁰ = 0                */
+#define PD_JACOBIAN_SCALAR   0 /* CH Step-(2): scalar J̄ (R#8), one spectral solve          */
+#define PD_JACOBIAN_TIME_AVG 1 /* CH Step-(2): J̃ = diag(mean_n 3U_n²), inner GMRES */
 
 typedef struct pd_problem {
   int32_t kind;          /* PD_BIHARMONIC | PD_LINEAR_CH | PD_CAHN_HILLIARD | PD_CAHN_HILLIARD_EYRE */
   int32_t bc;            /* PD_BC_NEUMANN | PD_BC_HINGED (CH: Neumann only)                */
   int32_t dim;           /* 1 or 2 (CH: 2 only)                                                  */
-  int32_t nt;            /* time steps per window, power of two in [2, 4096]                     */
+  int32_t nt;            /* time steps per window, power of two in [2, 2^20] (> 4096: k_tlong.cuh) */
   int64_t m;             /* intervals per axis, h = 1/m; 2D: power of two in [4, 4096]; 1D ≥ 4   */
   double  t_window;      /* window length T; Δt = T / nt, 1/Δt evaluated as nt / T (R#20)        */
   double  alpha;         /* PinT parameter α ∈ (0, 1)                              */
-  double  theta;         /* θ-method parameter; 1.0 (backward Euler) only                        */
+  double  theta;         /* θ-method parameter in [1/2, 1]; CH: 1 (backward Euler)   */
   double  beta;          /* LINEAR_CH β; β² := fl(β·β)                                     */
   double  eps;           /* LINEAR_CH / CH ε ≥ 0; ε² := fl(ε·ε)                                   */
   double  tol;           /* stop when ‖δ‖∞ ≤ tol·‖U‖∞ (R#4)                                       */
@@ -93,6 +95,10 @@ typedef struct pd_problem {
   int32_t max_iter;      /* iteration cap per window                                              */
   int32_t fixed_iters;   /* > 0: run exactly this many iterations per window, no stop test (c5)  */
   int32_t init;          /* PD_INIT_BROADCAST | PD_INIT_ZERO                                      */
+  int32_t jacobian;      /* CH Step-(2) Jacobian: PD_JACOBIAN_SCALAR (J̄ = mean(3U²-1), R#8) or
+                            PD_JACOBIAN_TIME_AVG (J̃ = diag(mean_n 3U_n²), NEXT-4: inner
+                            GMRES preconditioned by the scalar solve); linear kinds: 0          */
+  int32_t reserved;      /* 0                                                                     */
 } pd_problem;
 
 typedef struct pd_handle pd_handle;
@@ -145,6 +151,15 @@ PD_API int paradiag_residual(pd_handle* h, const double* u0, const double* U, do
 /* δ = P_α⁻¹ r — Steps (1)-(3), P:158-169 / P:491-499.  `jbar` is the scalar Jacobian average used
  * by CH (ignored otherwise).  r and delta may alias (in-place).  Asynchronous. */
 PD_API int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double jbar);
+
+/* δ = G̃'⁻¹ r with the time-only averaged Jacobian J̃ = diag(jt) of P:486 (NEXT-4; CH kinds, 2D,
+ * jacobian = PD_JACOBIAN_TIME_AVG): jt [ny][nx] (device) is the per-point time mean of 3U², so
+ * Step-(2) of P:495 (PinT-I) / P:545 (PinT-II) is (λ_{1,l} I - Δ_h diag(jt) + {1, λ_{3,l}} Δ_h +
+ * ε²Δ_h²) per bin.  Solved in the time domain as G̃' δ = r by restarted GMRES, left-preconditioned
+ * by the scalar-J̄ P_α⁻¹ with J̄ = mean(jt) - {1, 0}, to a relative preconditioned residual of
+ * 1e-13.  r and delta may alias.  Synchronises (one host read per Krylov step).
+ * PD_NOT_CONVERGED if the inner solve hit its iteration cap. */
+PD_API int paradiag_apply_precond_jt(pd_handle* h, const double* r, double* delta, const double* jt);
 
 /* One ParaDiag iteration on window data: r = b - K(U) (or -G(U)), δ = P_α⁻¹ r, U ← U + ω δ, with
  * ω = 1 (linear) or min(omega, tau/‖δ‖∞) (CH, R#9).  Fills *info (synchronises on 4 scalars).

@@ -18,6 +18,7 @@ PD_EINVAL, PD_ESINGULAR, PD_ECUDA, PD_ENCCL, PD_ENOMEM, PD_EDIVERGED = -1, -2, -
 KINDS = {"biharmonic": 0, "linear_ch": 1, "cahn_hilliard": 2, "cahn_hilliard_eyre": 3}
 BCS = {"neumann": 0, "hinged": 1}
 INITS = {"broadcast": 0, "zero": 1}
+JACOBIANS = {"scalar": 0, "time_avg": 1}
 MAX_WINDOWS = 64
 
 
@@ -33,7 +34,8 @@ class pd_problem(ctypes.Structure):
                 ("alpha", ctypes.c_double), ("theta", ctypes.c_double), ("beta", ctypes.c_double),
                 ("eps", ctypes.c_double), ("tol", ctypes.c_double), ("omega", ctypes.c_double),
                 ("tau", ctypes.c_double), ("n_windows", ctypes.c_int32), ("max_iter", ctypes.c_int32),
-                ("fixed_iters", ctypes.c_int32), ("init", ctypes.c_int32)]
+                ("fixed_iters", ctypes.c_int32), ("init", ctypes.c_int32), ("jacobian", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class pd_iter_info(ctypes.Structure):
@@ -54,12 +56,12 @@ class pd_kernel_time(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", "paradiag_strerror", "paradiag_last_error", "paradiag_workspace_bytes",
-           "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_iterate",
+           "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_apply_precond_jt", "paradiag_iterate",
            "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy",
            "paradiag_init_slab", "paradiag_slab_geometry", "paradiag_slab_residual", "paradiag_slab_xpass",
            "paradiag_slab_ypass", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read"]
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 def load(path: str = LIB_PATH):
@@ -79,6 +81,7 @@ def load(path: str = LIB_PATH):
     lib.paradiag_init.argtypes = [P(pd_problem), ctypes.c_int, vp, P(vp)]
     lib.paradiag_residual.argtypes = [vp, vp, vp, vp, P(ctypes.c_double)]
     lib.paradiag_apply_precond.argtypes = [vp, vp, vp, ctypes.c_double]
+    lib.paradiag_apply_precond_jt.argtypes = [vp, vp, vp, vp]
     lib.paradiag_iterate.argtypes = [vp, vp, vp, P(pd_iter_info)]
     lib.paradiag_solve.argtypes = [vp, vp, vp, P(pd_solve_info)]
     lib.paradiag_solve_host.argtypes = [vp, vp, vp, P(pd_solve_info)]
@@ -125,7 +128,7 @@ def make_problem(obj=None, **kw) -> pd_problem:
     f = {}
     if obj is not None:
         for k in ("kind", "bc", "dim", "nt", "m", "t_window", "alpha", "theta", "beta", "eps", "tol",
-                  "omega", "tau", "n_windows", "max_iter", "fixed_iters", "init"):
+                  "omega", "tau", "n_windows", "max_iter", "fixed_iters", "init", "jacobian"):
             if hasattr(obj, k):
                 f[k] = getattr(obj, k)
     f.update(kw)
@@ -150,6 +153,9 @@ def make_problem(obj=None, **kw) -> pd_problem:
     p.fixed_iters = int(fi) if fi else 0
     init = f.get("init", "broadcast")
     p.init = INITS[init] if isinstance(init, str) else int(init)
+    jac = f.get("jacobian", "scalar")
+    p.jacobian = JACOBIANS[jac] if isinstance(jac, str) else int(jac)
+    p.reserved = 0
     return p
 
 
@@ -187,6 +193,13 @@ def paradiag_residual(h, u0, U, r, want_jbar=False):
 def paradiag_apply_precond(h, r, delta, jbar: float = 0.0):
     _check(load().paradiag_apply_precond(h, _ptr(r, "r"), _ptr(delta, "delta"), float(jbar)),
            "paradiag_apply_precond")
+
+
+def paradiag_apply_precond_jt(h, r, delta, jt):
+    """δ = G̃'⁻¹ r with the time-averaged Jacobian diag(jt) (NEXT-4); returns the status (1: the
+    inner GMRES hit its cap)."""
+    return _check(load().paradiag_apply_precond_jt(h, _ptr(r, "r"), _ptr(delta, "delta"), _ptr(jt, "jt")),
+                  "paradiag_apply_precond_jt")
 
 
 def paradiag_iterate(h, u0, U, info: pd_iter_info = None) -> pd_iter_info:
@@ -306,6 +319,9 @@ class Solver:
 
     def apply_precond(self, r, delta, jbar=0.0):
         paradiag_apply_precond(self.h, r, delta, jbar)
+
+    def apply_precond_jt(self, r, delta, jt):
+        return paradiag_apply_precond_jt(self.h, r, delta, jt)
 
     def iterate(self, u0, U, info=None):
         return paradiag_iterate(self.h, u0, U, info)

@@ -26,6 +26,7 @@
 #include "fast_launch.cuh"
 #include "tlong.h"
 #include "k_x1d.cuh"
+#include "k_krylov.cuh"
 
 using namespace pd;
 
@@ -55,13 +56,13 @@ int fail(int code, const std::string& msg) {
 
 enum KernelId { K_RESET = 0, K_RESIDUAL, K_JBAR, K_XFWD, K_YFWD, K_TIME, K_YINV, K_XINV, K_UPDATE,
                 K_TFWD1D, K_PENTA, K_TINV1D, K_XINVUPD, K_RESUPD, K_TLA, K_TLB, K_TLD, K_TLBI, K_TLAI,
-                K_XRES, K_XUPD, K_TLBF, PD_NKERNELS };
+                K_XRES, K_XUPD, K_TLBF, K_KLAP, K_KVEC, PD_NKERNELS };
 const char* kKernelNames[PD_NKERNELS] = {"reset_stats", "residual", "jbar_finalize", "dtt_x_fwd", "dtt_y_fwd",
                                          "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "update",
                                          "time_fwd_1d", "penta_solve", "time_inv_1d", "dtt_x_inv_update",
                                          "residual_update", "tlong_a_fwd", "tlong_b_fwd", "tlong_divide",
                                          "tlong_b_inv", "tlong_a_inv", "residual_dst_x", "dst_x_inv_update",
-                                         "tlong_b_fused"};
+                                         "tlong_b_fused", "krylov_lap_w", "krylov_vector_ops"};
 
 constexpr int kTimeWarps = 8;   // 2D time pass: 16 spatial points (128-byte rows) per CTA
 constexpr size_t kSmemMax = 227 * 1024;   // opt-in dynamic shared memory per CTA (sm_100a)
@@ -141,6 +142,16 @@ struct pd_handle {
   bool tlfuse = true;                 // PARADIAG_TLFUSE=0: unfused pass B / divide / pass B⁻¹ (A/B, tests)
   double* x1T = nullptr;
   double* tlg = nullptr;              // k_tlong.cuh split Γ_α tables: ghi[N1] glo[N2] gihi[N1] gilo[N2]
+  // NEXT-4 (jacobian = PD_JACOBIAN_TIME_AVG, k_krylov.cuh): jt = mean_n 3U², w' = jt - c - J̄,
+  // GMRES(kKryM) basis V [kKryM+1][total], preconditioned right-hand side kb, dot partials
+  double* jt = nullptr;
+  double* wfld = nullptr;
+  double* kV = nullptr;
+  double* kb = nullptr;
+  double* kpart = nullptr;
+  double* kdev = nullptr;             // device copy of dot results / combination coefficients
+  double* khost = nullptr;            // pinned
+  int kry_last = 0;                   // Krylov steps of the last inner solve
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -216,6 +227,10 @@ int validate(const pd_problem* p) {
   if (p->fixed_iters <= 0 && !(p->tol > 0.0)) return fail(PD_EINVAL, "tol must be > 0");
   if (p->n_windows < 1 || p->n_windows > PD_MAX_WINDOWS) return fail(PD_EINVAL, "n_windows out of range");
   if (p->fixed_iters <= 0 && p->max_iter < 1) return fail(PD_EINVAL, "max_iter must be >= 1");
+  if (p->jacobian != PD_JACOBIAN_SCALAR && p->jacobian != PD_JACOBIAN_TIME_AVG)
+    return fail(PD_EINVAL, "unknown jacobian");
+  if (p->jacobian == PD_JACOBIAN_TIME_AVG && !is_ch(p->kind))
+    return fail(PD_EINVAL, "the time-averaged Jacobian (P:486) is a Cahn-Hilliard option");
   if (is_ch(p->kind) && !(p->omega > 0.0 && p->tau > 0.0))
     return fail(PD_EINVAL, "CH damping needs omega > 0 and tau > 0");
   if (p->init != PD_INIT_BROADCAST && p->init != PD_INIT_ZERO) return fail(PD_EINVAL, "unknown init");
@@ -543,6 +558,142 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   return PD_OK;
 }
 
+// ---- NEXT-4: Step-(2) with the time-averaged Jacobian (k_krylov.cuh) -------------------------
+constexpr int kKryM = 30;            // GMRES restart length
+constexpr int kKryCycles = 20;       // restarts before PD_NOT_CONVERGED
+constexpr double kKryTol = 1e-13;    // relative preconditioned residual
+
+unsigned kgrid(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+
+// dots of V_0..V_{nv-1} (stride total) with y → h->khost[0..nv) (synchronises; folds profiled events)
+int kdots(pd_handle* h, const double* V, int nv, const double* y) {
+  prof_begin(h, K_KVEC);
+  k_mdot<<<kKryBlocks, kKryThreads, 0, h->stream>>>(V, h->total, nv, y, h->total, h->kpart);
+  k_mdot_final<<<nv, 256, 0, h->stream>>>(h->kpart, kKryBlocks, h->kdev);
+  prof_end(h, K_KVEC);
+  PD_LAUNCHED();
+  PD_CUDA(cudaMemcpyAsync(h->khost, h->kdev, nv * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  return PD_OK;
+}
+
+// y += s · Σ_{i<nv} c_i V_i with c = h->khost[0..nv) (uploaded)
+int kcombine(pd_handle* h, double* y, const double* V, int nv, double s) {
+  PD_CUDA(cudaMemcpyAsync(h->kdev, h->khost, nv * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  prof_begin(h, K_KVEC);
+  k_maxpy<<<kgrid(h->total), 256, 0, h->stream>>>(y, V, h->total, nv, h->kdev, s, h->total);
+  prof_end(h, K_KVEC);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int kaxpby(pd_handle* h, double* y, const double* x, double a, double b) {
+  k_axpby<<<kgrid(h->total), 256, 0, h->stream>>>(y, x, a, b, h->total);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+// w' = jt - c - J̄ and J̄ = mean(jt) - c into the device stats (c = 1 PinT-I, 0 PinT-II)
+int setup_wprime(pd_handle* h, const double* jt) {
+  const double c = h->P.kind == PD_CAHN_HILLIARD ? 1.0 : 0.0;
+  k_block_sum<<<kKryBlocks, kKryThreads, 0, h->stream>>>(jt, h->ns, h->kpart);
+  k_wprime<<<kgrid(h->ns), 256, 0, h->stream>>>(jt, h->kpart, kKryBlocks, h->ns, c, h->wfld, h->st);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+// out = K x = P(J̄)⁻¹ Δ_h(w' ⊙ x)   (out may not alias x)
+int apply_K(pd_handle* h, const double* x, double* out) {
+  prof_begin(h, K_KLAP);
+  k_lap_w<<<kgrid(h->total), 256, 0, h->stream>>>(x, h->wfld, out, h->nx, h->ny, h->P.nt, h->inv_h2);
+  prof_end(h, K_KLAP);
+  PD_LAUNCHED();
+  return precond(h, out, out);
+}
+
+// δ = G̃'⁻¹ r: GMRES(kKryM) on (I - K) δ = P⁻¹ r, started from δ₀ = P⁻¹ r (the scalar-J̄ solution),
+// classical Gram-Schmidt applied twice, Givens rotations on the host.  r and delta may alias.
+int precond_jt(pd_handle* h, const double* r, double* delta) {
+  const int64_t n = h->total;
+  double* V = h->kV;
+  double* b = h->kb;
+  int rc;
+  if ((rc = precond(h, r, delta))) return rc;                         // δ₀ = b' = P⁻¹ r
+  PD_CUDA(cudaMemcpyAsync(b, delta, n * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  if ((rc = kdots(h, b, 1, b))) return rc;
+  const double bn = std::sqrt(h->khost[0]);
+  std::vector<double> H((size_t)(kKryM + 1) * kKryM, 0.0), cs(kKryM), sn(kKryM), g(kKryM + 1), y(kKryM);
+  auto Hij = [&](int i, int j) -> double& { return H[(size_t)i * kKryM + j]; };
+  bool conv = bn == 0.0;
+  int steps = 0;
+  // each cycle starts from the TRUE preconditioned residual, so convergence is only declared on it
+  for (int cyc = 0; cyc <= kKryCycles && !conv; ++cyc) {
+    // b' - (δ - Kδ) into V_0
+    if ((rc = apply_K(h, delta, V))) return rc;                       // V_0 = Kδ
+    if ((rc = kaxpby(h, V, delta, -1.0, 1.0))) return rc;             // Kδ - δ
+    if ((rc = kaxpby(h, V, b, 1.0, 1.0))) return rc;                  // + b'
+    if ((rc = kdots(h, V, 1, V))) return rc;
+    const double beta = std::sqrt(h->khost[0]);
+    if (!std::isfinite(beta)) return fail(PD_EDIVERGED, "inner GMRES: non-finite residual");
+    if (beta <= kKryTol * bn) {
+      conv = true;
+      break;
+    }
+    if (cyc == kKryCycles) break;
+    if ((rc = kaxpby(h, V, V, 1.0 / beta - 1.0, 1.0))) return rc;    // V_0 /= β
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < kKryM; ++j) {
+      double* vj = V + (size_t)j * n;
+      double* vn = V + (size_t)(j + 1) * n;
+      if ((rc = apply_K(h, vj, vn))) return rc;                       // K v_j
+      if ((rc = kaxpby(h, vn, vj, 1.0, -1.0))) return rc;             // A v_j = v_j - K v_j
+      for (int pass = 0; pass < 2; ++pass) {                          // classical Gram-Schmidt, twice
+        if ((rc = kdots(h, V, j + 1, vn))) return rc;
+        for (int i = 0; i <= j; ++i) Hij(i, j) += h->khost[i];
+        if ((rc = kcombine(h, vn, V, j + 1, -1.0))) return rc;
+      }
+      if ((rc = kdots(h, vn, 1, vn))) return rc;
+      const double hn = std::sqrt(h->khost[0]);
+      Hij(j + 1, j) = hn;
+      if (hn > 0.0 && (rc = kaxpby(h, vn, vn, 1.0 / hn - 1.0, 1.0))) return rc;
+      for (int i = 0; i < j; ++i) {                                   // previous rotations
+        const double a = Hij(i, j), c2 = Hij(i + 1, j);
+        Hij(i, j) = cs[i] * a + sn[i] * c2;
+        Hij(i + 1, j) = -sn[i] * a + cs[i] * c2;
+      }
+      const double a = Hij(j, j), c2 = Hij(j + 1, j), rr = std::hypot(a, c2);
+      cs[j] = rr > 0.0 ? a / rr : 1.0;
+      sn[j] = rr > 0.0 ? c2 / rr : 0.0;
+      Hij(j, j) = rr;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++steps;
+      if (std::fabs(g[j + 1]) <= kKryTol * bn || hn == 0.0) {
+        ++j;
+        break;
+      }
+    }
+    if (j > kKryM) j = kKryM;
+    for (int i = j - 1; i >= 0; --i) {                                // back substitution
+      double t = g[i];
+      for (int k = i + 1; k < j; ++k) t -= Hij(i, k) * y[k];
+      y[i] = t / Hij(i, i);
+    }
+    for (int i = 0; i < j; ++i) h->khost[i] = y[i];
+    if ((rc = kcombine(h, delta, V, j, 1.0))) return rc;
+    std::fill(H.begin(), H.end(), 0.0);
+  }
+  h->kry_last = steps;
+  k_reset_dmax<<<1, 1, 0, h->stream>>>(h->st);
+  k_amax_stats<<<kgrid(n), 256, 0, h->stream>>>(delta, n, h->st);
+  PD_LAUNCHED();
+  return conv ? PD_OK : PD_NOT_CONVERGED;
+}
+
 int launch_update(pd_handle* h, double* U, const double* delta) {
   const int damped = is_ch(h->P.kind);
   prof_begin(h, K_UPDATE);
@@ -563,7 +714,14 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   int rc;
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
-  if (h->x1) {           // residual + x transform, time pass, x inverse + update: 7 passes
+  if (h->P.jacobian == PD_JACOBIAN_TIME_AVG) {   // NEXT-4: J̃ = diag(mean_n 3U²), inner GMRES
+    if ((rc = launch_residual(h, u0, U, h->work))) return rc;
+    k_tavg_jt<<<kgrid(h->ns), 256, 0, h->stream>>>(U, h->jt, h->ns, h->P.nt);
+    PD_LAUNCHED();
+    if ((rc = setup_wprime(h, h->jt))) return rc;
+    if ((rc = precond_jt(h, h->work, h->work)) < 0) return rc;  // PD_NOT_CONVERGED: inexact step, continue
+    if ((rc = launch_update(h, U, h->work))) return rc;
+  } else if (h->x1) {    // residual + x transform, time pass, x inverse + update: 7 passes
     if ((rc = launch_x1d(h, 0, u0, U, h->work, K_XRES))) return rc;
     if ((rc = tlong_time(h, h->work, h->work))) return rc;
     if ((rc = launch_x1d(h, 3, nullptr, h->work, U, K_XUPD))) return rc;
@@ -705,6 +863,7 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
+  if (p->jacobian == PD_JACOBIAN_TIME_AVG) b += (size_t)(kKryM + 2) * total * sizeof(double) + 2 * ns * sizeof(double);
   *bytes = b;
   return PD_OK;
 }
@@ -856,6 +1015,17 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
                          (size_t)((h->nx + kResTX - 1) / kResTX) * ((h->ny + kResTY - 1) / kResTY) *
                              ((nt + kResChunk - 1) / kResChunk));
     PD_TRY(dalloc(h, &h->jpart, h->njpart));
+  }
+  if (p->jacobian == PD_JACOBIAN_TIME_AVG) {
+    if (p->dim != 2 || slab) return cleanup(fail(PD_EINVAL, "time-averaged Jacobian: 2D, single handle"));
+    PD_TRY(dalloc(h, &h->jt, (size_t)h->ns));
+    PD_TRY(dalloc(h, &h->wfld, (size_t)h->ns));
+    PD_TRY(dalloc(h, &h->kV, (size_t)(kKryM + 1) * (size_t)h->total));
+    PD_TRY(dalloc(h, &h->kb, (size_t)h->total));
+    PD_TRY(dalloc(h, &h->kpart, (size_t)kKryBlocks * (kKryM + 1)));
+    PD_TRY(dalloc(h, &h->kdev, (size_t)kKryM + 2));
+    if (cudaMallocHost(&h->khost, (kKryM + 1) * sizeof(double)) != cudaSuccess)
+      return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
@@ -1018,6 +1188,18 @@ int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double 
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
   return precond(h, r, delta);
+}
+
+int paradiag_apply_precond_jt(pd_handle* h, const double* r, double* delta, const double* jt) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!r || !delta || !jt) return fail(PD_EINVAL, "NULL buffer");
+  if (h->P.jacobian != PD_JACOBIAN_TIME_AVG || !h->kV)
+    return fail(PD_EINVAL, "handle was not initialised with jacobian = PD_JACOBIAN_TIME_AVG");
+  k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+  PD_LAUNCHED();
+  if ((rc = setup_wprime(h, jt))) return rc;
+  return precond_jt(h, r, delta);
 }
 
 int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
@@ -1322,6 +1504,7 @@ void paradiag_destroy(pd_handle* h) {
       if (h->ev[i][j]) cudaEventDestroy(h->ev[i][j]);
   for (void* q : h->allocs) cudaFree(q);
   if (h->st_host) cudaFreeHost(h->st_host);
+  if (h->khost) cudaFreeHost(h->khost);
   delete h;
 }
 

@@ -28,14 +28,14 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.paradiag_abi_version() == pd.ABI_VERSION == 2
+    assert lib.paradiag_abi_version() == pd.ABI_VERSION == 3
     assert pd.strerror(pd.PD_EINVAL).startswith("PD_EINVAL")
     assert pd.strerror(pd.PD_ESINGULAR).startswith("PD_ESINGULAR")
 
 
 def test_struct_layout_matches_header():
-    # pd_problem: 4 int32, int64, 8 doubles, 4 int32 -> 104 bytes with natural alignment
-    assert ctypes.sizeof(pd.pd_problem) == 104
+    # pd_problem: 4 int32, int64, 8 doubles, 6 int32 -> 112 bytes with natural alignment
+    assert ctypes.sizeof(pd.pd_problem) == 112
     assert ctypes.sizeof(pd.pd_iter_info) == 48
     assert ctypes.sizeof(pd.pd_solve_info) == 8 + 64 * 4 + 64 * 8 + 8
 
@@ -60,6 +60,16 @@ def test_invalid_problems_rejected(lib, bad):
 def test_max_nt_accepted(lib):
     """N_t = 4096 is the documented maximum (include/paradiag.h); the GPU parity suite runs it."""
     assert pd.paradiag_workspace_bytes(pd.make_problem(config("c2"), nt=4096)) > 0
+
+
+def test_time_avg_jacobian_is_a_ch_option(lib):
+    """NEXT-4: the time-averaged Jacobian applies to the CH kinds only."""
+    assert pd.paradiag_workspace_bytes(pd.make_problem(config("c4t"))) > \
+        pd.paradiag_workspace_bytes(pd.make_problem(config("c4")))
+    with pytest.raises(pd.ParadiagError):
+        pd.paradiag_workspace_bytes(pd.make_problem(config("c3"), jacobian="time_avg"))
+    with pytest.raises(pd.ParadiagError):
+        pd.paradiag_workspace_bytes(pd.make_problem(config("c4"), jacobian=7))
 
 
 def test_long_window_limits(lib):
