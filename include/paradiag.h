@@ -176,7 +176,8 @@ PD_API int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_in
  * ([ny][nx]).  The copies are part of the call (end-to-end path). */
 PD_API int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd_solve_info* info);
 
-/* Number of kernel launches one paradiag_iterate enqueues (for launch accounting). */
+/* Number of kernel launches one paradiag_iterate enqueues (for launch accounting); -1 when it is
+ * data dependent (jacobian = PD_JACOBIAN_TIME_AVG: inner GMRES steps). */
 PD_API int paradiag_launches_per_iteration(const pd_handle* h);
 
 /* Per-kernel device time, measured with CUDA events recorded around each launch on the

@@ -1297,8 +1297,11 @@ int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd
 
 int paradiag_launches_per_iteration(const pd_handle* h) {
   if (!h) return 0;
+  if (h->P.jacobian == PD_JACOBIAN_TIME_AVG) return -1;   // data dependent (inner GMRES steps)
+  const int ntime = h->tlong ? (h->tlfuse && h->log2n2 == 10 && h->log2n1 >= 5 ? 3 : 5) : 1;
+  if (h->x1) return 1 /*reset*/ + 1 /*residual + x*/ + ntime + 1 /*x⁻¹ + update*/;
   int n = 1 /*reset*/ + 1 /*residual*/ + (can_fuse_update(h) ? 0 : 1) /*update*/;
-  n += h->P.dim == 2 ? 5 : 3;
+  n += h->P.dim == 2 ? 4 + ntime : (h->tlong ? 2 + ntime : 3);
   if (is_ch(h->P.kind)) n += 1;
   return n;
 }
