@@ -152,6 +152,7 @@ struct pd_handle {
   double* kdev = nullptr;             // device copy of dot results / combination coefficients
   double* khost = nullptr;            // pinned
   int kry_last = 0;                   // Krylov steps of the last inner solve
+  int cgs_passes = 2;                 // PARADIAG_CGS_PASSES=1: single classical Gram-Schmidt (A/B)
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -256,7 +257,9 @@ int allow_smem(K kernel, size_t bytes) {
 
 size_t time_smem(int nt, int warps) { return (size_t)warps * padded16(nt) * sizeof(double2); }
 size_t rows_smem(int M) { return (size_t)kLineWarps * dpadded(M) * sizeof(double); }
-size_t cols_smem(int M) { return ((size_t)kColW * dpadded(M) + 66 * kColW) * sizeof(double); }
+size_t cols_smem(int M, int w = kColW) { return ((size_t)w * dpadded(M) + 66 * w) * sizeof(double); }
+// generic column pass: kColW columns per CTA, 4 when the line buffers would exceed shared memory (M = 4096)
+int cols_per_cta(int M) { return cols_smem(M) <= kSmemMax ? kColW : 4; }
 
 // ----------------------------------------------------------------------------- launches
 int setup_fast_attrs(pd_handle* h) {
@@ -399,11 +402,17 @@ int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned
       if (h->neumann) k_dtt_rows<1, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
       else k_dtt_rows<0, kLineWarps><<<grid, kLineWarps * 32, smem, h->stream>>>(in, out, L);
     } else {
-      const int64_t groups = (int64_t)h->P.nt * ((h->nx + kColW - 1) / kColW);
+      const int cw = cols_per_cta(L.M);
+      const int64_t groups = (int64_t)h->P.nt * ((h->nx + cw - 1) / cw);
       const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 64);
-      const size_t smem = cols_smem(L.M);
-      if (h->neumann) k_dtt_cols<1, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
-      else k_dtt_cols<0, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
+      const size_t smem = cols_smem(L.M, cw);
+      if (cw == kColW) {
+        if (h->neumann) k_dtt_cols<1, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
+        else k_dtt_cols<0, kColW><<<grid, kColW * 32, smem, h->stream>>>(in, out, L);
+      } else {
+        if (h->neumann) k_dtt_cols<1, 4><<<grid, 4 * 32, smem, h->stream>>>(in, out, L);
+        else k_dtt_cols<0, 4><<<grid, 4 * 32, smem, h->stream>>>(in, out, L);
+      }
     }
   }
   prof_end(h, kid);
@@ -650,7 +659,7 @@ int precond_jt(pd_handle* h, const double* r, double* delta) {
       double* vn = V + (size_t)(j + 1) * n;
       if ((rc = apply_K(h, vj, vn))) return rc;                       // K v_j
       if ((rc = kaxpby(h, vn, vj, 1.0, -1.0))) return rc;             // A v_j = v_j - K v_j
-      for (int pass = 0; pass < 2; ++pass) {                          // classical Gram-Schmidt, twice
+      for (int pass = 0; pass < h->cgs_passes; ++pass) {              // classical Gram-Schmidt, twice
         if ((rc = kdots(h, V, j + 1, vn))) return rc;
         for (int i = 0; i <= j; ++i) Hij(i, j) += h->khost[i];
         if ((rc = kcombine(h, vn, V, j + 1, -1.0))) return rc;
@@ -1026,6 +1035,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(dalloc(h, &h->kdev, (size_t)kKryM + 2));
     if (cudaMallocHost(&h->khost, (kKryM + 1) * sizeof(double)) != cudaSuccess)
       return cleanup(fail(PD_ENOMEM, "cudaMallocHost"));
+    if (const char* f = std::getenv("PARADIAG_CGS_PASSES")) h->cgs_passes = std::max(1, std::min(2, std::atoi(f)));
   }
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
@@ -1139,8 +1149,13 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     }
     PD_TRY(allow_smem(k_dtt_rows<1, kLineWarps>, rows_smem(M)));
     PD_TRY(allow_smem(k_dtt_rows<0, kLineWarps>, rows_smem(M)));
-    PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
-    PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
+    if (cols_per_cta(M) == kColW) {
+      PD_TRY(allow_smem(k_dtt_cols<1, kColW>, cols_smem(M)));
+      PD_TRY(allow_smem(k_dtt_cols<0, kColW>, cols_smem(M)));
+    } else {
+      PD_TRY(allow_smem(k_dtt_cols<1, 4>, cols_smem(M, 4)));
+      PD_TRY(allow_smem(k_dtt_cols<0, 4>, cols_smem(M, 4)));
+    }
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<1>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<2>, kResSmem));

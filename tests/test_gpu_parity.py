@@ -193,3 +193,31 @@ def test_invalid_alias_rejected(cuda_lib):
     U = s.empty()
     with pytest.raises(cuda_lib.ParadiagError):
         s.residual(to_dev(make_u0(p)), U, U)
+
+
+# Largest spatial sizes: 2D m = 4096 (the ABI maximum; line length 8192, the generic line
+# kernels) and 1D m = 8191 (8192 unknowns in the pentadiagonal solves; the ABI allows 2^20 but the
+# oracle's banded LU is assembled densely), shortest window; P_α⁻¹ and the residual.
+MAX_CASES = {
+    "c5_m4096_nt2": twin("c5", m=4096, nt=2),
+    "c3_m4096_nt2": twin("c3", m=4096, nt=2),
+    "c2_m8191_nt2": twin("c2", m=8191, nt=2),
+}
+
+
+@pytest.mark.parametrize("name", sorted(MAX_CASES))
+def test_max_size_precond_and_residual(cuda_lib, name):
+    p = MAX_CASES[name]
+    s = cuda_lib.Solver(p)
+    r = _rand_U(p, 12)
+    d = s.empty()
+    s.apply_precond(to_dev(r, p), d, 0.0)
+    r_o = r.reshape(p.nt, p.nx) if p.dim == 1 else r
+    d_o, _ = precond.apply_precond(p, r_o, 0.0)
+    assert rel_err(to_host(d, p), d_o) <= 1e-11
+    u0 = make_u0(p)
+    U = _rand_U(p, 11)
+    rr = s.empty()
+    s.residual(to_dev(u0), to_dev(U, p), rr)
+    res_o, _ = iterate.residual(p, oracle_u0(p, u0), U.reshape(p.nt, p.nx) if p.dim == 1 else U)
+    assert rel_err(to_host(rr, p), res_o) <= 1e-12
