@@ -93,7 +93,12 @@ PD_DEV double2 ghost(const double2* v, int i, int l, const PentaParams& P) {
   return v[(size_t)i * P.nb + l];
 }
 
-// spec (in: ŝ, out: x), w1, w2 scratch [n][nb].
+// spec (in: ŝ, out: x), w1, w2 scratch [n][nb].  Refinement repeats (at most kPentaRefine times)
+// until the correction is below 1e-15 of the iterate, per bin — the oracle's criterion (SURVEY
+// §8(c) step 3.3).  One step suffices for c1/c2 (probe p10: 2.6e-7 → 1.8e-12); the condition
+// number grows like m⁴, so longer lines (m = 8191: cond ≈ 1e14) need two or three.
+constexpr int kPentaRefine = 6;
+
 __global__ void k_penta_solve(double2* spec, double2* w1, double2* w2, PentaParams P) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= P.nb) return;
@@ -103,35 +108,47 @@ __global__ void k_penta_solve(double2* spec, double2* w1, double2* w2, PentaPara
   // x = (LU)^{-1} s
   for (int i = 0; i < n; ++i) w1[(size_t)i * nb + l] = spec[(size_t)i * nb + l];
   penta_lu_solve(w1, l, P);
-  // w2 = L x (nested Laplacian with the BC's ghost rule)
-  for (int i = 0; i < n; ++i) {
-    const double2 xm = ghost(w1, i - 1, l, P), xc = w1[(size_t)i * nb + l], xp = ghost(w1, i + 1, l, P);
-    w2[(size_t)i * nb + l] = make_double2(((xm.x + xp.x) - 2.0 * xc.x) * P.inv_h2,
-                                          ((xm.y + xp.y) - 2.0 * xc.y) * P.inv_h2);
+  for (int it = 0; it < kPentaRefine; ++it) {
+    // w2 = L x (nested Laplacian with the BC's ghost rule)
+    for (int i = 0; i < n; ++i) {
+      const double2 xm = ghost(w1, i - 1, l, P), xc = w1[(size_t)i * nb + l], xp = ghost(w1, i + 1, l, P);
+      w2[(size_t)i * nb + l] = make_double2(((xm.x + xp.x) - 2.0 * xc.x) * P.inv_h2,
+                                            ((xm.y + xp.y) - 2.0 * xc.y) * P.inv_h2);
+    }
+    // ρ = s - (d x + A x), written over w2 with a sliding window of L x values
+    double2 lm = ghost(w2, -1, l, P);
+    double2 lc = w2[l];
+    for (int i = 0; i < n; ++i) {
+      // L x at i+1; past the end the ghost is L x_{n-2} (Neumann, = lm here) or 0 (hinged)
+      const double2 lp = i + 1 < n ? w2[(size_t)(i + 1) * nb + l]
+                                   : (P.neumann ? lm : make_double2(0.0, 0.0));
+      const double2 ll = make_double2(((lm.x + lp.x) - 2.0 * lc.x) * P.inv_h2,
+                                      ((lm.y + lp.y) - 2.0 * lc.y) * P.inv_h2);
+      double2 Ax;
+      if (P.kind == 0) Ax = ll;
+      else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
+      const size_t o = (size_t)i * nb + l;
+      const double2 x = w1[o], s = spec[o];
+      const double2 dx = cmul(d, x);
+      const double2 eAx = P.el ? cmul(e, Ax) : Ax;
+      w2[o] = make_double2(s.x - (dx.x + eAx.x), s.y - (dx.y + eAx.y));
+      lm = lc; lc = lp;
+    }
+    penta_lu_solve(w2, l, P);
+    double cmax = 0.0, xmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const size_t o = (size_t)i * nb + l;
+      const double2 c = w2[o];
+      const double2 x = cadd(w1[o], c);
+      w1[o] = x;
+      cmax = fmax(cmax, fmax(fabs(c.x), fabs(c.y)));
+      xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
+    }
+    if (!(cmax > 1e-15 * xmax)) break;
   }
-  // ρ = s - (d x + A x), written over w2 with a sliding window of L x values
-  double2 lm = ghost(w2, -1, l, P);
-  double2 lc = w2[l];
-  for (int i = 0; i < n; ++i) {
-    // L x at i+1; past the end the ghost is L x_{n-2} (Neumann, = lm here) or 0 (hinged)
-    const double2 lp = i + 1 < n ? w2[(size_t)(i + 1) * nb + l]
-                                 : (P.neumann ? lm : make_double2(0.0, 0.0));
-    const double2 ll = make_double2(((lm.x + lp.x) - 2.0 * lc.x) * P.inv_h2,
-                                    ((lm.y + lp.y) - 2.0 * lc.y) * P.inv_h2);
-    double2 Ax;
-    if (P.kind == 0) Ax = ll;
-    else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
-    const size_t o = (size_t)i * nb + l;
-    const double2 x = w1[o], s = spec[o];
-    const double2 dx = cmul(d, x);
-    const double2 eAx = P.el ? cmul(e, Ax) : Ax;
-    w2[o] = make_double2(s.x - (dx.x + eAx.x), s.y - (dx.y + eAx.y));
-    lm = lc; lc = lp;
-  }
-  penta_lu_solve(w2, l, P);
   for (int i = 0; i < n; ++i) {
     const size_t o = (size_t)i * nb + l;
-    spec[o] = cadd(w1[o], w2[o]);
+    spec[o] = w1[o];
   }
 }
 

@@ -15,7 +15,7 @@ from dataclasses import replace
 import numpy as np
 import pytest
 
-from _helpers import gshape, to_dev, to_host, rel_err, oracle_u0
+from _helpers import gshape, to_dev, to_host, rel_err, oracle_u0, rounding_floor_1d
 from oracle import iterate, precond, modespace, spatial, circulant
 from workloads import config, twin, make_u0
 
@@ -54,21 +54,6 @@ def _is_ch(p):
     return p.kind.startswith("cahn_hilliard")
 
 
-def _rounding_floor_1d(p, r, d_lu):
-    """The rounding floor of this P_α⁻¹ instance: the oracle's own Step (2) solved a second, equally
-    exact way (the eigenbasis divide the GPU uses, as oracle.precond.step2_2d does in 2D) differs
-    from its banded-LU result by this much; 1D Neumann instances near the growing modes of linear
-    CH (μ < 0) sit at ~3e-12."""
-    S1 = circulant.step1(r, p.alpha)
-    d = circulant.eig_d(p.nt, p.alpha, circulant.inv_dt(p))
-    e = circulant.eig_e(p.nt, p.alpha, p.theta)
-    T = spatial.transform_matrix(p.m, p.bc)
-    mu = spatial.mu(spatial.Lam_grid(p), p).reshape(-1)
-    S2 = ((S1 @ T.T) / (d[:, None] + e[:, None] * mu[None, :])) @ T.T / (2.0 * p.m)
-    d_sp, _ = circulant.step3(S2, p.alpha)
-    return rel_err(d_sp, d_lu)
-
-
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_tlong_precond_parity(solver_for, name):
     p = CASES[name]
@@ -81,7 +66,7 @@ def test_tlong_precond_parity(solver_for, name):
     r_o = r.reshape(p.nt, p.nx) if p.dim == 1 else r
     d_o, _ = precond.apply_precond(p, r_o, jbar)
     # bar: 1e-11, or 10x the instance's rounding floor where that is larger (1D)
-    bar = max(1e-11, 10 * _rounding_floor_1d(p, r_o, d_o)) if p.dim == 1 else 1e-11
+    bar = max(1e-11, 10 * rounding_floor_1d(p, r_o, d_o)) if p.dim == 1 else 1e-11
     assert rel_err(to_host(d, p), d_o) <= bar
     s.apply_precond(rd, rd, jbar)                  # in place
     assert rel_err(to_host(rd, p), d_o) <= bar
