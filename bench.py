@@ -176,7 +176,8 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
     y0, nyl = L.rows[rank]
     x0, nxl = L.cols[rank]
     ops = pdist.GpuOps(p, local, stream.cuda_stream, y0, nyl, x0, nxl)
-    rk = pdist.SlabRank(L, rank, ops)
+    # PARADIAG_SLAB_FUSED=0: the copy-based pack / unpack orchestration (A/B)
+    rk = pdist.SlabRank(L, rank, ops, fused=os.environ.get("PARADIAG_SLAB_FUSED", "1") != "0")
     comm = pdist.TorchComm()
     u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).to(dev)
 

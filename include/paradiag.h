@@ -223,6 +223,19 @@ PD_API int paradiag_slab_xpass(pd_handle* h, const double* in, double* out, int 
 /* In place on the column slab: y transform, time pass (Steps (1)-(3) per spatial mode),
  * inverse y transform. */
 PD_API int paradiag_slab_ypass(pd_handle* h, double* cols);
+/* The same passes reading / writing the all-to-all buffers directly (no pack / unpack copies):
+ * seg_* = NULL means the slab layout above; otherwise an int64 host array {k, (e0, cnt, off) × k}
+ * (k ≤ 8, blocks tiling the line in order) describing transpose blocks:
+ *   x pass (lines along x, local line ln = n·nyl + y): element x ∈ [e0_q, e0_q + cnt_q) lives at
+ *     buf[off_q + ln·cnt_q + (x − e0_q)]   (block q = [nt][nyl][cnt_q], the send/recv block of peer q)
+ *   y pass (lines along y): row y ∈ [e0_s, e0_s + cnt_s) of slice n, local column c lives at
+ *     buf[off_s + (n·cnt_s + y − e0_s)·nxl + c]   (block s = [nt][cnt_s][nxl])
+ * slab_ypass_seg runs y-DTT (in → cols), the time pass in place on cols, y-DTT⁻¹ (cols → out).
+ * in must not alias out unless both are the slab (seg NULL). */
+PD_API int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax,
+                                   const int64_t* seg_in, const int64_t* seg_out);
+PD_API int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out,
+                                   const int64_t* seg_in, const int64_t* seg_out);
 /* U_l += δ_l (ω = 1) and fold max|U| into the handle's ‖U‖∞ statistic. */
 PD_API int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l);
 /* dst[a*d0 + b*d1 + c] = src[a*s0 + b*s1 + c], a < n0, b < n1, c < n2 (element strides): the pack /

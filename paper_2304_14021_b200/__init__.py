@@ -59,7 +59,7 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_apply_precond_jt", "paradiag_iterate",
            "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy",
            "paradiag_init_slab", "paradiag_slab_geometry", "paradiag_slab_residual", "paradiag_slab_xpass",
-           "paradiag_slab_ypass", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
+           "paradiag_slab_ypass", "paradiag_slab_xpass_seg", "paradiag_slab_ypass_seg", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read"]
 ABI_VERSION = 3
 
@@ -96,6 +96,8 @@ def load(path: str = LIB_PATH):
     lib.paradiag_slab_residual.argtypes = [vp, vp, vp, vp, vp, vp]
     lib.paradiag_slab_xpass.argtypes = [vp, vp, vp, ctypes.c_int]
     lib.paradiag_slab_ypass.argtypes = [vp, vp]
+    lib.paradiag_slab_xpass_seg.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
+    lib.paradiag_slab_ypass_seg.argtypes = [vp, vp, vp, vp, vp, vp]
     lib.paradiag_slab_update.argtypes = [vp, vp, vp]
     lib.paradiag_copy3d.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64]
     lib.paradiag_stats_reset.argtypes = [vp]
@@ -264,6 +266,28 @@ def paradiag_slab_xpass(h, src, dst, want_dmax=False):
 
 def paradiag_slab_ypass(h, cols):
     _check(load().paradiag_slab_ypass(h, _ptr(cols, "cols")), "paradiag_slab_ypass")
+
+
+def _segmap(seg):
+    """[(e0, cnt, off), ...] -> int64 {k, e0, cnt, off, ...} (None: slab layout)."""
+    if seg is None:
+        return None, None
+    a = np.array([len(seg)] + [v for blk in seg for v in blk], dtype=np.int64)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+def paradiag_slab_xpass_seg(h, src, dst, want_dmax=False, seg_in=None, seg_out=None):
+    a_in, p_in = _segmap(seg_in)
+    a_out, p_out = _segmap(seg_out)
+    _check(load().paradiag_slab_xpass_seg(h, _ptr(src, "src"), _ptr(dst, "dst"), int(bool(want_dmax)), p_in, p_out),
+           "paradiag_slab_xpass_seg")
+
+
+def paradiag_slab_ypass_seg(h, src, cols, dst, seg_in=None, seg_out=None):
+    a_in, p_in = _segmap(seg_in)
+    a_out, p_out = _segmap(seg_out)
+    _check(load().paradiag_slab_ypass_seg(h, _ptr(src, "src"), _ptr(cols, "cols"), _ptr(dst, "dst"), p_in, p_out),
+           "paradiag_slab_ypass_seg")
 
 
 def paradiag_slab_update(h, U_l, delta_l):

@@ -163,6 +163,21 @@ PD_DEV void store_line(const double* __restrict__ ob, double* __restrict__ d, in
   }
 }
 
+// store_line into transpose blocks (SegMap rows form): line ln's elements of block q are contiguous
+template <bool AMAX>
+PD_DEV void store_line_seg(const double* __restrict__ ob, double* __restrict__ buf, const SegMap& S, int64_t ln,
+                           int lane, double& lmax) {
+  for (int q = 0; q < S.n; ++q) {
+    const int e0 = S.e0[q], e1 = e0 + S.cnt[q];
+    double* d = buf + S.off[q] + ln * S.cnt[q] - e0;
+    for (int e = e0 + lane; e < e1; e += 32) {
+      const double v = ob[e + (e >> 6)];               // opos(e)
+      d[e] = v;
+      if (AMAX) lmax = amax_acc(lmax, v);
+    }
+  }
+}
+
 // Fused defect-correction update for the last pass (linear kinds, ω = 1): U_line += δ_line with
 // δ taken from the staged line (never written to HBM), ‖δ‖∞ and ‖U‖∞ (NaN-safe bit max).  The
 // whole U line is loaded into registers first (the transform's registers are dead by now), so
@@ -224,8 +239,16 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
         double* x = xb + p * D::LDX + (NEUMANN ? 0 : 1);
-        const double* s = src + p * L.nx;
-        for (int e = lane; e < L.nel; e += 32) cp_async8(x + e, s + e);
+        if (L.sin.n) {                                     // transpose blocks
+          for (int q = 0; q < L.sin.n; ++q) {
+            const int e0 = L.sin.e0[q], e1 = e0 + L.sin.cnt[q];
+            const double* s = in + L.sin.off[q] + (L0 + p) * L.sin.cnt[q] - e0;
+            for (int e = e0 + lane; e < e1; e += 32) cp_async8(x + e, s + e);
+          }
+        } else {
+          const double* s = src + p * L.nx;
+          for (int e = lane; e < L.nel; e += 32) cp_async8(x + e, s + e);
+        }
       }
     }
     cp_async_commit();
@@ -244,6 +267,8 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
         if (L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
+        else if (L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
+        else if (L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (L.amax) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
         else store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
       }
@@ -307,7 +332,28 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     constexpr int PER = 64 / RSTEP;
     const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
     const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
-    if (c_t < wcols) {
+    if (c_t < wcols && L.sin.n) {                        // transpose blocks: row y lives in block s(y)
+      double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
+      auto seg_base = [&](int sg) {
+        return in + L.sin.off[sg] + ((int64_t)n * L.sin.cnt[sg] - L.sin.e0[sg]) * L.nx + x0 + c_t;
+      };
+      int sg = 0, s_end = L.sin.e0[0] + L.sin.cnt[0];
+      const double* sb = seg_base(0);
+      for (int e0 = e_t; e0 < L.nel; e0 += 64, lb += 64) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int e = e0 + j * RSTEP;
+          if (e < L.nel) {
+            while (e >= s_end) {
+              ++sg;
+              sb = seg_base(sg);
+              s_end = L.sin.e0[sg] + L.sin.cnt[sg];
+            }
+            cp_async8(lb + j * RSTEP, sb + (int64_t)e * L.nx);
+          }
+        }
+      }
+    } else if (c_t < wcols) {
       double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
       const double* s = src + (int64_t)e_t * L.nx + c_t;
       const int64_t rstride = (int64_t)RSTEP * L.nx;
@@ -328,7 +374,30 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     __syncthreads();
     D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
     __syncthreads();
-    if (c_t < wcols) {
+    if (c_t < wcols && L.sout.n) {
+      const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;
+      auto seg_base = [&](int sg) {
+        return out + L.sout.off[sg] + ((int64_t)n * L.sout.cnt[sg] - L.sout.e0[sg]) * L.nx + x0 + c_t;
+      };
+      int sg = 0, s_end = L.sout.e0[0] + L.sout.cnt[0];
+      double* sb = seg_base(0);
+      for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int e = e0 + j * RSTEP;
+          if (e < L.nel) {
+            while (e >= s_end) {
+              ++sg;
+              sb = seg_base(sg);
+              s_end = L.sout.e0[sg] + L.sout.cnt[sg];
+            }
+            const double v = ob[j * RSTEP];
+            sb[(int64_t)e * L.nx] = v;
+            if (L.amax) lmax = amax_acc(lmax, v);
+          }
+        }
+      }
+    } else if (c_t < wcols) {
       const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
       double* d = dst + (int64_t)e_t * L.nx + c_t;
       const int64_t rstride = (int64_t)RSTEP * L.nx;

@@ -24,6 +24,21 @@
 
 namespace pd {
 
+// Transpose-block addressing of a line pass's input or output (multi-rank slab mode):
+// the all-to-all send / receive buffers hold one block per peer, so the passes next to a transpose
+// read or write the blocks directly instead of the slab plus a pack / unpack copy.
+//   rows (x pass):    element x ∈ [e0[q], e0[q]+cnt[q]) of local line ln at buf[off[q] + ln·cnt[q] + x - e0[q]]
+//   columns (y pass): row y ∈ [e0[s], e0[s]+cnt[s]) of slice n, column c at
+//                     buf[off[s] + (n·cnt[s] + y - e0[s])·nxl + c]
+// n == 0: plain slab addressing.
+constexpr int kMaxSeg = 8;
+struct SegMap {
+  int n;
+  int e0[kMaxSeg];
+  int cnt[kMaxSeg];
+  int64_t off[kMaxSeg];
+};
+
 struct LineParams {
   int64_t nlines;        // rows: nt·ny;  columns: nt·nx
   int64_t nx, ns;        // row length (elements) and slice size
@@ -38,6 +53,7 @@ struct LineParams {
   unsigned long long* umax;   // with upd: max |U| after the update (bit-pattern max, NaN-safe)
   const double* oscale;  // k_cols3 only: outputs of slice n scaled by oscale[n] (NULL = 1)
   int stagger_ns;        // k_cols3: start delay of the second CTA of each SM (phase offset)
+  SegMap sin, sout;      // k_rows3 / k_cols3: transpose-block input / output (n = 0: plain)
 };
 
 // buffer index of stored element e: Neumann x_e = node e; hinged x_{e+1} = interior node e+1

@@ -367,6 +367,8 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.oscale = nullptr;
   L.stagger_ns = h->stagger_ns;
   L.umax = upd ? &h->st->umax_bits : nullptr;
+  L.sin.n = 0;
+  L.sout.n = 0;
   return L;
 }
 
@@ -1407,66 +1409,140 @@ int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, 
   return PD_OK;
 }
 
+int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
+                            const int64_t* seg_out);
+int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out, const int64_t* seg_in,
+                            const int64_t* seg_out);
+
 int paradiag_slab_xpass(pd_handle* h, const double* in, double* out, int want_dmax) {
+  return paradiag_slab_xpass_seg(h, in, out, want_dmax, nullptr, nullptr);
+}
+
+int paradiag_slab_ypass(pd_handle* h, double* buf) {
+  return paradiag_slab_ypass_seg(h, buf, buf, buf, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+// {k, (e0, cnt, off) × k} → SegMap; checks that the blocks tile [0, nel) in order
+int read_segmap(const int64_t* d, int nel, SegMap* S) {
+  S->n = 0;
+  if (!d) return PD_OK;
+  const int64_t k = d[0];
+  if (k < 1 || k > kMaxSeg) return fail(PD_EINVAL, "segment map: 1..8 blocks");
+  int64_t next = 0;
+  for (int q = 0; q < k; ++q) {
+    const int64_t e0 = d[1 + 3 * q], cnt = d[2 + 3 * q], off = d[3 + 3 * q];
+    if (e0 != next || cnt < 0 || off < 0) return fail(PD_EINVAL, "segment map: blocks must tile the line in order");
+    S->e0[q] = (int)e0;
+    S->cnt[q] = (int)cnt;
+    S->off[q] = off;
+    next = e0 + cnt;
+  }
+  if (next != nel) return fail(PD_EINVAL, "segment map: blocks must cover the whole line");
+  // empty trailing blocks are skipped by the kernels' loops; the first block may not be empty
+  // for the column kernels' running block index, so drop leading empty blocks
+  int q0 = 0;
+  while (q0 < k && S->cnt[q0] == 0) ++q0;
+  if (q0) {
+    for (int q = q0; q < k; ++q) {
+      S->e0[q - q0] = S->e0[q];
+      S->cnt[q - q0] = S->cnt[q];
+      S->off[q - q0] = S->off[q];
+    }
+  }
+  S->n = (int)k - q0;
+  return PD_OK;
+}
+
+// one block covering the whole line is the plain layout shifted by its offset
+int64_t plain_shift(SegMap* S) {
+  if (S->n != 1) return 0;
+  S->n = 0;
+  return S->off[0];
+}
+}  // namespace
+
+extern "C" {
+
+int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
+                            const int64_t* seg_out) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
   if (!in || !out) return fail(PD_EINVAL, "NULL buffer");
   LineParams L = line_params(h, 0, want_dmax ? &h->st->dmax_bits : nullptr);
   L.nlines = (int64_t)h->P.nt * h->nyl;
+  if ((rc = read_segmap(seg_in, h->nx, &L.sin)) || (rc = read_segmap(seg_out, h->nx, &L.sout))) return rc;
+  in += plain_shift(&L.sin);
+  out += plain_shift(&L.sout);
+  const int ver = h->dtt_ver;
+  h->dtt_ver = 3;                                   // the block addressing lives in the v3 kernels
   prof_begin(h, want_dmax ? K_XINV : K_XFWD);
   const bool ok = fast_line_any(h, in, out, 0, L);
   prof_end(h, want_dmax ? K_XINV : K_XFWD);
+  h->dtt_ver = ver;
   if (!ok) return fail(PD_EINVAL, "slab mode: unsupported line length");
   PD_LAUNCHED();
   return PD_OK;
 }
 
-int paradiag_slab_ypass(pd_handle* h, double* buf) {
+int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out, const int64_t* seg_in,
+                            const int64_t* seg_out) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
-  if (!buf) return fail(PD_EINVAL, "NULL buffer");
+  if (!in || !cols || !out) return fail(PD_EINVAL, "NULL buffer");
   // column slab [nt][ny][nxl]: lines along y with row stride nxl
   LineParams L = line_params(h, 1, nullptr);
   L.nlines = (int64_t)h->P.nt * h->nxl;
   L.nx = h->nxl;
   L.ns = (int64_t)h->ny * h->nxl;
   L.nel = h->ny;
+  SegMap sin, sout;
+  if ((rc = read_segmap(seg_in, h->ny, &sin)) || (rc = read_segmap(seg_out, h->ny, &sout))) return rc;
+  in += plain_shift(&sin);
+  out += plain_shift(&sout);
   FastLaunch F = fast_launch(h);
   F.nx = h->nxl;
   F.ns = L.ns;
+  F.dtt_ver = 3;                                    // the block addressing lives in the v3 kernels
   TimeParams T = time_params(h, nullptr);
   T.ns = L.ns;
   T.nx = h->nxl;
   T.xoff = h->x0;
   T.gamma_folded = 1;
   const int nm = h->neumann ? 1 : 0;
-  auto yline = [&](int kid) {
+  auto yline = [&](int kid, const double* src, double* dst) {
     L.oscale = kid == K_YFWD ? h->gam : h->ginv;
     prof_begin(h, kid);
     switch (L.M) {
-      case 64: fast_line<1>(nm, 1, buf, buf, L, F); break;
-      case 128: fast_line<2>(nm, 1, buf, buf, L, F); break;
-      case 256: fast_line<4>(nm, 1, buf, buf, L, F); break;
-      case 512: fast_line<8>(nm, 1, buf, buf, L, F); break;
-      case 1024: fast_line<16>(nm, 1, buf, buf, L, F); break;
-      default: fast_line<32>(nm, 1, buf, buf, L, F); break;
+      case 64: fast_line<1>(nm, 1, src, dst, L, F); break;
+      case 128: fast_line<2>(nm, 1, src, dst, L, F); break;
+      case 256: fast_line<4>(nm, 1, src, dst, L, F); break;
+      case 512: fast_line<8>(nm, 1, src, dst, L, F); break;
+      case 1024: fast_line<16>(nm, 1, src, dst, L, F); break;
+      default: fast_line<32>(nm, 1, src, dst, L, F); break;
     }
     prof_end(h, kid);
   };
-  yline(K_YFWD);
+  L.sin = sin;                                      // y forward: blocks (or the slab) → cols
+  L.sout.n = 0;
+  yline(K_YFWD, in, cols);
   prof_begin(h, K_TIME);
   switch (h->P.nt) {
-    case 32: fast_time<1>(buf, buf, T, F); break;
-    case 64: fast_time<2>(buf, buf, T, F); break;
-    case 128: fast_time<4>(buf, buf, T, F); break;
-    case 256: fast_time<8>(buf, buf, T, F); break;
-    case 512: fast_time<16>(buf, buf, T, F); break;
-    default: fast_time<32>(buf, buf, T, F); break;
+    case 32: fast_time<1>(cols, cols, T, F); break;
+    case 64: fast_time<2>(cols, cols, T, F); break;
+    case 128: fast_time<4>(cols, cols, T, F); break;
+    case 256: fast_time<8>(cols, cols, T, F); break;
+    case 512: fast_time<16>(cols, cols, T, F); break;
+    default: fast_time<32>(cols, cols, T, F); break;
   }
   prof_end(h, K_TIME);
-  yline(K_YINV);
+  L.sin.n = 0;                                      // y inverse: cols → blocks (or the slab)
+  L.sout = sout;
+  yline(K_YINV, cols, out);
   PD_LAUNCHED();
   return PD_OK;
 }

@@ -101,6 +101,28 @@ class SlabLayout:
     def bwd_unpack(self, r) -> List[Desc]:
         return [(n, d, s, do, so) for (n, s, d, so, do) in self.fwd_pack(r)]
 
+    # transpose-block maps (paradiag_slab_*_seg): the passes next to a transpose address the
+    # all-to-all buffers directly, so the packs / unpacks above are not copies at run time
+    def xmap(self, r):
+        """x-pass blocks of rank r: the forward send / backward receive buffer, block q =
+        [nt][nyl_r][nxl_q] holding x ∈ cols[q]: [(x0_q, nxl_q, offset_q)]"""
+        out, off = [], 0
+        for q in range(self.P):
+            x0, nxl = self.cols[q]
+            out.append((x0, nxl, off))
+            off += self.block(r, q)
+        return out
+
+    def ymap(self, q):
+        """y-pass blocks of rank q: the forward receive / backward send buffer, block s =
+        [nt][nyl_s][nxl_q] holding y ∈ rows[s]: [(y0_s, nyl_s, offset_s)]"""
+        out, off = [], 0
+        for s in range(self.P):
+            y0, nyl = self.rows[s]
+            out.append((y0, nyl, off))
+            off += self.block(s, q)
+        return out
+
     # residual halo: first / last two local rows of every slice, packed [nt][2][n]
     def halo_pack(self, r) -> Tuple[Desc, Desc]:
         nyl = self.rows[r][1]
@@ -144,6 +166,14 @@ class GpuOps:
     def ypass(self, cols):
         from . import paradiag_slab_ypass
         paradiag_slab_ypass(self.h, cols)
+
+    def xpass_seg(self, src, dst, want_dmax=False, seg_in=None, seg_out=None):
+        from . import paradiag_slab_xpass_seg
+        paradiag_slab_xpass_seg(self.h, src, dst, want_dmax, seg_in, seg_out)
+
+    def ypass_seg(self, src, cols, dst, seg_in=None, seg_out=None):
+        from . import paradiag_slab_ypass_seg
+        paradiag_slab_ypass_seg(self.h, src, cols, dst, seg_in, seg_out)
 
     def update(self, U_l, delta_l):
         from . import paradiag_slab_update
@@ -200,16 +230,39 @@ class SlabRank:
     """State and phases of one rank.  ``iterate`` runs one defect-correction iteration
     U ← U + P_α⁻¹(b − K U) on the rank's row slab."""
 
-    def __init__(self, layout: SlabLayout, rank: int, ops):
+    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True):
+        """fused: the x / y passes read and write the all-to-all buffers through the block maps
+        (no pack / unpack copies); False: the copy-based reference orchestration."""
         self.L, self.r, self.ops = layout, rank, ops
+        self.fused = fused
         self.y0, self.nyl = layout.rows[rank]
         self.x0, self.nxl = layout.cols[rank]
-        P = layout.P
-        tsz = max(sum(layout.fwd_send_splits(rank)), sum(layout.fwd_recv_splits(rank)))
+        P, r = layout.P, rank
         self.rows = ops.empty(layout.row_slab(rank))         # r, then δ
         self.cols = ops.empty(layout.col_slab(rank))
-        self.send = ops.empty(tsz)
-        self.recv = ops.empty(tsz)
+        if fused:
+            # one buffer [send | recv | self]: the block a rank keeps (row slab r ∩ column slab r)
+            # goes straight from the x pass to the y pass through the self region and is left out of
+            # the collective (split 0), so NCCL moves only the peer blocks
+            fs = [0 if q == r else layout.block(r, q) for q in range(P)]     # forward send / backward recv
+            fr = [0 if q == r else layout.block(q, r) for q in range(P)]     # forward recv / backward send
+            self.splits = {"fwd": (fs, fr), "bwd": (fr, fs)}                  # (send, recv) splits
+            ns, nr = max(sum(fs), sum(fr)), max(sum(fs), sum(fr))
+            self.buf = ops.empty(ns + nr + layout.block(r, r))
+            self.send, self.recv = self.buf[:ns], self.buf[ns:ns + nr]
+            so = ns + nr
+            cum = lambda sp: [sum(sp[:i]) for i in range(P)]
+            cfs, cfr = cum(fs), cum(fr)
+            self.xm_out = [(x0, c, so if q == r else cfs[q]) for q, (x0, c) in enumerate(layout.cols)]
+            self.ym_in = [(y0, c, so if q == r else ns + cfr[q]) for q, (y0, c) in enumerate(layout.rows)]
+            self.ym_out = [(y0, c, so if q == r else cfr[q]) for q, (y0, c) in enumerate(layout.rows)]
+            self.xm_in = [(x0, c, so if q == r else ns + cfs[q]) for q, (x0, c) in enumerate(layout.cols)]
+        else:
+            self.splits = {"fwd": (layout.fwd_send_splits(r), layout.fwd_recv_splits(r)),
+                           "bwd": (layout.bwd_send_splits(r), layout.bwd_recv_splits(r))}
+            tsz = max(sum(layout.fwd_send_splits(rank)), sum(layout.fwd_recv_splits(rank)))
+            self.send = ops.empty(tsz)
+            self.recv = ops.empty(tsz)
         hs = layout.halo_size()
         self.hsend_lo, self.hsend_hi = ops.empty(hs), ops.empty(hs)
         self.hlo = ops.empty(hs) if rank > 0 else None
@@ -225,11 +278,17 @@ class SlabRank:
 
     def phase_residual_xfwd(self, u0_l, U_l):
         self.ops.residual(u0_l, U_l, self.hlo, self.hhi, self.rows)
+        if self.fused:                                   # x pass stores straight into the send blocks
+            self.ops.xpass_seg(self.rows, self.buf, False, None, self.xm_out)
+            return
         self.ops.xpass(self.rows, self.rows)
         for d in self.L.fwd_pack(self.r):
             self.ops.copy(self.rows, self.send, d)
 
     def phase_ypass(self):
+        if self.fused:                                   # receive blocks -> cols -> send blocks
+            self.ops.ypass_seg(self.buf, self.cols, self.buf, self.ym_in, self.ym_out)
+            return
         for d in self.L.fwd_unpack(self.r):
             self.ops.copy(self.recv, self.cols, d)
         self.ops.ypass(self.cols)
@@ -237,10 +296,20 @@ class SlabRank:
             self.ops.copy(self.cols, self.send, d)
 
     def phase_xinv_update(self, U_l):
-        for d in self.L.bwd_unpack(self.r):
-            self.ops.copy(self.recv, self.rows, d)
-        self.ops.xpass(self.rows, self.rows, want_dmax=True)
+        if self.fused:                                   # inverse x pass loads the receive blocks
+            self.ops.xpass_seg(self.buf, self.rows, True, self.xm_in, None)
+        else:
+            for d in self.L.bwd_unpack(self.r):
+                self.ops.copy(self.recv, self.rows, d)
+            self.ops.xpass(self.rows, self.rows, want_dmax=True)
         self.ops.update(U_l, self.rows)
+
+    def _alltoall(self, comm, tm, phase):
+        ssp, rsp = self.splits[phase]
+        if sum(ssp) + sum(rsp) == 0:                     # P = 1 with the fused layout: nothing to move
+            return
+        with tm("alltoall_" + phase):
+            comm.all_to_all(self.recv, self.send, rsp, ssp)
 
     # ---- one iteration of a real multi-process run
     def iterate(self, u0_l, U_l, comm: TorchComm, timer=None):
@@ -252,11 +321,9 @@ class SlabRank:
             comm.halo(self.hsend_lo, self.hsend_hi, self.hlo if self.hlo is not None else self._dummy,
                       self.hhi if self.hhi is not None else self._dummy)
         self.phase_residual_xfwd(u0_l, U_l)
-        with tm("alltoall_fwd"):
-            comm.all_to_all(self.recv, self.send, L.fwd_recv_splits(r), L.fwd_send_splits(r))
+        self._alltoall(comm, tm, "fwd")
         self.phase_ypass()
-        with tm("alltoall_bwd"):
-            comm.all_to_all(self.recv, self.send, L.bwd_recv_splits(r), L.bwd_send_splits(r))
+        self._alltoall(comm, tm, "bwd")
         self.phase_xinv_update(U_l)
         dmax, umax = self.ops.stats_read()
         t = self.ops.empty(2) if hasattr(self.ops, "empty") else None
@@ -288,18 +355,19 @@ def iterate_virtual(ranks: List[SlabRank], u0s, Us):
             ranks[k].hhi.copy_(ranks[k + 1].hsend_lo)
     for k in range(P):
         ranks[k].phase_residual_xfwd(u0s[k], Us[k])
-    _alltoall_virtual(ranks, [L.fwd_send_splits(k) for k in range(P)])
+    _alltoall_virtual(ranks, "fwd")
     for k in range(P):
         ranks[k].phase_ypass()
-    _alltoall_virtual(ranks, [L.bwd_send_splits(k) for k in range(P)])
+    _alltoall_virtual(ranks, "bwd")
     for k in range(P):
         ranks[k].phase_xinv_update(Us[k])
     st = [rk.ops.stats_read() for rk in ranks]
     return max(s[0] for s in st), max(s[1] for s in st)
 
 
-def _alltoall_virtual(ranks, send_splits):
+def _alltoall_virtual(ranks, phase):
     P = len(ranks)
+    send_splits = [rk.splits[phase][0] for rk in ranks]
     soff = [[sum(send_splits[s][:q]) for q in range(P)] for s in range(P)]
     for q in range(P):
         off = 0

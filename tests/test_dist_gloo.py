@@ -68,6 +68,47 @@ class CpuOps:
         out = np.einsum("qy,tyx->tqx", self.T, x) / (2.0 * p.m) ** 2
         cols.copy_(torch.from_numpy(np.ascontiguousarray(out).reshape(-1)))
 
+    # transpose-block variants (the maps of SlabLayout.xmap / ymap): gather, run, scatter
+    def _gather_x(self, src, seg):
+        nt, nyl, n = self.p.nt, self.nyl, self.n
+        if seg is None:
+            return src.numpy().reshape(nt, nyl, n)
+        out = np.empty((nt, nyl, n))
+        for x0, cnt, off in seg:
+            out[:, :, x0:x0 + cnt] = src.numpy()[off:off + nt * nyl * cnt].reshape(nt, nyl, cnt)
+        return out
+
+    def _scatter_x(self, a, dst, seg):
+        nt, nyl = self.p.nt, self.nyl
+        if seg is None:
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)))
+            return
+        for x0, cnt, off in seg:
+            dst[off:off + nt * nyl * cnt] = torch.from_numpy(np.ascontiguousarray(a[:, :, x0:x0 + cnt]).reshape(-1))
+
+    def xpass_seg(self, src, dst, want_dmax=False, seg_in=None, seg_out=None):
+        a = self._gather_x(src, seg_in) @ self.T.T
+        if want_dmax:
+            self.dmax = max(self.dmax, float(np.abs(a).max()))
+        self._scatter_x(a, dst, seg_out)
+
+    def ypass_seg(self, src, cols, dst, seg_in=None, seg_out=None):
+        nt, n, nxl = self.p.nt, self.n, self.nxl
+        if seg_in is None:
+            cols.copy_(src)
+        else:
+            c = np.empty((nt, n, nxl))
+            for y0, cnt, off in seg_in:
+                c[:, y0:y0 + cnt, :] = src.numpy()[off:off + nt * cnt * nxl].reshape(nt, cnt, nxl)
+            cols.copy_(torch.from_numpy(c.reshape(-1)))
+        self.ypass(cols)
+        if seg_out is None:
+            dst.copy_(cols)
+            return
+        c = cols.numpy().reshape(nt, n, nxl)
+        for y0, cnt, off in seg_out:
+            dst[off:off + nt * cnt * nxl] = torch.from_numpy(np.ascontiguousarray(c[:, y0:y0 + cnt, :]).reshape(-1))
+
     def update(self, U_l, delta_l):
         U_l += delta_l
         self.umax = max(self.umax, float(U_l.abs().max()))
@@ -87,7 +128,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, K, out):
+def _worker(rank, world, port, name, K, out, fused=True):
     import torch.distributed as dist
     from paper_2304_14021_b200 import dist as pdist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -101,7 +142,7 @@ def _worker(rank, world, port, name, K, out):
         y0, nyl = L.rows[rank]
         x0, nxl = L.cols[rank]
         ops = CpuOps(p, y0, nyl, x0, nxl)
-        rk = pdist.SlabRank(L, rank, ops)
+        rk = pdist.SlabRank(L, rank, ops, fused=fused)
         comm = pdist.TorchComm()
         U_l = torch.from_numpy(np.ascontiguousarray(U0[:, y0:y0 + nyl]).reshape(-1))
         u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl]))
@@ -119,13 +160,14 @@ def _worker(rank, world, port, name, K, out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["block-io", "pack-copies"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_two_rank_gloo_iteration_matches_oracle(tmp_path, name):
+def test_two_rank_gloo_iteration_matches_oracle(tmp_path, name, fused):
     import torch.multiprocessing as mp
     p = CASES[name]
     K = 2
     out = str(tmp_path / "U.npy")
-    mp.spawn(_worker, args=(2, _free_port(), name, K, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), name, K, out, fused), nprocs=2, join=True)
     got = np.load(out)
     stats = np.load(out + ".stats.npy")
     u0 = make_u0(p)
@@ -158,3 +200,33 @@ def test_layout_descriptors_cover_every_element():
             assert (seen == 1).all()
             assert sum(L.fwd_send_splits(r)) == L.row_slab(r)
             assert sum(L.fwd_recv_splits(r)) == L.col_slab(r)
+
+
+def test_block_maps_match_the_pack_descriptors():
+    """SlabLayout.xmap / ymap (the addressing the fused passes use) place every element exactly
+    where the fwd_pack / fwd_unpack copies put it."""
+    from paper_2304_14021_b200.dist import SlabLayout
+    for n, nt, P in [(33, 3, 2), (33, 2, 3), (127, 2, 8)]:
+        L = SlabLayout(n, nt, P)
+        for r in range(P):
+            y0r, nyl = L.rows[r]
+            # x map: row-slab element (t, y, x) -> send offset
+            dest = np.full((nt, nyl, n), -1, dtype=np.int64)
+            for (n0, n1, n2), (s0, s1), (d0, d1), so, do in L.fwd_pack(r):
+                t, yy, xx = np.meshgrid(np.arange(n0), np.arange(n1), np.arange(n2), indexing="ij")
+                src = so + t * s0 + yy * s1 + xx
+                x = src % n
+                dest[t, yy, x] = do + t * d0 + yy * d1 + xx
+            for x0, cnt, off in L.xmap(r):
+                t, yy, xx = np.meshgrid(np.arange(nt), np.arange(nyl), np.arange(cnt), indexing="ij")
+                assert (dest[t, yy, x0 + xx] == off + (t * nyl + yy) * cnt + xx).all()
+            # y map: column-slab element (t, y, c) <- receive offset
+            x0r, nxl = L.cols[r]
+            srcof = np.full((nt, n, nxl), -1, dtype=np.int64)
+            for (n0, n1, n2), (s0, s1), (d0, d1), so, do in L.fwd_unpack(r):
+                t, yy, cc = np.meshgrid(np.arange(n0), np.arange(n1), np.arange(n2), indexing="ij")
+                dst = do + t * d0 + yy * d1 + cc
+                srcof[t, (dst % (n * nxl)) // nxl, cc] = so + t * s0 + yy * s1 + cc
+            for y0, cnt, off in L.ymap(r):
+                t, yy, cc = np.meshgrid(np.arange(nt), np.arange(cnt), np.arange(nxl), indexing="ij")
+                assert (srcof[t, y0 + yy, cc] == off + (t * cnt + yy) * nxl + cc).all()

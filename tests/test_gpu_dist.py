@@ -22,7 +22,7 @@ CASES = {
 }
 
 
-def _slabs(cuda_lib, p, P):
+def _slabs(cuda_lib, p, P, fused=True):
     from paper_2304_14021_b200 import dist
     L = dist.SlabLayout(p.n, p.nt, P)
     ranks = []
@@ -30,13 +30,14 @@ def _slabs(cuda_lib, p, P):
         y0, nyl = L.rows[r]
         x0, nxl = L.cols[r]
         ops = dist.GpuOps(p, 0, None, y0, nyl, x0, nxl)
-        ranks.append(dist.SlabRank(L, r, ops))
+        ranks.append(dist.SlabRank(L, r, ops, fused=fused))
     return L, ranks
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["block-io", "pack-copies"])
 @pytest.mark.parametrize("name", sorted(CASES))
-@pytest.mark.parametrize("P", [2, 3, 8])
-def test_virtual_ranks_match_single_gpu(cuda_lib, name, P):
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, fused):
     import torch
     from paper_2304_14021_b200 import dist
     p = CASES[name]
@@ -45,7 +46,7 @@ def test_virtual_ranks_match_single_gpu(cuda_lib, name, P):
     s = cuda_lib.Solver(p)
     U = to_dev(U0, p)
     u0d = to_dev(u0)
-    L, ranks = _slabs(cuda_lib, p, P)
+    L, ranks = _slabs(cuda_lib, p, P, fused)
     Us = [U.clone()[:, y0:y0 + nyl, :].contiguous().reshape(-1) for (y0, nyl) in L.rows]
     u0s = [u0d[y0:y0 + nyl, :].contiguous() for (y0, nyl) in L.rows]
     info = None
