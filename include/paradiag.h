@@ -236,6 +236,16 @@ PD_API int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, 
                                    const int64_t* seg_in, const int64_t* seg_out);
 PD_API int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out,
                                    const int64_t* seg_in, const int64_t* seg_out);
+/* Slice-range forms for overlapping the all-to-all with the passes (slices [n0, n0 + nn)):
+ * slab-layout buffers (seg NULL) are given from slice 0 and shifted by the library; block buffers
+ * are addressed relative to the range (the map's offsets point at this range's blocks, each
+ * [nn][…][cnt] / [nn][cnt][nxl]).  yrange stage 0: y-DTT in → cols, 1: the time pass on cols (all
+ * slices, n0/nn ignored), 2: y-DTT⁻¹ cols → out. */
+PD_API int paradiag_slab_xrange(pd_handle* h, const double* in, double* out, int want_dmax,
+                                const int64_t* seg_in, const int64_t* seg_out, int64_t n0, int64_t nn);
+PD_API int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* out, int stage,
+                                const int64_t* seg, int64_t n0, int64_t nn);
+PD_API int paradiag_slab_update_range(pd_handle* h, double* U_l, const double* delta_l, int64_t n0, int64_t nn);
 /* U_l += δ_l (ω = 1) and fold max|U| into the handle's ‖U‖∞ statistic. */
 PD_API int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l);
 /* dst[a*d0 + b*d1 + c] = src[a*s0 + b*s1 + c], a < n0, b < n1, c < n2 (element strides): the pack /

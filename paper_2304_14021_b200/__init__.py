@@ -59,7 +59,8 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_init", "paradiag_residual", "paradiag_apply_precond", "paradiag_apply_precond_jt", "paradiag_iterate",
            "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy",
            "paradiag_init_slab", "paradiag_slab_geometry", "paradiag_slab_residual", "paradiag_slab_xpass",
-           "paradiag_slab_ypass", "paradiag_slab_xpass_seg", "paradiag_slab_ypass_seg", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
+           "paradiag_slab_ypass", "paradiag_slab_xpass_seg", "paradiag_slab_ypass_seg", "paradiag_slab_xrange", "paradiag_slab_yrange",
+           "paradiag_slab_update_range", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read"]
 ABI_VERSION = 3
 
@@ -98,6 +99,9 @@ def load(path: str = LIB_PATH):
     lib.paradiag_slab_ypass.argtypes = [vp, vp]
     lib.paradiag_slab_xpass_seg.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
     lib.paradiag_slab_ypass_seg.argtypes = [vp, vp, vp, vp, vp, vp]
+    lib.paradiag_slab_xrange.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp, i64, i64]
+    lib.paradiag_slab_yrange.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp, i64, i64]
+    lib.paradiag_slab_update_range.argtypes = [vp, vp, vp, i64, i64]
     lib.paradiag_slab_update.argtypes = [vp, vp, vp]
     lib.paradiag_copy3d.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64]
     lib.paradiag_stats_reset.argtypes = [vp]
@@ -288,6 +292,24 @@ def paradiag_slab_ypass_seg(h, src, cols, dst, seg_in=None, seg_out=None):
     a_out, p_out = _segmap(seg_out)
     _check(load().paradiag_slab_ypass_seg(h, _ptr(src, "src"), _ptr(cols, "cols"), _ptr(dst, "dst"), p_in, p_out),
            "paradiag_slab_ypass_seg")
+
+
+def paradiag_slab_xrange(h, src, dst, want_dmax, seg_in, seg_out, n0, nn):
+    a_in, p_in = _segmap(seg_in)
+    a_out, p_out = _segmap(seg_out)
+    _check(load().paradiag_slab_xrange(h, _ptr(src, "src"), _ptr(dst, "dst"), int(bool(want_dmax)), p_in, p_out,
+                                       int(n0), int(nn)), "paradiag_slab_xrange")
+
+
+def paradiag_slab_yrange(h, src, cols, dst, stage, seg, n0, nn):
+    a, pp = _segmap(seg)
+    _check(load().paradiag_slab_yrange(h, _ptr(src, "src"), _ptr(cols, "cols"), _ptr(dst, "dst"), int(stage), pp,
+                                       int(n0), int(nn)), "paradiag_slab_yrange")
+
+
+def paradiag_slab_update_range(h, U_l, delta_l, n0, nn):
+    _check(load().paradiag_slab_update_range(h, _ptr(U_l, "U_l"), _ptr(delta_l, "delta_l"), int(n0), int(nn)),
+           "paradiag_slab_update_range")
 
 
 def paradiag_slab_update(h, U_l, delta_l):

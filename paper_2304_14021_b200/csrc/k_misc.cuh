@@ -23,6 +23,17 @@ k_update(double* U, const double* delta, size_t n, DevStats* st, int damped, dou
   // reaches the host check (the ‖δ‖∞ epilogues of the line passes do not propagate NaN)
   unsigned long long lbits = 0ull;
   const unsigned long long absmask = 0x7fffffffffffffffull;
+  if ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(Usrc) | reinterpret_cast<uintptr_t>(delta)) & 15) {
+    // a slice range of an odd-sized slab (chunked multi-rank schedule): scalar path
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const double u = Usrc[i] + w * delta[i];
+      U[i] = u;
+      lbits = max(lbits, (unsigned long long)__double_as_longlong(u) & absmask);
+    }
+    lbits = warp_max_u64(lbits);
+    if ((threadIdx.x & 31) == 0 && lbits) atomicMax(&st->umax_bits, lbits);
+    return;
+  }
   const size_t n2 = n / 2;
   double2* U2 = reinterpret_cast<double2*>(U);
   const double2* S2 = reinterpret_cast<const double2*>(Usrc);

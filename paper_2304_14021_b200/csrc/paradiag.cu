@@ -1409,17 +1409,31 @@ int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, 
   return PD_OK;
 }
 
-int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
-                            const int64_t* seg_out);
-int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out, const int64_t* seg_in,
-                            const int64_t* seg_out);
+int paradiag_slab_xrange(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
+                         const int64_t* seg_out, int64_t n0, int64_t nn);
+int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* out, int stage, const int64_t* seg,
+                         int64_t n0, int64_t nn);
 
 int paradiag_slab_xpass(pd_handle* h, const double* in, double* out, int want_dmax) {
-  return paradiag_slab_xpass_seg(h, in, out, want_dmax, nullptr, nullptr);
+  return paradiag_slab_xrange(h, in, out, want_dmax, nullptr, nullptr, 0, h ? h->P.nt : 0);
 }
 
 int paradiag_slab_ypass(pd_handle* h, double* buf) {
   return paradiag_slab_ypass_seg(h, buf, buf, buf, nullptr, nullptr);
+}
+
+int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
+                            const int64_t* seg_out) {
+  return paradiag_slab_xrange(h, in, out, want_dmax, seg_in, seg_out, 0, h ? h->P.nt : 0);
+}
+
+int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out, const int64_t* seg_in,
+                            const int64_t* seg_out) {
+  const int64_t nt = h ? h->P.nt : 0;
+  int rc;
+  if ((rc = paradiag_slab_yrange(h, in, cols, cols, 0, seg_in, 0, nt))) return rc;
+  if ((rc = paradiag_slab_yrange(h, cols, cols, cols, 1, nullptr, 0, nt))) return rc;
+  return paradiag_slab_yrange(h, cols, cols, out, 2, seg_out, 0, nt);
 }
 
 }  // extern "C"
@@ -1466,17 +1480,20 @@ int64_t plain_shift(SegMap* S) {
 
 extern "C" {
 
-int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
-                            const int64_t* seg_out) {
+int paradiag_slab_xrange(pd_handle* h, const double* in, double* out, int want_dmax, const int64_t* seg_in,
+                         const int64_t* seg_out, int64_t n0, int64_t nn) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
   if (!in || !out) return fail(PD_EINVAL, "NULL buffer");
+  if (n0 < 0 || nn < 1 || n0 + nn > h->P.nt) return fail(PD_EINVAL, "slice range outside [0, nt)");
   LineParams L = line_params(h, 0, want_dmax ? &h->st->dmax_bits : nullptr);
-  L.nlines = (int64_t)h->P.nt * h->nyl;
+  L.nlines = nn * h->nyl;
   if ((rc = read_segmap(seg_in, h->nx, &L.sin)) || (rc = read_segmap(seg_out, h->nx, &L.sout))) return rc;
-  in += plain_shift(&L.sin);
-  out += plain_shift(&L.sout);
+  // slab-layout buffers start at slice n0; block buffers are addressed relative to the range
+  const int64_t slice = (int64_t)h->nyl * h->nx;
+  in += seg_in ? plain_shift(&L.sin) : n0 * slice;
+  out += seg_out ? plain_shift(&L.sout) : n0 * slice;
   const int ver = h->dtt_ver;
   h->dtt_ver = 3;                                   // the block addressing lives in the v3 kernels
   prof_begin(h, want_dmax ? K_XINV : K_XFWD);
@@ -1488,61 +1505,89 @@ int paradiag_slab_xpass_seg(pd_handle* h, const double* in, double* out, int wan
   return PD_OK;
 }
 
-int paradiag_slab_ypass_seg(pd_handle* h, const double* in, double* cols, double* out, const int64_t* seg_in,
-                            const int64_t* seg_out) {
+int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* out, int stage, const int64_t* seg,
+                         int64_t n0, int64_t nn) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
   if (!in || !cols || !out) return fail(PD_EINVAL, "NULL buffer");
-  // column slab [nt][ny][nxl]: lines along y with row stride nxl
-  LineParams L = line_params(h, 1, nullptr);
-  L.nlines = (int64_t)h->P.nt * h->nxl;
-  L.nx = h->nxl;
-  L.ns = (int64_t)h->ny * h->nxl;
-  L.nel = h->ny;
-  SegMap sin, sout;
-  if ((rc = read_segmap(seg_in, h->ny, &sin)) || (rc = read_segmap(seg_out, h->ny, &sout))) return rc;
-  in += plain_shift(&sin);
-  out += plain_shift(&sout);
+  if (stage < 0 || stage > 2) return fail(PD_EINVAL, "stage: 0 y-DTT, 1 time pass, 2 y-DTT inverse");
+  if (stage != 1 && (n0 < 0 || nn < 1 || n0 + nn > h->P.nt)) return fail(PD_EINVAL, "slice range outside [0, nt)");
+  const int64_t slice = (int64_t)h->ny * h->nxl;     // column slab [nt][ny][nxl]: lines along y, stride nxl
   FastLaunch F = fast_launch(h);
   F.nx = h->nxl;
-  F.ns = L.ns;
+  F.ns = slice;
   F.dtt_ver = 3;                                    // the block addressing lives in the v3 kernels
-  TimeParams T = time_params(h, nullptr);
-  T.ns = L.ns;
-  T.nx = h->nxl;
-  T.xoff = h->x0;
-  T.gamma_folded = 1;
-  const int nm = h->neumann ? 1 : 0;
-  auto yline = [&](int kid, const double* src, double* dst) {
-    L.oscale = kid == K_YFWD ? h->gam : h->ginv;
-    prof_begin(h, kid);
-    switch (L.M) {
-      case 64: fast_line<1>(nm, 1, src, dst, L, F); break;
-      case 128: fast_line<2>(nm, 1, src, dst, L, F); break;
-      case 256: fast_line<4>(nm, 1, src, dst, L, F); break;
-      case 512: fast_line<8>(nm, 1, src, dst, L, F); break;
-      case 1024: fast_line<16>(nm, 1, src, dst, L, F); break;
-      default: fast_line<32>(nm, 1, src, dst, L, F); break;
+  if (stage == 1) {
+    TimeParams T = time_params(h, nullptr);
+    T.ns = slice;
+    T.nx = h->nxl;
+    T.xoff = h->x0;
+    T.gamma_folded = 1;
+    prof_begin(h, K_TIME);
+    switch (h->P.nt) {
+      case 32: fast_time<1>(cols, cols, T, F); break;
+      case 64: fast_time<2>(cols, cols, T, F); break;
+      case 128: fast_time<4>(cols, cols, T, F); break;
+      case 256: fast_time<8>(cols, cols, T, F); break;
+      case 512: fast_time<16>(cols, cols, T, F); break;
+      default: fast_time<32>(cols, cols, T, F); break;
     }
-    prof_end(h, kid);
-  };
-  L.sin = sin;                                      // y forward: blocks (or the slab) → cols
-  L.sout.n = 0;
-  yline(K_YFWD, in, cols);
-  prof_begin(h, K_TIME);
-  switch (h->P.nt) {
-    case 32: fast_time<1>(cols, cols, T, F); break;
-    case 64: fast_time<2>(cols, cols, T, F); break;
-    case 128: fast_time<4>(cols, cols, T, F); break;
-    case 256: fast_time<8>(cols, cols, T, F); break;
-    case 512: fast_time<16>(cols, cols, T, F); break;
-    default: fast_time<32>(cols, cols, T, F); break;
+    prof_end(h, K_TIME);
+    PD_LAUNCHED();
+    return PD_OK;
   }
-  prof_end(h, K_TIME);
-  L.sin.n = 0;                                      // y inverse: cols → blocks (or the slab)
-  L.sout = sout;
-  yline(K_YINV, cols, out);
+  LineParams L = line_params(h, 1, nullptr);
+  L.nlines = nn * h->nxl;
+  L.nx = h->nxl;
+  L.ns = slice;
+  L.nel = h->ny;
+  F.nt = (int)nn;
+  SegMap S;
+  if ((rc = read_segmap(seg, h->ny, &S))) return rc;
+  const int64_t shift = seg ? plain_shift(&S) : n0 * slice;
+  const double* src;
+  double* dst;
+  int kid;
+  if (stage == 0) {                                 // y forward: blocks (or the slab) → cols
+    L.sin = S;
+    src = in + shift;
+    dst = cols + n0 * slice;
+    L.oscale = h->gam + n0;                         // Γ_α folded into the forward y outputs
+    kid = K_YFWD;
+  } else {                                          // y inverse: cols → blocks (or the slab)
+    L.sout = S;
+    src = cols + n0 * slice;
+    dst = out + shift;
+    L.oscale = h->ginv + n0;
+    kid = K_YINV;
+  }
+  const int nm = h->neumann ? 1 : 0;
+  prof_begin(h, kid);
+  switch (L.M) {
+    case 64: fast_line<1>(nm, 1, src, dst, L, F); break;
+    case 128: fast_line<2>(nm, 1, src, dst, L, F); break;
+    case 256: fast_line<4>(nm, 1, src, dst, L, F); break;
+    case 512: fast_line<8>(nm, 1, src, dst, L, F); break;
+    case 1024: fast_line<16>(nm, 1, src, dst, L, F); break;
+    default: fast_line<32>(nm, 1, src, dst, L, F); break;
+  }
+  prof_end(h, kid);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_slab_update_range(pd_handle* h, double* U_l, const double* delta_l, int64_t n0, int64_t nn) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->slab) return fail(PD_EINVAL, "not a slab handle");
+  if (!U_l || !delta_l) return fail(PD_EINVAL, "NULL buffer");
+  if (n0 < 0 || nn < 1 || n0 + nn > h->P.nt) return fail(PD_EINVAL, "slice range outside [0, nt)");
+  const int64_t slice = (int64_t)h->nyl * h->nx;
+  prof_begin(h, K_UPDATE);
+  k_update<<<148 * 8, 256, 0, h->stream>>>(U_l + n0 * slice, delta_l + n0 * slice, (size_t)(nn * slice), h->st, 0,
+                                           1.0, 1.0);
+  prof_end(h, K_UPDATE);
   PD_LAUNCHED();
   return PD_OK;
 }

@@ -167,6 +167,18 @@ class GpuOps:
         from . import paradiag_slab_ypass
         paradiag_slab_ypass(self.h, cols)
 
+    def xrange(self, src, dst, want_dmax, seg_in, seg_out, n0, nn):
+        from . import paradiag_slab_xrange
+        paradiag_slab_xrange(self.h, src, dst, want_dmax, seg_in, seg_out, n0, nn)
+
+    def yrange(self, src, cols, dst, stage, seg, n0, nn):
+        from . import paradiag_slab_yrange
+        paradiag_slab_yrange(self.h, src, cols, dst, stage, seg, n0, nn)
+
+    def update_range(self, U_l, delta_l, n0, nn):
+        from . import paradiag_slab_update_range
+        paradiag_slab_update_range(self.h, U_l, delta_l, n0, nn)
+
     def xpass_seg(self, src, dst, want_dmax=False, seg_in=None, seg_out=None):
         from . import paradiag_slab_xpass_seg
         paradiag_slab_xpass_seg(self.h, src, dst, want_dmax, seg_in, seg_out)
@@ -204,9 +216,11 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def all_to_all(self, recv, send, recv_splits, send_splits):
-        self.dist.all_to_all_single(recv[:sum(recv_splits)], send[:sum(send_splits)], recv_splits, send_splits,
-                                    group=self.group)
+    def all_to_all(self, recv, send, recv_splits, send_splits, async_op=False):
+        """async_op: return the work handle; wait() on it orders the caller's stream after the
+        collective (NCCL) or blocks until it is done (gloo)."""
+        return self.dist.all_to_all_single(recv[:sum(recv_splits)], send[:sum(send_splits)], recv_splits,
+                                           send_splits, group=self.group, async_op=async_op)
 
     def halo(self, send_lo, send_hi, recv_lo, recv_hi):
         """send_lo -> rank-1 (its upper halo), send_hi -> rank+1 (its lower halo)"""
@@ -230,33 +244,50 @@ class SlabRank:
     """State and phases of one rank.  ``iterate`` runs one defect-correction iteration
     U ← U + P_α⁻¹(b − K U) on the rank's row slab."""
 
-    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True):
+    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True, chunks: int = 1):
         """fused: the x / y passes read and write the all-to-all buffers through the block maps
-        (no pack / unpack copies); False: the copy-based reference orchestration."""
+        (no pack / unpack copies); False: the copy-based reference orchestration.
+        chunks > 1 (fused only): the time slices are cut into that many ranges, each with its own
+        blocks in the buffer, so the all-to-all of one range runs (async) while the passes work on
+        the next (the time pass in the middle needs every slice and waits for all of them)."""
         self.L, self.r, self.ops = layout, rank, ops
         self.fused = fused
+        self.chunks = max(1, min(chunks, layout.nt)) if fused else 1
+        self.ranges = split(layout.nt, self.chunks)
         self.y0, self.nyl = layout.rows[rank]
         self.x0, self.nxl = layout.cols[rank]
         P, r = layout.P, rank
         self.rows = ops.empty(layout.row_slab(rank))         # r, then δ
         self.cols = ops.empty(layout.col_slab(rank))
         if fused:
-            # one buffer [send | recv | self]: the block a rank keeps (row slab r ∩ column slab r)
-            # goes straight from the x pass to the y pass through the self region and is left out of
-            # the collective (split 0), so NCCL moves only the peer blocks
-            fs = [0 if q == r else layout.block(r, q) for q in range(P)]     # forward send / backward recv
-            fr = [0 if q == r else layout.block(q, r) for q in range(P)]     # forward recv / backward send
-            self.splits = {"fwd": (fs, fr), "bwd": (fr, fs)}                  # (send, recv) splits
-            ns, nr = max(sum(fs), sum(fr)), max(sum(fs), sum(fr))
-            self.buf = ops.empty(ns + nr + layout.block(r, r))
-            self.send, self.recv = self.buf[:ns], self.buf[ns:ns + nr]
-            so = ns + nr
+            # per slice range one region [send | recv | self] of a single buffer: the block a rank
+            # keeps (row slab r ∩ column slab r) goes straight from the x pass to the y pass through
+            # the self region and is left out of the collective (split 0), so NCCL moves only the
+            # peer blocks.  Blocks of a range are [nn][rows][cols] (range-relative addressing).
             cum = lambda sp: [sum(sp[:i]) for i in range(P)]
-            cfs, cfr = cum(fs), cum(fr)
-            self.xm_out = [(x0, c, so if q == r else cfs[q]) for q, (x0, c) in enumerate(layout.cols)]
-            self.ym_in = [(y0, c, so if q == r else ns + cfr[q]) for q, (y0, c) in enumerate(layout.rows)]
-            self.ym_out = [(y0, c, so if q == r else cfr[q]) for q, (y0, c) in enumerate(layout.rows)]
-            self.xm_in = [(x0, c, so if q == r else ns + cfs[q]) for q, (x0, c) in enumerate(layout.cols)]
+            regions, base = [], 0
+            for n0, nn in self.ranges:
+                fs = [0 if q == r else nn * self.nyl * layout.cols[q][1] for q in range(P)]   # fwd send / bwd recv
+                fr = [0 if q == r else nn * layout.rows[q][1] * self.nxl for q in range(P)]  # fwd recv / bwd send
+                ns = max(sum(fs), sum(fr))
+                so = base + 2 * ns                                              # the self block
+                cfs, cfr = cum(fs), cum(fr)
+                regions.append(dict(
+                    n0=n0, nn=nn, base=base, ns=ns, splits={"fwd": (fs, fr), "bwd": (fr, fs)},
+                    xm_out=[(x0, c, so if q == r else base + cfs[q]) for q, (x0, c) in enumerate(layout.cols)],
+                    ym_in=[(y0, c, so if q == r else base + ns + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
+                    ym_out=[(y0, c, so if q == r else base + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
+                    xm_in=[(x0, c, so if q == r else base + ns + cfs[q]) for q, (x0, c) in enumerate(layout.cols)]))
+                base = so + nn * self.nyl * self.nxl
+            self.buf = ops.empty(base)
+            for g in regions:
+                g["send"] = self.buf[g["base"]:g["base"] + g["ns"]]
+                g["recv"] = self.buf[g["base"] + g["ns"]:g["base"] + 2 * g["ns"]]
+            self.regions = regions
+            # whole-range aliases (chunks = 1)
+            g = regions[0]
+            self.splits, self.send, self.recv = g["splits"], g["send"], g["recv"]
+            self.xm_out, self.ym_in, self.ym_out, self.xm_in = g["xm_out"], g["ym_in"], g["ym_out"], g["xm_in"]
         else:
             self.splits = {"fwd": (layout.fwd_send_splits(r), layout.fwd_recv_splits(r)),
                            "bwd": (layout.bwd_send_splits(r), layout.bwd_recv_splits(r))}
@@ -311,6 +342,57 @@ class SlabRank:
         with tm("alltoall_" + phase):
             comm.all_to_all(self.recv, self.send, rsp, ssp)
 
+    # ---- chunked phases (chunks > 1): range c's collective overlaps the passes of range c+1
+    def chunk_xfwd(self, c):
+        g = self.regions[c]
+        self.ops.xrange(self.rows, self.buf, False, None, g["xm_out"], g["n0"], g["nn"])
+
+    def chunk_yfwd(self, c):
+        g = self.regions[c]
+        self.ops.yrange(self.buf, self.cols, self.cols, 0, g["ym_in"], g["n0"], g["nn"])
+
+    def phase_time(self):
+        self.ops.yrange(self.cols, self.cols, self.cols, 1, None, 0, self.L.nt)
+
+    def chunk_yinv(self, c):
+        g = self.regions[c]
+        self.ops.yrange(self.cols, self.cols, self.buf, 2, g["ym_out"], g["n0"], g["nn"])
+
+    def chunk_xinv_update(self, c, U_l):
+        g = self.regions[c]
+        self.ops.xrange(self.buf, self.rows, True, g["xm_in"], None, g["n0"], g["nn"])
+        self.ops.update_range(U_l, self.rows, g["n0"], g["nn"])
+
+    def _alltoall_chunk(self, comm, c, phase):
+        g = self.regions[c]
+        ssp, rsp = g["splits"][phase]
+        if sum(ssp) + sum(rsp) == 0:
+            return None
+        return comm.all_to_all(g["recv"], g["send"], rsp, ssp, async_op=True)
+
+    def _iterate_chunked(self, u0_l, U_l, comm, tm):
+        self.ops.residual(u0_l, U_l, self.hlo, self.hhi, self.rows)
+        C = len(self.regions)
+        works = []
+        for c in range(C):                                # x pass of range c, then its transpose in flight
+            self.chunk_xfwd(c)
+            works.append(self._alltoall_chunk(comm, c, "fwd"))
+        with tm("alltoall_fwd_tail"):
+            for c in range(C):
+                if works[c] is not None:
+                    works[c].wait()
+                self.chunk_yfwd(c)
+        self.phase_time()
+        works = []
+        for c in range(C):
+            self.chunk_yinv(c)
+            works.append(self._alltoall_chunk(comm, c, "bwd"))
+        with tm("alltoall_bwd_tail"):
+            for c in range(C):
+                if works[c] is not None:
+                    works[c].wait()
+                self.chunk_xinv_update(c, U_l)
+
     # ---- one iteration of a real multi-process run
     def iterate(self, u0_l, U_l, comm: TorchComm, timer=None):
         """timer: optional callable(name) -> context manager timing a collective on the device"""
@@ -320,6 +402,13 @@ class SlabRank:
         with tm("halo"):
             comm.halo(self.hsend_lo, self.hsend_hi, self.hlo if self.hlo is not None else self._dummy,
                       self.hhi if self.hhi is not None else self._dummy)
+        if self.chunks > 1:
+            self._iterate_chunked(u0_l, U_l, comm, tm)
+            dmax, umax = self.ops.stats_read()
+            t = self.ops.empty(2)
+            t[0], t[1] = dmax, umax
+            comm.allreduce_max(t)
+            return float(t[0]), float(t[1])
         self.phase_residual_xfwd(u0_l, U_l)
         self._alltoall(comm, tm, "fwd")
         self.phase_ypass()
@@ -353,6 +442,8 @@ def iterate_virtual(ranks: List[SlabRank], u0s, Us):
             ranks[k].hlo.copy_(ranks[k - 1].hsend_hi)
         if k < P - 1:
             ranks[k].hhi.copy_(ranks[k + 1].hsend_lo)
+    if ranks[0].chunks > 1:
+        return _iterate_virtual_chunked(ranks, u0s, Us)
     for k in range(P):
         ranks[k].phase_residual_xfwd(u0s[k], Us[k])
     _alltoall_virtual(ranks, "fwd")
@@ -365,13 +456,44 @@ def iterate_virtual(ranks: List[SlabRank], u0s, Us):
     return max(s[0] for s in st), max(s[1] for s in st)
 
 
-def _alltoall_virtual(ranks, phase):
+def _iterate_virtual_chunked(ranks, u0s, Us):
+    """The chunked schedule with the per-range transposes emulated by copies."""
     P = len(ranks)
-    send_splits = [rk.splits[phase][0] for rk in ranks]
+    C = len(ranks[0].regions)
+    for k in range(P):
+        ranks[k].ops.residual(u0s[k], Us[k], ranks[k].hlo, ranks[k].hhi, ranks[k].rows)
+    for c in range(C):
+        for k in range(P):
+            ranks[k].chunk_xfwd(c)
+        _alltoall_virtual(ranks, "fwd", c)
+        for k in range(P):
+            ranks[k].chunk_yfwd(c)
+    for k in range(P):
+        ranks[k].phase_time()
+    for c in range(C):
+        for k in range(P):
+            ranks[k].chunk_yinv(c)
+        _alltoall_virtual(ranks, "bwd", c)
+        for k in range(P):
+            ranks[k].chunk_xinv_update(c, Us[k])
+    st = [rk.ops.stats_read() for rk in ranks]
+    return max(s[0] for s in st), max(s[1] for s in st)
+
+
+def _alltoall_virtual(ranks, phase, chunk=None):
+    P = len(ranks)
+    if chunk is not None:
+        send_splits = [rk.regions[chunk]["splits"][phase][0] for rk in ranks]
+        sends = [rk.regions[chunk]["send"] for rk in ranks]
+        recvs = [rk.regions[chunk]["recv"] for rk in ranks]
+    else:
+        send_splits = [rk.splits[phase][0] for rk in ranks]
+        sends = [rk.send for rk in ranks]
+        recvs = [rk.recv for rk in ranks]
     soff = [[sum(send_splits[s][:q]) for q in range(P)] for s in range(P)]
     for q in range(P):
         off = 0
         for s in range(P):
             c = send_splits[s][q]
-            ranks[q].recv[off:off + c].copy_(ranks[s].send[soff[s][q]:soff[s][q] + c])
+            recvs[q][off:off + c].copy_(sends[s][soff[s][q]:soff[s][q] + c])
             off += c

@@ -109,6 +109,48 @@ class CpuOps:
         for y0, cnt, off in seg_out:
             dst[off:off + nt * cnt * nxl] = torch.from_numpy(np.ascontiguousarray(c[:, y0:y0 + cnt, :]).reshape(-1))
 
+    # slice-range forms (chunked schedule): slab buffers from slice 0, blocks range-relative
+    def xrange(self, src, dst, want_dmax, seg_in, seg_out, n0, nn):
+        nyl, n = self.nyl, self.n
+        if seg_in is None:
+            a = src.numpy().reshape(self.p.nt, nyl, n)[n0:n0 + nn]
+        else:
+            a = np.empty((nn, nyl, n))
+            for x0, cnt, off in seg_in:
+                a[:, :, x0:x0 + cnt] = src.numpy()[off:off + nn * nyl * cnt].reshape(nn, nyl, cnt)
+        a = a @ self.T.T
+        if want_dmax:
+            self.dmax = max(self.dmax, float(np.abs(a).max()))
+        if seg_out is None:
+            dst.view(self.p.nt, nyl, n)[n0:n0 + nn] = torch.from_numpy(np.ascontiguousarray(a))
+        else:
+            for x0, cnt, off in seg_out:
+                dst[off:off + nn * nyl * cnt] = torch.from_numpy(np.ascontiguousarray(a[:, :, x0:x0 + cnt]).reshape(-1))
+
+    def yrange(self, src, cols, dst, stage, seg, n0, nn):
+        p, nt, n, nxl = self.p, self.p.nt, self.n, self.nxl
+        cv = cols.view(nt, n, nxl)
+        if stage == 0:
+            c = np.empty((nn, n, nxl))
+            for y0, cnt, off in seg:
+                c[:, y0:y0 + cnt, :] = src.numpy()[off:off + nn * cnt * nxl].reshape(nn, cnt, nxl)
+            cv[n0:n0 + nn] = torch.from_numpy(np.einsum("qy,tyx->tqx", self.T, c))
+        elif stage == 1:
+            S = circulant.step1(cv.numpy(), p.alpha)
+            d = circulant.eig_d(nt, p.alpha, circulant.inv_dt(p))
+            mu = precond._step2_mu(p, 0.0)[:, self.x0:self.x0 + nxl]
+            x, _ = circulant.step3(S / (d[:, None, None] + mu[None]), p.alpha)
+            cv.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+        else:
+            out = np.einsum("qy,tyx->tqx", self.T, cv.numpy()[n0:n0 + nn]) / (2.0 * p.m) ** 2
+            for y0, cnt, off in seg:
+                dst[off:off + nn * cnt * nxl] = torch.from_numpy(np.ascontiguousarray(out[:, y0:y0 + cnt, :]).reshape(-1))
+
+    def update_range(self, U_l, delta_l, n0, nn):
+        sl = slice(n0 * self.nyl * self.n, (n0 + nn) * self.nyl * self.n)
+        U_l[sl] += delta_l[sl]
+        self.umax = max(self.umax, float(U_l[sl].abs().max()))
+
     def update(self, U_l, delta_l):
         U_l += delta_l
         self.umax = max(self.umax, float(U_l.abs().max()))
@@ -128,7 +170,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, K, out, fused=True):
+def _worker(rank, world, port, name, K, out, fused=True, chunks=1):
     import torch.distributed as dist
     from paper_2304_14021_b200 import dist as pdist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -142,7 +184,7 @@ def _worker(rank, world, port, name, K, out, fused=True):
         y0, nyl = L.rows[rank]
         x0, nxl = L.cols[rank]
         ops = CpuOps(p, y0, nyl, x0, nxl)
-        rk = pdist.SlabRank(L, rank, ops, fused=fused)
+        rk = pdist.SlabRank(L, rank, ops, fused=fused, chunks=chunks)
         comm = pdist.TorchComm()
         U_l = torch.from_numpy(np.ascontiguousarray(U0[:, y0:y0 + nyl]).reshape(-1))
         u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl]))
@@ -160,14 +202,14 @@ def _worker(rank, world, port, name, K, out, fused=True):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["block-io", "pack-copies"])
+@pytest.mark.parametrize("mode", [(True, 1), (False, 1), (True, 3)], ids=["block-io", "pack-copies", "chunked3"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_two_rank_gloo_iteration_matches_oracle(tmp_path, name, fused):
+def test_two_rank_gloo_iteration_matches_oracle(tmp_path, name, mode):
     import torch.multiprocessing as mp
     p = CASES[name]
     K = 2
     out = str(tmp_path / "U.npy")
-    mp.spawn(_worker, args=(2, _free_port(), name, K, out, fused), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), name, K, out, mode[0], mode[1]), nprocs=2, join=True)
     got = np.load(out)
     stats = np.load(out + ".stats.npy")
     u0 = make_u0(p)

@@ -22,7 +22,7 @@ CASES = {
 }
 
 
-def _slabs(cuda_lib, p, P, fused=True):
+def _slabs(cuda_lib, p, P, fused=True, chunks=1):
     from paper_2304_14021_b200 import dist
     L = dist.SlabLayout(p.n, p.nt, P)
     ranks = []
@@ -30,14 +30,15 @@ def _slabs(cuda_lib, p, P, fused=True):
         y0, nyl = L.rows[r]
         x0, nxl = L.cols[r]
         ops = dist.GpuOps(p, 0, None, y0, nyl, x0, nxl)
-        ranks.append(dist.SlabRank(L, r, ops, fused=fused))
+        ranks.append(dist.SlabRank(L, r, ops, fused=fused, chunks=chunks))
     return L, ranks
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["block-io", "pack-copies"])
+@pytest.mark.parametrize("mode", [(True, 1), (False, 1), (True, 3)], ids=["block-io", "pack-copies", "chunked3"])
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
-def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, fused):
+def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, mode):
+    fused, chunks = mode
     import torch
     from paper_2304_14021_b200 import dist
     p = CASES[name]
@@ -46,7 +47,7 @@ def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, fused):
     s = cuda_lib.Solver(p)
     U = to_dev(U0, p)
     u0d = to_dev(u0)
-    L, ranks = _slabs(cuda_lib, p, P, fused)
+    L, ranks = _slabs(cuda_lib, p, P, fused, chunks)
     Us = [U.clone()[:, y0:y0 + nyl, :].contiguous().reshape(-1) for (y0, nyl) in L.rows]
     u0s = [u0d[y0:y0 + nyl, :].contiguous() for (y0, nyl) in L.rows]
     info = None
