@@ -207,11 +207,15 @@ k_tl_divide(double2* __restrict__ X, TlongParams Q) {
 // shared memory.  The forward FFT leaves bin k2 = lane + 32r in register r, which is exactly the
 // input layout of the inverse FFT, so the divided spectrum never leaves registers; Y is read and
 // written once (in place) instead of three round trips through X.
-constexpr int kFbPairs = 4;
-constexpr int kFbRowC = kFbPairs + 1;                 // staged row pitch (complex): 80 B
+#ifndef PD_FB_PAIRS
+#define PD_FB_PAIRS 4
+#endif
+constexpr int kFbPairs = PD_FB_PAIRS;                 // pencil pairs per group (2 groups per CTA)
+constexpr int kFbThreads = 2 * kFbPairs * 32;
+constexpr int kFbRowC = kFbPairs + 1;                 // staged row pitch (complex)
 constexpr size_t kFbSmem = (size_t)2 * 1024 * kFbRowC * sizeof(double2);   // 160 KB ≥ 8 × kWarpScratch
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kFbThreads, kFbPairs <= 2 ? 2 : 1)
 k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
   constexpr int L = 1024;
   extern __shared__ double2 sm[];
@@ -220,8 +224,8 @@ k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
   const int64_t chunk = blockIdx.x % nch4;
   const int j = (int)(blockIdx.x / nch4);               // 0: (0, N1/2); j ≥ 1: (j, N1 - j)
   const int k1b = j == 0 ? Q.N1 / 2 : Q.N1 - j;        // the second group's k1
-  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += 256) {
-    const int w = idx & 3, row = idx >> 2;
+  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += kFbThreads) {
+    const int w = idx % kFbPairs, row = idx / kFbPairs;
     const int n2 = row & (L - 1), grp = row >> 10;
     const int64_t p = chunk * kFbPairs + w;
     double2* d = sm + (grp * L + n2) * kFbRowC + w;
@@ -231,7 +235,7 @@ k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  const int grp = warp >> 2, pw = warp & 3;
+  const int grp = warp / kFbPairs, pw = warp % kFbPairs;
   const int k1 = grp ? k1b : j;
   double2 v[32];
 #pragma unroll
@@ -278,8 +282,8 @@ k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
     for (int r = 0; r < 32; ++r) sm[(grp * L + lane + 32 * r) * kFbRowC + pw] = tw.apply(v[r], r);
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += 256) {
-    const int w = idx & 3, row = idx >> 2;
+  for (int idx = threadIdx.x; idx < 2 * L * kFbPairs; idx += kFbThreads) {
+    const int w = idx % kFbPairs, row = idx / kFbPairs;
     const int n2 = row & (L - 1), g = row >> 10;
     const int64_t p = chunk * kFbPairs + w;
     if (p < Q.P) Y[((int64_t)(g ? k1b : j) * L + n2) * Q.P + p] = sm[(g * L + n2) * kFbRowC + w];

@@ -63,7 +63,7 @@ bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cu
   if (stage == 5) {                                     // fused B: Y in place (`out`)
     if (!tlong_fusable(Q)) return false;
     const int64_t nch4 = (Q.P + kFbPairs - 1) / kFbPairs;
-    k_tl_b_fused<<<(unsigned)(nch4 * (Q.N1 / 2)), 256, kFbSmem, s>>>(static_cast<double2*>(out), Q);
+    k_tl_b_fused<<<(unsigned)(nch4 * (Q.N1 / 2)), kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
     return true;
   }
   if (stage == 2) {
