@@ -276,15 +276,20 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
         e2e = {"value": K * p.dofs / te, "unit": "dof/s", "h2d_bytes_per_step": int(p.ns * 8),
                "d2h_bytes_per_step": int(p.ns * 8), "step": f"H2D u0 slabs, {K} sharded iterations, D2H u_Nt slabs",
                "seconds_per_step": te}
-    launches = 10 + 4 * world
+    # this rank's kernels in the timed region: the library's profiled launches plus, per step, the
+    # two halo pack copies and the stats reset (not profiled); every rank launches the same set
+    launches = sum(n for n, _ in prof.values()) + 3 * args.steps
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "dof/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": dict(cfg, parallelism=f"slab{world}: row slabs (residual, x transforms, update) / column "
-                                                 f"slabs (y transforms, time pass), NCCL all-to-all + halo"),
+                                                 f"slabs (y transforms, time pass), NCCL all-to-all + halo; passes "
+                                                 f"address the transpose blocks directly"
+                                                 + (f", {rk.chunks} slice ranges overlapping the transposes"
+                                                    if rk.chunks > 1 else "")),
                 "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
-                "gpu_launches": args.steps * launches * world, "clocks": clk.summary(), "kernels": kernels,
+                "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
                 "last_iter": {"delta_max": dmax, "u_max": umax}}
         print(json.dumps(line), flush=True)
     ops.close()
