@@ -178,9 +178,13 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
     ops = pdist.GpuOps(p, local, stream.cuda_stream, y0, nyl, x0, nxl)
     # PARADIAG_SLAB_FUSED=0: the copy-based pack / unpack orchestration (A/B)
     # PARADIAG_SLAB_CHUNKS: slice ranges whose all-to-all overlaps the next range's passes
+    # PARADIAG_SLAB_P2P=1 (opt-in): peer-memory transposes over CUDA IPC instead of the all-to-all
+    p2p = os.environ.get("PARADIAG_SLAB_P2P", "0") == "1"
     rk = pdist.SlabRank(L, rank, ops, fused=os.environ.get("PARADIAG_SLAB_FUSED", "1") != "0",
-                        chunks=int(os.environ.get("PARADIAG_SLAB_CHUNKS", "4" if world > 1 else "1")))
+                        chunks=int(os.environ.get("PARADIAG_SLAB_CHUNKS", "4" if world > 1 else "1")), p2p=p2p)
     comm = pdist.TorchComm()
+    if p2p:
+        rk.setup_p2p(comm)
     u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).to(dev)
 
     def fresh_U():
@@ -235,7 +239,7 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
     # own afterwards: the iteration's forward transpose (every range), timed on the device.
     sent = 8 * (sum(L.fwd_send_splits(rank)) - L.block(rank, rank))
     nvlink = None
-    if world > 1:
+    if world > 1 and not rk.p2p:
         groups = getattr(rk, "regions", None) or [{"send": rk.send, "recv": rk.recv, "splits": rk.splits}]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 3

@@ -246,6 +246,14 @@ PD_API int paradiag_slab_xrange(pd_handle* h, const double* in, double* out, int
 PD_API int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* out, int stage,
                                 const int64_t* seg, int64_t n0, int64_t nn);
 PD_API int paradiag_slab_update_range(pd_handle* h, double* U_l, const double* delta_l, int64_t n0, int64_t nn);
+/* Peer-memory transposes (opt-in): a block map offset may point into another rank's
+ * buffer mapped into this process (element offset from the call's buffer pointer, possibly
+ * negative), so the x pass and the inverse y pass store their peer blocks straight into the peers'
+ * receive buffers over NVLink.  These wrap CUDA IPC: export a device allocation (64-byte handle),
+ * map a peer's, unmap. */
+PD_API int paradiag_ipc_handle(const void* dev_ptr, unsigned char handle[64]);
+PD_API int paradiag_ipc_open(const unsigned char handle[64], void** dev_ptr);
+PD_API int paradiag_ipc_close(void* dev_ptr);
 /* U_l += δ_l (ω = 1) and fold max|U| into the handle's ‖U‖∞ statistic. */
 PD_API int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l);
 /* dst[a*d0 + b*d1 + c] = src[a*s0 + b*s1 + c], a < n0, b < n1, c < n2 (element strides): the pack /

@@ -60,7 +60,8 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_solve", "paradiag_solve_host", "paradiag_launches_per_iteration", "paradiag_destroy",
            "paradiag_init_slab", "paradiag_slab_geometry", "paradiag_slab_residual", "paradiag_slab_xpass",
            "paradiag_slab_ypass", "paradiag_slab_xpass_seg", "paradiag_slab_ypass_seg", "paradiag_slab_xrange", "paradiag_slab_yrange",
-           "paradiag_slab_update_range", "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
+           "paradiag_slab_update_range", "paradiag_ipc_handle", "paradiag_ipc_open", "paradiag_ipc_close",
+           "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read"]
 ABI_VERSION = 3
 
@@ -102,6 +103,9 @@ def load(path: str = LIB_PATH):
     lib.paradiag_slab_xrange.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp, i64, i64]
     lib.paradiag_slab_yrange.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp, i64, i64]
     lib.paradiag_slab_update_range.argtypes = [vp, vp, vp, i64, i64]
+    lib.paradiag_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+    lib.paradiag_ipc_open.argtypes = [ctypes.c_char_p, P(vp)]
+    lib.paradiag_ipc_close.argtypes = [vp]
     lib.paradiag_slab_update.argtypes = [vp, vp, vp]
     lib.paradiag_copy3d.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64]
     lib.paradiag_stats_reset.argtypes = [vp]
@@ -310,6 +314,26 @@ def paradiag_slab_yrange(h, src, cols, dst, stage, seg, n0, nn):
 def paradiag_slab_update_range(h, U_l, delta_l, n0, nn):
     _check(load().paradiag_slab_update_range(h, _ptr(U_l, "U_l"), _ptr(delta_l, "delta_l"), int(n0), int(nn)),
            "paradiag_slab_update_range")
+
+
+def paradiag_ipc_handle(addr) -> bytes:
+    """64-byte CUDA IPC handle of the allocation containing device address addr (int or tensor)."""
+    if not isinstance(addr, int):
+        addr = addr.data_ptr()
+    buf = ctypes.create_string_buffer(64)
+    _check(load().paradiag_ipc_handle(ctypes.c_void_p(addr), buf), "paradiag_ipc_handle")
+    return buf.raw
+
+
+def paradiag_ipc_open(handle: bytes) -> int:
+    """Map a peer's exported allocation; returns its device address in this process."""
+    ptr = ctypes.c_void_p()
+    _check(load().paradiag_ipc_open(ctypes.c_char_p(handle), ctypes.byref(ptr)), "paradiag_ipc_open")
+    return int(ptr.value)
+
+
+def paradiag_ipc_close(ptr: int):
+    _check(load().paradiag_ipc_close(ctypes.c_void_p(ptr)), "paradiag_ipc_close")
 
 
 def paradiag_slab_update(h, U_l, delta_l):

@@ -280,6 +280,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     ubits = warp_max_u64(ubits);
     if (lane == 0 && ubits) atomicMax(L.umax, ubits);
   }
+  if (L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
 }
 
 // ---------------------------------------------------------------- columns (stride nx)
@@ -422,6 +423,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     __syncthreads();
   }
   if (L.amax) warp_atomic_max_abs(L.amax, lmax);
+  if (L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
 }
 
 }  // namespace pd

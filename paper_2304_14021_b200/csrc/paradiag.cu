@@ -1448,7 +1448,9 @@ int read_segmap(const int64_t* d, int nel, SegMap* S) {
   int64_t next = 0;
   for (int q = 0; q < k; ++q) {
     const int64_t e0 = d[1 + 3 * q], cnt = d[2 + 3 * q], off = d[3 + 3 * q];
-    if (e0 != next || cnt < 0 || off < 0) return fail(PD_EINVAL, "segment map: blocks must tile the line in order");
+    // off may be negative: a peer's buffer mapped into this address space (CUDA IPC / one device)
+    // is addressed as an element offset from this call's buffer pointer
+    if (e0 != next || cnt < 0) return fail(PD_EINVAL, "segment map: blocks must tile the line in order");
     S->e0[q] = (int)e0;
     S->cnt[q] = (int)cnt;
     S->off[q] = off;
@@ -1574,6 +1576,29 @@ int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* o
   }
   prof_end(h, kid);
   PD_LAUNCHED();
+  return PD_OK;
+}
+
+int paradiag_ipc_handle(const void* dev_ptr, unsigned char handle[64]) {
+  if (!dev_ptr || !handle) return fail(PD_EINVAL, "NULL argument");
+  cudaIpcMemHandle_t hd;
+  PD_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(hd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &hd, 64);
+  return PD_OK;
+}
+
+int paradiag_ipc_open(const unsigned char handle[64], void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(PD_EINVAL, "NULL argument");
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, 64);
+  PD_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  return PD_OK;
+}
+
+int paradiag_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(PD_EINVAL, "NULL argument");
+  PD_CUDA(cudaIpcCloseMemHandle(dev_ptr));
   return PD_OK;
 }
 

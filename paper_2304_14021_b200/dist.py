@@ -239,27 +239,52 @@ class TorchComm:
     def allreduce_max(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
 
+    def fence(self):
+        """Stream-ordered barrier (a one-element NCCL all-reduce): every rank's preceding kernels,
+        including their peer-memory stores, complete before anyone's following kernels start."""
+        if not hasattr(self, "_tok"):
+            import torch
+            self._tok = torch.zeros(1, dtype=torch.float64, device=torch.cuda.current_device())
+        self.dist.all_reduce(self._tok, group=self.group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
 
 class SlabRank:
     """State and phases of one rank.  ``iterate`` runs one defect-correction iteration
     U ← U + P_α⁻¹(b − K U) on the rank's row slab."""
 
-    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True, chunks: int = 1):
+    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True, chunks: int = 1, p2p: bool = False):
         """fused: the x / y passes read and write the all-to-all buffers through the block maps
         (no pack / unpack copies); False: the copy-based reference orchestration.
         chunks > 1 (fused only): the time slices are cut into that many ranges, each with its own
         blocks in the buffer, so the all-to-all of one range runs (async) while the passes work on
         the next (the time pass in the middle needs every slice and waits for all of them)."""
         self.L, self.r, self.ops = layout, rank, ops
-        self.fused = fused
-        self.chunks = max(1, min(chunks, layout.nt)) if fused else 1
+        self.fused = fused or p2p
+        self.p2p = p2p
+        self.peer = None                                   # p2p: peer buffer addresses (connect_p2p)
+        self.chunks = 1 if p2p else (max(1, min(chunks, layout.nt)) if fused else 1)
         self.ranges = split(layout.nt, self.chunks)
         self.y0, self.nyl = layout.rows[rank]
         self.x0, self.nxl = layout.cols[rank]
         P, r = layout.P, rank
         self.rows = ops.empty(layout.row_slab(rank))         # r, then δ
         self.cols = ops.empty(layout.col_slab(rank))
-        if fused:
+        if p2p:
+            # peer-memory transposes: [recv_f | recv_b | self]; the x pass and the inverse y pass
+            # store their peer blocks straight into the peers' receive regions (maps set by
+            # connect_p2p once the peers' addresses are known), NCCL only fences
+            fs = [0 if q == r else layout.block(r, q) for q in range(P)]
+            fr = [0 if q == r else layout.block(q, r) for q in range(P)]
+            self.p2p_sizes = (sum(fr), sum(fs))
+            self.buf = ops.empty(sum(fr) + sum(fs) + layout.block(r, r))
+            self.send = self.recv = None
+            self.splits = {"fwd": ([0] * P, [0] * P), "bwd": ([0] * P, [0] * P)}
+        elif self.fused:
             # per slice range one region [send | recv | self] of a single buffer: the block a rank
             # keeps (row slab r ∩ column slab r) goes straight from the x pass to the y pass through
             # the self region and is left out of the collective (split 0), so NCCL moves only the
@@ -336,11 +361,73 @@ class SlabRank:
         self.ops.update(U_l, self.rows)
 
     def _alltoall(self, comm, tm, phase):
+        if self.p2p:                                     # the blocks were stored into the peers: fence
+            with tm("p2p_fence_" + phase):
+                comm.fence()
+            return
         ssp, rsp = self.splits[phase]
         if sum(ssp) + sum(rsp) == 0:                     # P = 1 with the fused layout: nothing to move
             return
         with tm("alltoall_" + phase):
             comm.all_to_all(self.recv, self.send, rsp, ssp)
+
+    # ---- peer-memory transposes
+    def p2p_layout(self, q):
+        """(recv_f base, recv_b base, fwd-recv block offsets, bwd-recv block offsets) of rank q's
+        buffer, in elements"""
+        L, P = self.L, self.L.P
+        fr_q = [0 if s == q else L.block(s, q) for s in range(P)]
+        fs_q = [0 if t == q else L.block(q, t) for t in range(P)]
+        cum = lambda sp: [sum(sp[:i]) for i in range(P)]
+        return 0, sum(fr_q), cum(fr_q), cum(fs_q)
+
+    def connect_p2p(self, peer_addr):
+        """peer_addr[q]: device address (in this process) of rank q's buffer; builds the maps whose
+        peer blocks are element offsets from this rank's own buffer."""
+        L, P, r = self.L, self.L.P, self.r
+        self.peer = list(peer_addr)
+        me = self.peer[r]
+        rf, rb, cfr, cfs = self.p2p_layout(r)
+        so = rb + sum(0 if t == r else L.block(r, t) for t in range(P))     # self region
+        rel = lambda q: (self.peer[q] - me) // 8
+        xm_out, ym_out = [], []
+        for q, (x0, c) in enumerate(L.cols):
+            if q == r:
+                xm_out.append((x0, c, so))
+            else:
+                qf, _, qcfr, _ = self.p2p_layout(q)
+                xm_out.append((x0, c, rel(q) + qf + qcfr[r]))      # my block in q's forward receive region
+        for s_, (y0, c) in enumerate(L.rows):
+            if s_ == r:
+                ym_out.append((y0, c, so))
+            else:
+                _, sb, _, scfs = self.p2p_layout(s_)
+                ym_out.append((y0, c, rel(s_) + sb + scfs[r]))     # my block in s's backward receive region
+        self.xm_out, self.ym_out = xm_out, ym_out
+        self.ym_in = [(y0, c, so if q == r else rf + cfr[q]) for q, (y0, c) in enumerate(L.rows)]
+        self.xm_in = [(x0, c, so if q == r else rb + cfs[q]) for q, (x0, c) in enumerate(L.cols)]
+
+    def setup_p2p(self, comm):
+        """Real multi-process run: export this rank's buffer (CUDA IPC), map every peer's."""
+        from . import paradiag_ipc_handle, paradiag_ipc_open
+        import cuda.bindings.driver as drv
+        ptr = self.buf.data_ptr()
+        err, base, _ = drv.cuMemGetAddressRange(ptr)
+        base = int(base)
+        if err != drv.CUresult.CUDA_SUCCESS:
+            raise RuntimeError(f"cuMemGetAddressRange: {err}")
+        info = (paradiag_ipc_handle(base), ptr - base)     # handle of the allocation, tensor offset
+        allinfo = comm.all_gather_object(info)
+        peer = []
+        self._mapped = []
+        for q, (hd, off) in enumerate(allinfo):
+            if q == self.r:
+                peer.append(ptr)
+            else:
+                b = paradiag_ipc_open(hd)
+                self._mapped.append(b)
+                peer.append(b + off)
+        self.connect_p2p(peer)
 
     # ---- chunked phases (chunks > 1): range c's collective overlaps the passes of range c+1
     def chunk_xfwd(self, c):
@@ -444,6 +531,10 @@ def iterate_virtual(ranks: List[SlabRank], u0s, Us):
             ranks[k].hhi.copy_(ranks[k + 1].hsend_lo)
     if ranks[0].chunks > 1:
         return _iterate_virtual_chunked(ranks, u0s, Us)
+    if ranks[0].p2p and ranks[0].peer is None:           # one process: the peers' buffers are local
+        addr = [rk.buf.data_ptr() for rk in ranks]
+        for rk in ranks:
+            rk.connect_p2p(addr)
     for k in range(P):
         ranks[k].phase_residual_xfwd(u0s[k], Us[k])
     _alltoall_virtual(ranks, "fwd")
@@ -482,6 +573,8 @@ def _iterate_virtual_chunked(ranks, u0s, Us):
 
 def _alltoall_virtual(ranks, phase, chunk=None):
     P = len(ranks)
+    if ranks[0].p2p:                                     # stored directly into the peers' regions
+        return
     if chunk is not None:
         send_splits = [rk.regions[chunk]["splits"][phase][0] for rk in ranks]
         sends = [rk.regions[chunk]["send"] for rk in ranks]

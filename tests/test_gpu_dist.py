@@ -22,7 +22,7 @@ CASES = {
 }
 
 
-def _slabs(cuda_lib, p, P, fused=True, chunks=1):
+def _slabs(cuda_lib, p, P, fused=True, chunks=1, p2p=False):
     from paper_2304_14021_b200 import dist
     L = dist.SlabLayout(p.n, p.nt, P)
     ranks = []
@@ -30,15 +30,16 @@ def _slabs(cuda_lib, p, P, fused=True, chunks=1):
         y0, nyl = L.rows[r]
         x0, nxl = L.cols[r]
         ops = dist.GpuOps(p, 0, None, y0, nyl, x0, nxl)
-        ranks.append(dist.SlabRank(L, r, ops, fused=fused, chunks=chunks))
+        ranks.append(dist.SlabRank(L, r, ops, fused=fused, chunks=chunks, p2p=p2p))
     return L, ranks
 
 
-@pytest.mark.parametrize("mode", [(True, 1), (False, 1), (True, 3)], ids=["block-io", "pack-copies", "chunked3"])
+@pytest.mark.parametrize("mode", [(True, 1, False), (False, 1, False), (True, 3, False), (True, 1, True)],
+                         ids=["block-io", "pack-copies", "chunked3", "peer-stores"])
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, mode):
-    fused, chunks = mode
+    fused, chunks, p2p = mode
     import torch
     from paper_2304_14021_b200 import dist
     p = CASES[name]
@@ -47,7 +48,7 @@ def test_virtual_ranks_match_single_gpu(cuda_lib, name, P, mode):
     s = cuda_lib.Solver(p)
     U = to_dev(U0, p)
     u0d = to_dev(u0)
-    L, ranks = _slabs(cuda_lib, p, P, fused, chunks)
+    L, ranks = _slabs(cuda_lib, p, P, fused, chunks, p2p)
     Us = [U.clone()[:, y0:y0 + nyl, :].contiguous().reshape(-1) for (y0, nyl) in L.rows]
     u0s = [u0d[y0:y0 + nyl, :].contiguous() for (y0, nyl) in L.rows]
     info = None
@@ -77,3 +78,47 @@ def test_slab_entry_points_reject_bad_geometry(cuda_lib):
     q = twin("c4", m=64, nt=32)
     with pytest.raises(cuda_lib.ParadiagError):                                          # CH: replicas only
         cuda_lib.paradiag_init_slab(cuda_lib.make_problem(q), 0, 0, 0, 10, 0, 10)
+
+
+def _ipc_child(handle, off, n, q):
+    import torch
+    import paper_2304_14021_b200 as pd
+    torch.cuda.set_device(0)
+    base = pd.paradiag_ipc_open(handle)
+    try:
+        # write through the mapped address with the library's own copy (a device kernel)
+        src = torch.arange(n, dtype=torch.float64, device="cuda") + 0.5
+        import ctypes
+        solver = pd.Solver(twin("c5", m=64, nt=32))         # any handle: copy3d runs on its stream
+        lib = pd.load()
+        rc = lib.paradiag_copy3d(solver.h, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(base + off),
+                                 1, 1, n, n, n, n, n)
+        torch.cuda.synchronize()
+        q.put(rc)
+    finally:
+        pd.paradiag_ipc_close(base)
+
+
+def test_ipc_export_and_map(cuda_lib):
+    """The peer-memory transposes' plumbing (CUDA IPC through the C ABI): a second process maps this
+    process's buffer (allocation base + the tensor's offset, as SlabRank.setup_p2p computes it) and
+    stores into it with a library kernel; this process reads the values back.  Two processes on one
+    device, no rank waits on another's kernels."""
+    import torch
+    import torch.multiprocessing as mp
+    import cuda.bindings.driver as drv
+    pool = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    t = pool[1000:1000 + 512]                          # not at the start of its allocation
+    err, base, _ = drv.cuMemGetAddressRange(t.data_ptr())
+    assert err == drv.CUresult.CUDA_SUCCESS
+    handle = cuda_lib.paradiag_ipc_handle(int(base))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_ipc_child, args=(handle, t.data_ptr() - int(base), 512, q))
+    pr.start()
+    rc = q.get(timeout=300)
+    pr.join(timeout=300)
+    assert rc == 0 and pr.exitcode == 0
+    torch.cuda.synchronize()
+    assert torch.equal(t.cpu(), torch.arange(512, dtype=torch.float64) + 0.5)
+    assert float(pool[:1000].abs().max()) == 0.0 and float(pool[1512:].abs().max()) == 0.0
