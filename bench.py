@@ -42,6 +42,24 @@ BYTES_PER_DOF = {  # algorithmic HBM bytes per space-time dof per launch (DESIGN
 }
 
 
+# the kernels of one P_α⁻¹ application (BASELINE.json target: "the preconditioner application at
+# ≥ 60% of the B200 HBM roofline"), by engine path
+PRECOND_KERNELS = ("dtt_x_fwd", "dtt_y_fwd", "time_solve_2d", "dtt_y_inv", "dtt_x_inv", "dtt_x_inv_update",
+                   "time_fwd_1d", "penta_solve", "time_inv_1d", "tlong_a_fwd", "tlong_b_fwd", "tlong_divide",
+                   "tlong_b_inv", "tlong_a_inv", "tlong_b_fused")
+
+
+def precond_summary(prof, steps, dofs, peak):
+    """Device time of the P_α⁻¹ kernels per step and the HBM fraction at their algorithmic bytes."""
+    ms = sum(tot for k, (n, tot) in prof.items() if k in PRECOND_KERNELS) / max(steps, 1)
+    nbytes = sum(BYTES_PER_DOF.get(k, 0.0) * n for k, (n, _) in prof.items() if k in PRECOND_KERNELS) / max(steps, 1) * dofs
+    if ms <= 0:
+        return None
+    return {"ms_per_step": ms, "algorithmic_bytes": nbytes, "achieved_gbs": nbytes / (ms * 1e-3) / 1e9,
+            "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peak,
+            "kernels": [k for k in prof if k in PRECOND_KERNELS]}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -294,6 +312,7 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
                                                     if rk.chunks > 1 else "")),
                 "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
+                "precond": precond_summary(prof, args.steps, local_dofs, peak),
                 "last_iter": {"delta_max": dmax, "u_max": umax}}
         print(json.dumps(line), flush=True)
     ops.close()
@@ -479,6 +498,7 @@ def main():
                 "gpu_launches": launches,
                 "clocks": clk.summary(), "kernels": kernels,
                 "iteration_hbm_frac_at_design_bytes": design_bytes / (ms_step * 1e-3) / 1e9 / peak,
+                "precond": precond_summary(prof, args.steps, p.dofs, peak),
                 "last_iter": {"delta_max": info.delta_max, "u_max": info.u_max}}
         print(json.dumps(line), flush=True)
     if world > 1:
