@@ -58,29 +58,62 @@ __global__ void k_penta_factor(PentaParams P) {
   }
 }
 
+// The solves are one thread per bin, so every row step is a dependent chain through the
+// recurrence; the loads it needs are not.  Rows are processed in chunks of kPentaChunk whose loads
+// are all issued before the chunk's arithmetic, so one memory latency is paid per chunk instead of
+// per row (c2: 129 bins, i.e. 129 threads on the whole GPU — latency is all there is).
+constexpr int kPentaChunk = 4;
+
 // Solve L U x = b in place in `v` (column l of an [n][nb] array).
-PD_DEV void penta_lu_solve(double2* v, int l, const PentaParams& P) {
+__device__ __noinline__ void penta_lu_solve(double2* __restrict__ v, int l, const PentaParams& P) {
   const int n = P.n, nb = P.nb;
-  const double* c2 = P.band + 4 * n;
+  const double* __restrict__ c2 = P.band + 4 * n;
   const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
   double2 y1 = {0, 0}, y2 = {0, 0};
-  for (int i = 0; i < n; ++i) {
-    const size_t o = (size_t)i * nb + l;
-    double2 y = v[o];
-    y = csub(y, cmul(P.l1[o], y1));
-    y = csub(y, cmul(P.l2[o], y2));
-    v[o] = y;
-    y2 = y1; y1 = y;
+  for (int i0 = 0; i0 < n; i0 += kPentaChunk) {
+    double2 vv[kPentaChunk], a1[kPentaChunk], a2[kPentaChunk];
+#pragma unroll
+    for (int k = 0; k < kPentaChunk; ++k)
+      if (i0 + k < n) {
+        const size_t o = (size_t)(i0 + k) * nb + l;
+        vv[k] = v[o];
+        a1[k] = P.l1[o];
+        a2[k] = P.l2[o];
+      }
+#pragma unroll
+    for (int k = 0; k < kPentaChunk; ++k)
+      if (i0 + k < n) {
+        double2 y = vv[k];
+        y = csub(y, cmul(a1[k], y1));
+        y = csub(y, cmul(a2[k], y2));
+        v[(size_t)(i0 + k) * nb + l] = y;
+        y2 = y1; y1 = y;
+      }
   }
   double2 x1 = {0, 0}, x2 = {0, 0};
-  for (int i = n - 1; i >= 0; --i) {
-    const size_t o = (size_t)i * nb + l;
-    double2 x = v[o];
-    x = csub(x, cmul(P.u1[o], x1));
-    x = csub(x, cscale(cmul(e, x2), c2[i]));
-    x = cmul(x, P.iu0[o]);
-    v[o] = x;
-    x2 = x1; x1 = x;
+  for (int i1 = n - 1; i1 >= 0; i1 -= kPentaChunk) {
+    double2 vv[kPentaChunk], b1[kPentaChunk], iu[kPentaChunk];
+    double cc[kPentaChunk];
+#pragma unroll
+    for (int k = 0; k < kPentaChunk; ++k)
+      if (i1 - k >= 0) {
+        const int i = i1 - k;
+        const size_t o = (size_t)i * nb + l;
+        vv[k] = v[o];
+        b1[k] = P.u1[o];
+        iu[k] = P.iu0[o];
+        cc[k] = c2[i];
+      }
+#pragma unroll
+    for (int k = 0; k < kPentaChunk; ++k)
+      if (i1 - k >= 0) {
+        double2 x = vv[k];
+        x = csub(x, cmul(b1[k], x1));
+        x = csub(x, cscale(cmul(e, x2), cc[k]));
+        x = cmul(x, iu[k]);
+        v[(size_t)(i1 - k) * nb + l] = x;
+        x2 = x1; x1 = x;
+      }
   }
 }
 
@@ -99,56 +132,104 @@ PD_DEV double2 ghost(const double2* v, int i, int l, const PentaParams& P) {
 // number grows like m⁴, so longer lines (m = 8191: cond ≈ 1e14) need two or three.
 constexpr int kPentaRefine = 6;
 
-__global__ void k_penta_solve(double2* spec, double2* w1, double2* w2, PentaParams P) {
+__global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ w1, double2* __restrict__ w2,
+                              PentaParams P) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= P.nb) return;
   const int n = P.n, nb = P.nb;
   const double2 d = P.dl[l];
   const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
+  constexpr int K = kPentaChunk;
   // x = (LU)^{-1} s
-  for (int i = 0; i < n; ++i) w1[(size_t)i * nb + l] = spec[(size_t)i * nb + l];
+  for (int i0 = 0; i0 < n; i0 += K) {
+    double2 t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (i0 + k < n) t[k] = spec[(size_t)(i0 + k) * nb + l];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (i0 + k < n) w1[(size_t)(i0 + k) * nb + l] = t[k];
+  }
   penta_lu_solve(w1, l, P);
   for (int it = 0; it < kPentaRefine; ++it) {
-    // w2 = L x (nested Laplacian with the BC's ghost rule)
-    for (int i = 0; i < n; ++i) {
-      const double2 xm = ghost(w1, i - 1, l, P), xc = w1[(size_t)i * nb + l], xp = ghost(w1, i + 1, l, P);
-      w2[(size_t)i * nb + l] = make_double2(((xm.x + xp.x) - 2.0 * xc.x) * P.inv_h2,
-                                            ((xm.y + xp.y) - 2.0 * xc.y) * P.inv_h2);
+    // ρ = s - (d x + A x) into w2, A x in nested form from a sliding window of x values:
+    // L x at i uses x_{i-1}, x_i, x_{i+1}; A x at i uses L x at i-1, i, i+1 (ghost rules of the BC)
+    auto lap = [&](double2 xm, double2 xc, double2 xp) {
+      return make_double2(((xm.x + xp.x) - 2.0 * xc.x) * P.inv_h2, ((xm.y + xp.y) - 2.0 * xc.y) * P.inv_h2);
+    };
+    // x at -1, 0, 1 (ghosts) and L x at -1, 0
+    double2 xm1 = ghost(w1, -1, l, P), x0 = w1[l], xp1 = ghost(w1, 1, l, P);
+    double2 lc = lap(xm1, x0, xp1);                          // L x at 0
+    double2 lm;                                             // L x at -1 (ghost rule for L x)
+    if (P.neumann) {
+      const double2 x2 = ghost(w1, 2, l, P);
+      lm = lap(x0, xp1, x2);                                 // L x_{-1} = L x_1 (even reflection)
+    } else {
+      lm = make_double2(0.0, 0.0);
     }
-    // ρ = s - (d x + A x), written over w2 with a sliding window of L x values
-    double2 lm = ghost(w2, -1, l, P);
-    double2 lc = w2[l];
-    for (int i = 0; i < n; ++i) {
-      // L x at i+1; past the end the ghost is L x_{n-2} (Neumann, = lm here) or 0 (hinged)
-      const double2 lp = i + 1 < n ? w2[(size_t)(i + 1) * nb + l]
-                                   : (P.neumann ? lm : make_double2(0.0, 0.0));
-      const double2 ll = make_double2(((lm.x + lp.x) - 2.0 * lc.x) * P.inv_h2,
-                                      ((lm.y + lp.y) - 2.0 * lc.y) * P.inv_h2);
-      double2 Ax;
-      if (P.kind == 0) Ax = ll;
-      else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
-      const size_t o = (size_t)i * nb + l;
-      const double2 x = w1[o], s = spec[o];
-      const double2 dx = cmul(d, x);
-      const double2 eAx = P.el ? cmul(e, Ax) : Ax;
-      w2[o] = make_double2(s.x - (dx.x + eAx.x), s.y - (dx.y + eAx.y));
-      lm = lc; lc = lp;
+    double2 xa = x0, xb = xp1;                               // x_i, x_{i+1}
+    for (int i0 = 0; i0 < n; i0 += K) {
+      double2 xn[K], sv[K], xv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int i = i0 + k;
+        if (i < n) {
+          xn[k] = ghost(w1, i + 2, l, P);                      // x_{i+2}
+          sv[k] = spec[(size_t)i * nb + l];
+          xv[k] = w1[(size_t)i * nb + l];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int i = i0 + k;
+        if (i < n) {
+          // L x at i+1 (past the end: Neumann reflects, hinged ghost L = 0)
+          double2 lp;
+          if (i + 1 < n) lp = lap(xa, xb, xn[k]);
+          else lp = P.neumann ? lm : make_double2(0.0, 0.0);
+          const double2 ll = lap(lm, lc, lp);
+          double2 Ax;
+          if (P.kind == 0) Ax = ll;
+          else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
+          const double2 x = xv[k], s = sv[k];
+          const double2 dx = cmul(d, x);
+          const double2 eAx = P.el ? cmul(e, Ax) : Ax;
+          w2[(size_t)i * nb + l] = make_double2(s.x - (dx.x + eAx.x), s.y - (dx.y + eAx.y));
+          lm = lc; lc = lp;
+          xa = xb; xb = xn[k];
+        }
+      }
     }
     penta_lu_solve(w2, l, P);
     double cmax = 0.0, xmax = 0.0;
-    for (int i = 0; i < n; ++i) {
-      const size_t o = (size_t)i * nb + l;
-      const double2 c = w2[o];
-      const double2 x = cadd(w1[o], c);
-      w1[o] = x;
-      cmax = fmax(cmax, fmax(fabs(c.x), fabs(c.y)));
-      xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
+    for (int i0 = 0; i0 < n; i0 += K) {
+      double2 cv[K], xv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (i0 + k < n) {
+          const size_t o = (size_t)(i0 + k) * nb + l;
+          cv[k] = w2[o];
+          xv[k] = w1[o];
+        }
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (i0 + k < n) {
+          const double2 x = cadd(xv[k], cv[k]);
+          w1[(size_t)(i0 + k) * nb + l] = x;
+          cmax = fmax(cmax, fmax(fabs(cv[k].x), fabs(cv[k].y)));
+          xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
+        }
     }
     if (!(cmax > 1e-15 * xmax)) break;
   }
-  for (int i = 0; i < n; ++i) {
-    const size_t o = (size_t)i * nb + l;
-    spec[o] = w1[o];
+  for (int i0 = 0; i0 < n; i0 += K) {
+    double2 t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (i0 + k < n) t[k] = w1[(size_t)(i0 + k) * nb + l];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (i0 + k < n) spec[(size_t)(i0 + k) * nb + l] = t[k];
   }
 }
 

@@ -155,6 +155,16 @@ struct pd_handle {
   // Gram-Schmidt passes per Arnoldi step: 1 (measured c4t 3.3 s vs 4.7 s with 2, same counts and
   // parity; convergence is only ever declared on the recomputed true residual); PARADIAG_CGS_PASSES=2
   int cgs_passes = 1;
+  // device-side window loop (paradiag_solve): graph of a conditional WHILE node around one
+  // iteration, captured for one U pointer; PARADIAG_GRAPH=0 keeps the host loop
+  bool use_graph = true;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphConditionalHandle gcond = 0;
+  cudaStream_t cap_stream = nullptr;
+  double* gU = nullptr;
+  void* ctl = nullptr;                // LoopCtl (device)
+  void* ctl_host = nullptr;           // pinned
   std::vector<void*> allocs;
   // optional per-kernel timing with CUDA events on the handle's stream (paradiag_profile)
   bool prof = false;
@@ -723,7 +733,8 @@ int init_iterate(pd_handle* h, double* U, const double* u0) {
   return PD_OK;
 }
 
-int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
+// One iteration's kernels (no host synchronisation except inside the NEXT-4 inner solve).
+int enqueue_iteration(pd_handle* h, const double* u0, double* U) {
   int rc;
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
@@ -746,6 +757,12 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
     if ((rc = precond(h, h->work, h->work))) return rc;
     if ((rc = launch_update(h, U, h->work))) return rc;
   }
+  return PD_OK;
+}
+
+int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
+  int rc;
+  if ((rc = enqueue_iteration(h, u0, U))) return rc;
   PD_CUDA(cudaMemcpyAsync(h->st_host, h->st, sizeof(DevStats), cudaMemcpyDeviceToHost, h->stream));
   PD_CUDA(cudaStreamSynchronize(h->stream));
   prof_collect(h);
@@ -758,6 +775,98 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
   info->jbar = is_ch(h->P.kind) ? h->st_host->jbar : 0.0;
   info->omega = h->st_host->omega;
   if (!std::isfinite(dmax) || !std::isfinite(umax)) return fail(PD_EDIVERGED, "non-finite increment or iterate");
+  return PD_OK;
+}
+
+// ---- device-side window loop (CUDA graph with a conditional WHILE node; SURVEY §8(a) a5 "scalars
+// to host or graph conditional"): the body is one iteration's kernels plus k_loop_decide, which
+// applies the stop rule on the device — no host round trip per iteration
+struct LoopCtl {
+  int iters, limit, fixed, status;   // status: 0 running, 1 converged, 2 iteration limit, 3 non-finite
+  double tol, rel, dmax, umax;
+};
+
+__global__ void k_loop_decide(const DevStats* st, LoopCtl* c, cudaGraphConditionalHandle cond) {
+  const double dmax = __longlong_as_double((long long)st->dmax_bits);
+  const double umax = __longlong_as_double((long long)st->umax_bits);
+  const int it = ++c->iters;
+  const bool finite = isfinite(dmax) && isfinite(umax);
+  const bool conv = c->fixed <= 0 && dmax <= c->tol * umax;           // R#4, as the host loop
+  c->status = !finite ? 3 : conv ? 1 : (it >= c->limit ? 2 : 0);
+  c->rel = umax > 0 ? dmax / umax : 0.0;
+  c->dmax = dmax;
+  c->umax = umax;
+  cudaGraphSetConditional(cond, c->status == 0 ? 1 : 0);
+}
+
+bool can_pipeline(const pd_handle* h);
+
+bool graph_ok(const pd_handle* h) {
+  return h->use_graph && !h->prof && !h->slab && h->P.jacobian == PD_JACOBIAN_SCALAR && !can_pipeline(h);
+}
+
+// Capture one iteration (reading u0 from the hand-off buffer, iterating on U) plus the stop rule
+// as the body of a conditional WHILE node.  Captured on a private stream (the caller's may be the
+// legacy default stream, which cannot be captured); launched on the caller's.
+int build_graph(pd_handle* h, double* U) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  h->gexec = nullptr;
+  h->graph = nullptr;
+  h->gU = nullptr;
+  if (!h->cap_stream) PD_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  if (!h->ctl) {
+    LoopCtl* c = nullptr;
+    int rc = dalloc(h, &c, 1);
+    if (rc) return rc;
+    h->ctl = c;
+  }
+  if (!h->ctl_host) PD_CUDA(cudaMallocHost(&h->ctl_host, sizeof(LoopCtl)));
+  PD_CUDA(cudaGraphCreate(&h->graph, 0));
+  PD_CUDA(cudaGraphConditionalHandleCreate(&h->gcond, h->graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h->gcond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  PD_CUDA(cudaGraphAddNode(&node, h->graph, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t saved = h->stream;
+  h->stream = h->cap_stream;
+  int rc = PD_OK;
+  if (cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess) {
+    rc = fail(PD_ECUDA, "graph capture begin");
+  } else {
+    rc = enqueue_iteration(h, h->u0buf, U);
+    if (rc == PD_OK) k_loop_decide<<<1, 1, 0, h->cap_stream>>>(h->st, static_cast<LoopCtl*>(h->ctl), h->gcond);
+    cudaGraph_t captured = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(h->cap_stream, &captured);
+    if (rc == PD_OK && e != cudaSuccess) rc = fail(PD_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  }
+  h->stream = saved;
+  if (rc) return rc;
+  PD_CUDA(cudaGraphInstantiate(&h->gexec, h->graph, 0));
+  h->gU = U;
+  return PD_OK;
+}
+
+// One window on the device: reset the loop control, launch the graph, read the outcome.
+int graph_window(pd_handle* h, int* iters, bool* conv, double* rel) {
+  LoopCtl* c = static_cast<LoopCtl*>(h->ctl_host);
+  *c = LoopCtl{};
+  c->fixed = h->P.fixed_iters;
+  c->limit = h->P.fixed_iters > 0 ? h->P.fixed_iters : h->P.max_iter;
+  c->tol = h->P.tol;
+  PD_CUDA(cudaMemcpyAsync(h->ctl, c, sizeof(LoopCtl), cudaMemcpyHostToDevice, h->stream));
+  PD_CUDA(cudaGraphLaunch(h->gexec, h->stream));
+  PD_CUDA(cudaMemcpyAsync(c, h->ctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, h->stream));
+  PD_CUDA(cudaStreamSynchronize(h->stream));
+  *iters = c->iters;
+  *conv = c->status == 1;
+  *rel = c->rel;
+  if (c->status == 3) return fail(PD_EDIVERGED, "non-finite increment or iterate");
   return PD_OK;
 }
 
@@ -924,6 +1033,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
     h->x1 = h->tlong && p->dim == 1 && h->nx <= 2 * kX1H;
     if (const char* f3 = std::getenv("PARADIAG_TLFUSE")) h->tlfuse = std::atoi(f3) != 0;
+    if (const char* f4 = std::getenv("PARADIAG_GRAPH")) h->use_graph = std::atoi(f4) != 0;
     if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
   }
   h->log2h = (p->dim == 2 || h->tlong) ? ilog2(M) - 1 : 0;
@@ -1259,6 +1369,38 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
       all_conv = all_conv && conv;
       if (!conv && h->P.fixed_iters <= 0) status = PD_NOT_CONVERGED;
       if (w + 1 < h->P.n_windows) {
+        PD_CUDA(cudaMemcpyAsync(h->u0buf, U + (size_t)(h->P.nt - 1) * h->ns, h->ns * sizeof(double),
+                                cudaMemcpyDeviceToDevice, h->stream));
+        cur_u0 = h->u0buf;
+      }
+      continue;
+    }
+    if (graph_ok(h)) {                 // device-side loop: one graph launch per window
+      if (cur_u0 != h->u0buf) {
+        PD_CUDA(cudaMemcpyAsync(h->u0buf, cur_u0, h->ns * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        cur_u0 = h->u0buf;
+      }
+      if ((!h->gexec || h->gU != U) && build_graph(h, U) != PD_OK) {
+        h->use_graph = false;            // capture unsupported here: host loop from now on
+        cudaGetLastError();
+      }
+    }
+    if (graph_ok(h) && h->gexec && h->gU == U) {
+      if ((rc = init_iterate(h, U, cur_u0))) return rc;
+      int iters = 0;
+      bool conv = false;
+      double rel = 0.0;
+      rc = graph_window(h, &iters, &conv, &rel);
+      info->iters[w] = iters;
+      info->last_rel[w] = rel;
+      if (rc) {
+        info->windows_done = w;
+        return rc;
+      }
+      info->windows_done = w + 1;
+      all_conv = all_conv && conv;
+      if (!conv && h->P.fixed_iters <= 0) status = PD_NOT_CONVERGED;
+      if (w + 1 < h->P.n_windows) {    // hand-off: u0 ← U_{N_t}
         PD_CUDA(cudaMemcpyAsync(h->u0buf, U + (size_t)(h->P.nt - 1) * h->ns, h->ns * sizeof(double),
                                 cudaMemcpyDeviceToDevice, h->stream));
         cur_u0 = h->u0buf;
@@ -1671,6 +1813,10 @@ void paradiag_destroy(pd_handle* h) {
   for (void* q : h->allocs) cudaFree(q);
   if (h->st_host) cudaFreeHost(h->st_host);
   if (h->khost) cudaFreeHost(h->khost);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  if (h->ctl_host) cudaFreeHost(h->ctl_host);
   delete h;
 }
 
