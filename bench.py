@@ -315,6 +315,10 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
                 "precond": precond_summary(prof, args.steps, local_dofs, peak),
                 "last_iter": {"delta_max": dmax, "u_max": umax}}
         print(json.dumps(line), flush=True)
+    if rk.p2p:
+        torch.cuda.synchronize()
+        dist.barrier()                      # no rank still stores into a peer before unmapping
+        rk.close_p2p()
     ops.close()
     dist.destroy_process_group()
     return 0

@@ -429,6 +429,13 @@ class SlabRank:
                 peer.append(b + off)
         self.connect_p2p(peer)
 
+    def close_p2p(self):
+        """Unmap the peers' buffers (setup_p2p)."""
+        from . import paradiag_ipc_close
+        for b in getattr(self, "_mapped", []):
+            paradiag_ipc_close(b)
+        self._mapped = []
+
     # ---- chunked phases (chunks > 1): range c's collective overlaps the passes of range c+1
     def chunk_xfwd(self, c):
         g = self.regions[c]
