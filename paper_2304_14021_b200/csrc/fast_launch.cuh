@@ -60,16 +60,25 @@ size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * s
 
 template <int E>
 cudaError_t fast_attrs() {
-  PD_ATTR((k_time2d_v2<E, kFastTimeWarps>), fast_time_smem(E));
+  PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 0>), fast_time_smem(E));
+  PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 1>), fast_time_smem(E));
+  PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 2>), fast_time_smem(E));
+  PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 3>), fast_time_smem(E));
   if (fast_time_smem(E, 8) <= 227 * 1024) PD_ATTR((k_time2d_v2<E, 8>), fast_time_smem(E, 8));
   PD_ATTR((k_rows_v2<1, E, kFastRowWarps>), fast_rows_smem());
   PD_ATTR((k_rows_v2<0, E, kFastRowWarps>), fast_rows_smem());
   PD_ATTR((k_cols_v2<1, E, fast_col_warps(E)>), fast_cols_smem(E));
   PD_ATTR((k_cols_v2<0, E, fast_col_warps(E)>), fast_cols_smem(E));
-  PD_ATTR((k_rows3<1, E, kFastRowWarps>), dtt3_rows_smem<E>() + 100 * 1024);
-  PD_ATTR((k_rows3<0, E, kFastRowWarps>), dtt3_rows_smem<E>() + 100 * 1024);
-  PD_ATTR((k_cols3<1, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
-  PD_ATTR((k_cols3<0, E, fast_col_warps(E)>), dtt3_cols_smem<E>());
+  PD_ATTR((k_rows3<1, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<0, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<1, E, kFastRowWarps, 1>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<0, E, kFastRowWarps, 1>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<1, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<0, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_cols3<1, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols3<0, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols3<1, E, fast_col_warps(E), 2>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols3<0, E, fast_col_warps(E), 2>), dtt3_cols_smem<E>());
   if (E == 32) {
     PD_ATTR((k_rows4<1, kPairsPerRowCta>), dttp_rows_smem());
     PD_ATTR((k_rows4<0, kPairsPerRowCta>), dttp_rows_smem());
@@ -103,7 +112,10 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
       const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
       // tune 256: pad the dynamic smem so only one CTA (4 warps) fits per SM (occupancy probe)
       const size_t smem = dtt3_rows_smem<E>() + ((L.tune & 256) ? 100 * 1024 : 0);
-      k_rows3<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+      const bool gen = L.sin.n || L.sout.n || L.upd;
+      if (gen) k_rows3<NEUMANN, E, kFastRowWarps, 2><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+      else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+      else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
       constexpr int C4 = 4 * (32 / E);
       const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);
@@ -112,7 +124,10 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
     } else {
       const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
       const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
-      k_cols3<NEUMANN, E, NW><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+      if (L.sin.n || L.sout.n || L.amax)
+        k_cols3<NEUMANN, E, NW, 2><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+      else
+        k_cols3<NEUMANN, E, NW, 0><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
     }
     return;
   }
@@ -145,7 +160,15 @@ void fast_time(const double* in, double* out, const TimeParams& T, const FastLau
   constexpr int S = 2 * (32 / E) * kFastTimeWarps;
   const int64_t tiles = (F.ns + S - 1) / S;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
-  k_time2d_v2<E, kFastTimeWarps><<<grid, kFastTimeWarps * 32, fast_time_smem(E), F.stream>>>(in, out, T);
+  const int flags = ((!T.el && !T.l3) ? 1 : 0) | (T.gamma_folded ? 2 : 0);
+  const size_t sm = fast_time_smem(E);
+  constexpr int NWT = kFastTimeWarps;
+  switch (flags) {
+    case 3: k_time2d_v2<E, NWT, 3><<<grid, NWT * 32, sm, F.stream>>>(in, out, T); break;
+    case 2: k_time2d_v2<E, NWT, 2><<<grid, NWT * 32, sm, F.stream>>>(in, out, T); break;
+    case 1: k_time2d_v2<E, NWT, 1><<<grid, NWT * 32, sm, F.stream>>>(in, out, T); break;
+    default: k_time2d_v2<E, NWT, 0><<<grid, NWT * 32, sm, F.stream>>>(in, out, T); break;
+  }
 }
 
 #define PD_FAST_INSTANTIATE(E)                                                                       \

@@ -207,9 +207,12 @@ PD_DEV void update_line(const double* __restrict__ ob, double* __restrict__ U, i
 // ---------------------------------------------------------------- rows (contiguous lines)
 // Warps are independent: each takes P consecutive lines per step, prefetches its next group into
 // L2, stages the lines with cp.async, transforms and stores them coalesced.
-template <int NEUMANN, int E, int NW>
+// V: 0 plain (no block I/O, no ‖·‖∞, no fused update), 1 with the ‖·‖∞ epilogue, 2 general
+// (runtime block maps / fused update / ‖·‖∞) — the common passes compile without the branches
+template <int NEUMANN, int E, int NW, int V = 2>
 __global__ void __launch_bounds__(NW * 32, 2)
 k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
+  constexpr bool GEN = V == 2;
   using D = Dtt3<NEUMANN, E>;
   extern __shared__ double2 smem2[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -233,13 +236,13 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     if ((L.tune & 1) && lane == 0 && g + gstride < ngroups)
       bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
     // fused update: bring this group's U rows towards L2 now, they are read after the transform
-    if (L.upd && lane == 0)
+    if (GEN && L.upd && lane == 0)
       bulk_prefetch_l2(L.upd + L0 * L.nx, (size_t)nl * L.nx * sizeof(double), L.upd + L.nlines * L.nx);
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
         double* x = xb + p * D::LDX + (NEUMANN ? 0 : 1);
-        if (L.sin.n) {                                     // transpose blocks
+        if (GEN && L.sin.n) {                              // transpose blocks
           for (int q = 0; q < L.sin.n; ++q) {
             const int e0 = L.sin.e0[q], e1 = e0 + L.sin.cnt[q];
             const double* s = in + L.sin.off[q] + (L0 + p) * L.sin.cnt[q] - e0;
@@ -266,30 +269,31 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
-        if (L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
-        else if (L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
-        else if (L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
-        else if (L.amax) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
+        if (GEN && L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
+        else if (GEN && L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
+        else if (GEN && L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
+        else if (V == 1 || (GEN && L.amax)) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
         else store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
       }
     }
     __syncwarp();
   }
-  if (L.amax) warp_atomic_max_abs(L.amax, lmax);
-  if (L.upd) {
+  if (V == 1 || (GEN && L.amax)) warp_atomic_max_abs(L.amax, lmax);
+  if (GEN && L.upd) {
     ubits = warp_max_u64(ubits);
     if (lane == 0 && ubits) atomicMax(L.umax, ubits);
   }
-  if (L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
+  if (GEN && L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
 }
 
 // ---------------------------------------------------------------- columns (stride nx)
 // CTA = NW warps x P lines = C adjacent columns of one slice.  Rows of the tile are loaded C
 // doubles wide (cp.async straight into each column's line buffer), the next tile is prefetched
 // into L2 during the transforms, outputs are read back from the line buffers row by row.
-template <int NEUMANN, int E, int NW>
+template <int NEUMANN, int E, int NW, int V = 2>
 __global__ void __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1)
 k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
+  constexpr bool GEN = V == 2;
   using D = Dtt3<NEUMANN, E>;
   constexpr int C = NW * D::P;
   constexpr int NTH = NW * 32;
@@ -333,7 +337,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     constexpr int PER = 64 / RSTEP;
     const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
     const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
-    if (c_t < wcols && L.sin.n) {                        // transpose blocks: row y lives in block s(y)
+    if (GEN && c_t < wcols && L.sin.n) {                        // transpose blocks: row y lives in block s(y)
       double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
       auto seg_base = [&](int sg) {
         return in + L.sin.off[sg] + ((int64_t)n * L.sin.cnt[sg] - L.sin.e0[sg]) * L.nx + x0 + c_t;
@@ -375,7 +379,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     __syncthreads();
     D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
     __syncthreads();
-    if (c_t < wcols && L.sout.n) {
+    if (GEN && c_t < wcols && L.sout.n) {
       const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;
       auto seg_base = [&](int sg) {
         return out + L.sout.off[sg] + ((int64_t)n * L.sout.cnt[sg] - L.sout.e0[sg]) * L.nx + x0 + c_t;
@@ -394,7 +398,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
             }
             const double v = ob[j * RSTEP];
             sb[(int64_t)e * L.nx] = v;
-            if (L.amax) lmax = amax_acc(lmax, v);
+            if (GEN && L.amax) lmax = amax_acc(lmax, v);
           }
         }
       }
@@ -402,7 +406,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
       double* d = dst + (int64_t)e_t * L.nx + c_t;
       const int64_t rstride = (int64_t)RSTEP * L.nx;
-      if (L.amax) {
+      if (V == 1 || (GEN && L.amax)) {
         for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65, d += 64 * L.nx) {
 #pragma unroll
           for (int j = 0; j < PER; ++j)
@@ -422,8 +426,8 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     }
     __syncthreads();
   }
-  if (L.amax) warp_atomic_max_abs(L.amax, lmax);
-  if (L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
+  if (V == 1 || (GEN && L.amax)) warp_atomic_max_abs(L.amax, lmax);
+  if (GEN && L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
 }
 
 }  // namespace pd
