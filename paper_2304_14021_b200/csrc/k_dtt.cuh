@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1)
 k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
   constexpr bool GEN = V == 2;
   using D = Dtt3<NEUMANN, E>;
+  constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;   // stored elements per line (= L.nel)
   constexpr int C = NW * D::P;
   constexpr int NTH = NW * 32;
   extern __shared__ double2 smem2[];
@@ -322,9 +323,9 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
         const double* lim = in + L.nlines * L.nx;
         if (L.tune & 8) {      // one bulk prefetch per row segment, lane 0 of each warp
           if (lane == 0)
-            for (int e = warp; e < L.nel; e += NW) bulk_prefetch_l2(s + (int64_t)e * L.nx, (size_t)wn * 8, lim);
+            for (int e = warp; e < kNel; e += NW) bulk_prefetch_l2(s + (int64_t)e * L.nx, (size_t)wn * 8, lim);
         } else {
-          for (int e = threadIdx.x; e < L.nel; e += NTH) {
+          for (int e = threadIdx.x; e < kNel; e += NTH) {
             prefetch_l2(s + (int64_t)e * L.nx);
             prefetch_l2(s + (int64_t)e * L.nx + wn - 1);
           }
@@ -344,11 +345,11 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       };
       int sg = 0, s_end = L.sin.e0[0] + L.sin.cnt[0];
       const double* sb = seg_base(0);
-      for (int e0 = e_t; e0 < L.nel; e0 += 64, lb += 64) {
+      for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64) {
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
           const int e = e0 + j * RSTEP;
-          if (e < L.nel) {
+          if (e < kNel) {
             while (e >= s_end) {
               ++sg;
               sb = seg_base(sg);
@@ -362,10 +363,10 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
       const double* s = src + (int64_t)e_t * L.nx + c_t;
       const int64_t rstride = (int64_t)RSTEP * L.nx;
-      for (int e0 = e_t; e0 < L.nel; e0 += 64, lb += 64, s += 64 * L.nx) {
+      for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.nx) {
 #pragma unroll
         for (int j = 0; j < PER; ++j)
-          if (e0 + j * RSTEP < L.nel) cp_async8(lb + j * RSTEP, s + j * rstride);
+          if (e0 + j * RSTEP < kNel) cp_async8(lb + j * RSTEP, s + j * rstride);
       }
     }
     cp_async_commit();
@@ -386,11 +387,11 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       };
       int sg = 0, s_end = L.sout.e0[0] + L.sout.cnt[0];
       double* sb = seg_base(0);
-      for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65) {
+      for (int e0 = e_t; e0 < kNel; e0 += 64, ob += 65) {
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
           const int e = e0 + j * RSTEP;
-          if (e < L.nel) {
+          if (e < kNel) {
             while (e >= s_end) {
               ++sg;
               sb = seg_base(sg);
@@ -407,20 +408,20 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       double* d = dst + (int64_t)e_t * L.nx + c_t;
       const int64_t rstride = (int64_t)RSTEP * L.nx;
       if (V == 1 || (GEN && L.amax)) {
-        for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65, d += 64 * L.nx) {
+        for (int e0 = e_t; e0 < kNel; e0 += 64, ob += 65, d += 64 * L.nx) {
 #pragma unroll
           for (int j = 0; j < PER; ++j)
-            if (e0 + j * RSTEP < L.nel) {
+            if (e0 + j * RSTEP < kNel) {
               const double v = ob[j * RSTEP];
               d[j * rstride] = v;
               lmax = amax_acc(lmax, v);
             }
         }
       } else {
-        for (int e0 = e_t; e0 < L.nel; e0 += 64, ob += 65, d += 64 * L.nx) {
+        for (int e0 = e_t; e0 < kNel; e0 += 64, ob += 65, d += 64 * L.nx) {
 #pragma unroll
           for (int j = 0; j < PER; ++j)
-            if (e0 + j * RSTEP < L.nel) d[j * rstride] = ob[j * RSTEP];
+            if (e0 + j * RSTEP < kNel) d[j * rstride] = ob[j * RSTEP];
         }
       }
     }

@@ -341,6 +341,8 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
         k_residual_tile<2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.theta != 1.0)
         k_residual_tile<1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else if (!is_ch(h->P.kind))       // linear, single handle (launch_residual has no slab halos)
+        k_residual_tile<0, false, true><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else
         k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y * grd.z;
@@ -1271,6 +1273,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       PD_TRY(allow_smem(k_dtt_cols<0, 4>, cols_smem(M, 4)));
     }
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<0, false, true>), kResSmem));
     PD_TRY(allow_smem(k_residual_tile<1>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<2>, kResSmem));
     PD_TRY(allow_smem(k_residual_tile<0, true>, kResSmemUpd));
