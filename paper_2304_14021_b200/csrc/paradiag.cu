@@ -338,13 +338,13 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
       else if (dU)
         k_residual_tile<0, true><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.kind == PD_CAHN_HILLIARD_EYRE)
-        k_residual_tile<2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+        k_residual_tile<2, false, 2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.theta != 1.0)
-        k_residual_tile<1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+        k_residual_tile<1, false, 1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (!is_ch(h->P.kind))       // linear, single handle (launch_residual has no slab halos)
-        k_residual_tile<0, false, true><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
-      else
-        k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+        k_residual_tile<0, false, 1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else                              // CH PinT-I, single handle
+        k_residual_tile<0, false, 2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       nparts = (size_t)grd.x * grd.y * grd.z;
     }
   } else {
@@ -1273,9 +1273,10 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       PD_TRY(allow_smem(k_dtt_cols<0, 4>, cols_smem(M, 4)));
     }
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
-    PD_TRY(allow_smem((k_residual_tile<0, false, true>), kResSmem));
-    PD_TRY(allow_smem(k_residual_tile<1>, kResSmem));
-    PD_TRY(allow_smem(k_residual_tile<2>, kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<0, false, 1>), kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<0, false, 2>), kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<1, false, 1>), kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<2, false, 2>), kResSmem));
     PD_TRY(allow_smem(k_residual_tile<0, true>, kResSmemUpd));
     PD_TRY(allow_smem(k_residual_tile<1, true>, kResSmemUpd));
     if (const char* f = std::getenv("PARADIAG_PIPELINE")) h->pipe = std::atoi(f) != 0;
