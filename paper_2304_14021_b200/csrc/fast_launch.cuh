@@ -75,6 +75,8 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 1>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<1, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_rows3<0, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_cols3<1, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<0, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<1, E, fast_col_warps(E), 2>), dtt3_cols_smem<E>());
@@ -112,8 +114,9 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
       const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
       // tune 256: pad the dynamic smem so only one CTA (4 warps) fits per SM (occupancy probe)
       const size_t smem = dtt3_rows_smem<E>() + ((L.tune & 256) ? 100 * 1024 : 0);
-      const bool gen = L.sin.n || L.sout.n || L.upd;
+      const bool gen = L.sin.n || L.sout.n;
       if (gen) k_rows3<NEUMANN, E, kFastRowWarps, 2><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+      else if (L.upd) k_rows3<NEUMANN, E, kFastRowWarps, 3><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
       else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
       else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)

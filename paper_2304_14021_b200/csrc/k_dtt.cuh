@@ -208,11 +208,13 @@ PD_DEV void update_line(const double* __restrict__ ob, double* __restrict__ U, i
 // Warps are independent: each takes P consecutive lines per step, prefetches its next group into
 // L2, stages the lines with cp.async, transforms and stores them coalesced.
 // V: 0 plain (no block I/O, no ‖·‖∞, no fused update), 1 with the ‖·‖∞ epilogue, 2 general
-// (runtime block maps / fused update / ‖·‖∞) — the common passes compile without the branches
+// (runtime block maps / fused update / ‖·‖∞), 3 the fused update (tune 16) — the common passes
+// compile without the branches
 template <int NEUMANN, int E, int NW, int V = 2>
 __global__ void __launch_bounds__(NW * 32, 2)
 k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
   constexpr bool GEN = V == 2;
+  constexpr bool UPD = V == 3 || GEN;             // V = 3: the fused update only
   using D = Dtt3<NEUMANN, E>;
   extern __shared__ double2 smem2[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -236,7 +238,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     if ((L.tune & 1) && lane == 0 && g + gstride < ngroups)
       bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
     // fused update: bring this group's U rows towards L2 now, they are read after the transform
-    if (GEN && L.upd && lane == 0)
+    if (UPD && L.upd && lane == 0)
       bulk_prefetch_l2(L.upd + L0 * L.nx, (size_t)nl * L.nx * sizeof(double), L.upd + L.nlines * L.nx);
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
@@ -269,7 +271,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
-        if (GEN && L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
+        if (UPD && L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
         else if (GEN && L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (GEN && L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (V == 1 || (GEN && L.amax)) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
@@ -278,8 +280,8 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     }
     __syncwarp();
   }
-  if (V == 1 || (GEN && L.amax)) warp_atomic_max_abs(L.amax, lmax);
-  if (GEN && L.upd) {
+  if (V == 1 || ((GEN || V == 3) && L.amax)) warp_atomic_max_abs(L.amax, lmax);
+  if (UPD && L.upd) {
     ubits = warp_max_u64(ubits);
     if (lane == 0 && ubits) atomicMax(L.umax, ubits);
   }
