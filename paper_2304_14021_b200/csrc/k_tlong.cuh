@@ -215,6 +215,7 @@ constexpr int kFbThreads = 2 * kFbPairs * 32;
 constexpr int kFbRowC = kFbPairs + 1;                 // staged row pitch (complex)
 constexpr size_t kFbSmem = (size_t)2 * 1024 * kFbRowC * sizeof(double2);   // 160 KB ≥ 8 × kWarpScratch
 
+template <bool PLAIN>      // PLAIN: θ = 1 and no λ₃ term, divisor d_k + μ
 __global__ void __launch_bounds__(kFbThreads, kFbPairs <= 2 ? 2 : 1)
 k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
   constexpr int L = 1024;
@@ -268,8 +269,14 @@ k_tl_b_fused(double2* __restrict__ Y, TlongParams Q) {
       const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
       const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
       const double2 d = __ldg(Q.T.dl + k);
-      const double2 Af = cmul(A, cinv_fast(shifted(d, Q.T.el, k, mua, Q.T.l3, lama)));
-      const double2 Bf = cmul(B, cinv_fast(shifted(d, Q.T.el, k, mub, Q.T.l3, lamb)));
+      double2 Af, Bf;
+      if (PLAIN) {
+        Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
+        Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
+      } else {
+        Af = cmul(A, cinv_fast(shifted(d, Q.T.el, k, mua, Q.T.l3, lama)));
+        Bf = cmul(B, cinv_fast(shifted(d, Q.T.el, k, mub, Q.T.l3, lamb)));
+      }
       v[r] = make_double2(Af.x - Bf.y, Af.y + Bf.x);
     }
   }

@@ -56,14 +56,18 @@ cudaError_t tlong_attrs() {
   if ((e = attrs_e<1>()) || (e = attrs_e<2>()) || (e = attrs_e<4>()) || (e = attrs_e<8>()) || (e = attrs_e<16>()) ||
       (e = attrs_e<32>()))
     return e;
-  return cudaFuncSetAttribute(k_tl_b_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
+  if ((e = cudaFuncSetAttribute(k_tl_b_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem)))
+    return e;
+  return cudaFuncSetAttribute(k_tl_b_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
 }
 
 bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s) {
   if (stage == 5) {                                     // fused B: Y in place (`out`)
     if (!tlong_fusable(Q)) return false;
     const int64_t nch4 = (Q.P + kFbPairs - 1) / kFbPairs;
-    k_tl_b_fused<<<(unsigned)(nch4 * (Q.N1 / 2)), kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
+    const unsigned grid = (unsigned)(nch4 * (Q.N1 / 2));
+    if (!Q.T.el && !Q.T.l3) k_tl_b_fused<true><<<grid, kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
+    else k_tl_b_fused<false><<<grid, kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
     return true;
   }
   if (stage == 2) {
