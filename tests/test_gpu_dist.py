@@ -80,6 +80,34 @@ def test_slab_entry_points_reject_bad_geometry(cuda_lib):
         cuda_lib.paradiag_init_slab(cuda_lib.make_problem(q), 0, 0, 0, 10, 0, 10)
 
 
+def test_block_maps_and_ranges_reject_bad_arguments(cuda_lib):
+    """Transpose-block maps must tile the line in order (≤ 8 blocks); slice ranges must lie in
+    [0, nt); the y-range stage must be 0, 1 or 2."""
+    import torch
+    p = CASES["c5_m64_nt64"]
+    n = p.n
+    h = cuda_lib.paradiag_init_slab(cuda_lib.make_problem(p), 0, 0, 0, n, 0, n)
+    try:
+        a = torch.zeros(p.nt * n * n, dtype=torch.float64, device="cuda")
+        b = torch.zeros_like(a)
+        good = [(0, 40, 0), (40, n - 40, p.nt * n * 40)]
+        cuda_lib.paradiag_slab_xpass_seg(h, a, b, False, None, good)                 # accepted
+        for bad in ([(0, 40, 0), (41, n - 41, 0)],                                     # gap
+                    [(0, 40, 0), (40, n - 41, 0)],                                     # does not cover
+                    [(0, 40, 0), (40, 10, 0)] + [(50 + i, 1, 0) for i in range(7)] + [(57, n - 57, 0)]):  # > 8
+            with pytest.raises(cuda_lib.ParadiagError):
+                cuda_lib.paradiag_slab_xpass_seg(h, a, b, False, None, bad)
+        with pytest.raises(cuda_lib.ParadiagError):
+            cuda_lib.paradiag_slab_xrange(h, a, b, False, None, None, p.nt - 1, 2)      # past nt
+        with pytest.raises(cuda_lib.ParadiagError):
+            cuda_lib.paradiag_slab_yrange(h, a, b, a, 3, None, 0, 1)                   # unknown stage
+        with pytest.raises(cuda_lib.ParadiagError):
+            cuda_lib.paradiag_slab_update_range(h, a, b, -1, 1)
+        torch.cuda.synchronize()
+    finally:
+        cuda_lib.paradiag_destroy(h)
+
+
 def _ipc_child(handle, off, n, q):
     import torch
     import paper_2304_14021_b200 as pd
