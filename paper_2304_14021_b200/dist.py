@@ -257,7 +257,8 @@ class SlabRank:
     """State and phases of one rank.  ``iterate`` runs one defect-correction iteration
     U ← U + P_α⁻¹(b − K U) on the rank's row slab."""
 
-    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True, chunks: int = 1, p2p: bool = False):
+    def __init__(self, layout: SlabLayout, rank: int, ops, fused: bool = True, chunks: int = 1, p2p: bool = False,
+                 self_via_comm: bool = False):
         """fused: the x / y passes read and write the all-to-all buffers through the block maps
         (no pack / unpack copies); False: the copy-based reference orchestration.
         chunks > 1 (fused only): the time slices are cut into that many ranges, each with its own
@@ -291,19 +292,23 @@ class SlabRank:
             # peer blocks.  Blocks of a range are [nn][rows][cols] (range-relative addressing).
             cum = lambda sp: [sum(sp[:i]) for i in range(P)]
             regions, base = [], 0
+            # self_via_comm (test hook): the kept block also travels through the collective, so a
+            # one-rank NCCL run exercises the asynchronous all-to-all and its stream ordering
+            keep = not self_via_comm
             for n0, nn in self.ranges:
-                fs = [0 if q == r else nn * self.nyl * layout.cols[q][1] for q in range(P)]   # fwd send / bwd recv
-                fr = [0 if q == r else nn * layout.rows[q][1] * self.nxl for q in range(P)]  # fwd recv / bwd send
+                fs = [0 if (q == r and keep) else nn * self.nyl * layout.cols[q][1] for q in range(P)]   # fwd send / bwd recv
+                fr = [0 if (q == r and keep) else nn * layout.rows[q][1] * self.nxl for q in range(P)]  # fwd recv / bwd send
                 ns = max(sum(fs), sum(fr))
                 so = base + 2 * ns                                              # the self block
                 cfs, cfr = cum(fs), cum(fr)
+                own = lambda q: q == r and keep
                 regions.append(dict(
                     n0=n0, nn=nn, base=base, ns=ns, splits={"fwd": (fs, fr), "bwd": (fr, fs)},
-                    xm_out=[(x0, c, so if q == r else base + cfs[q]) for q, (x0, c) in enumerate(layout.cols)],
-                    ym_in=[(y0, c, so if q == r else base + ns + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
-                    ym_out=[(y0, c, so if q == r else base + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
-                    xm_in=[(x0, c, so if q == r else base + ns + cfs[q]) for q, (x0, c) in enumerate(layout.cols)]))
-                base = so + nn * self.nyl * self.nxl
+                    xm_out=[(x0, c, so if own(q) else base + cfs[q]) for q, (x0, c) in enumerate(layout.cols)],
+                    ym_in=[(y0, c, so if own(q) else base + ns + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
+                    ym_out=[(y0, c, so if own(q) else base + cfr[q]) for q, (y0, c) in enumerate(layout.rows)],
+                    xm_in=[(x0, c, so if own(q) else base + ns + cfs[q]) for q, (x0, c) in enumerate(layout.cols)]))
+                base = so + (nn * self.nyl * self.nxl if keep else 0)
             self.buf = ops.empty(base)
             for g in regions:
                 g["send"] = self.buf[g["base"]:g["base"] + g["ns"]]

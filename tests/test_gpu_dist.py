@@ -150,3 +150,58 @@ def test_ipc_export_and_map(cuda_lib):
     torch.cuda.synchronize()
     assert torch.equal(t.cpu(), torch.arange(512, dtype=torch.float64) + 0.5)
     assert float(pool[:1000].abs().max()) == 0.0 and float(pool[1512:].abs().max()) == 0.0
+
+
+def _nccl_world1(chunks, out_q):
+    import os
+    import socket
+    import torch
+    import torch.distributed as tdist
+    from paper_2304_14021_b200 import dist
+    import paper_2304_14021_b200 as pd
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    try:
+        p = CASES["c5_m64_nt64"]
+        u0 = make_u0(p)
+        U0 = iterate.initial_iterate(p, u0)
+        L = dist.SlabLayout(p.n, p.nt, 1)
+        stream = torch.cuda.current_stream()
+        ops = dist.GpuOps(p, 0, stream.cuda_stream, 0, p.n, 0, p.n)
+        rk = dist.SlabRank(L, 0, ops, fused=True, chunks=chunks, self_via_comm=True)
+        comm = dist.TorchComm()
+        U = to_dev(U0, p).reshape(-1).clone()
+        u0d = to_dev(u0)
+        s = pd.Solver(p)
+        Ur = to_dev(U0, p)
+        info = None
+        errs = []
+        for _ in range(3):
+            rk.iterate(u0d, U, comm)
+            info = s.iterate(u0d, Ur, info)
+            errs.append(rel_err(U.reshape(Ur.shape).cpu().numpy(), Ur.cpu().numpy()))
+        ops.close()
+        out_q.put(errs)
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_nccl_async_transposes_world1(cuda_lib, chunks):
+    """A one-rank NCCL world where the kept block also goes through the (asynchronous, per slice
+    range) all-to-all: the real collective's stream ordering against the library's kernels, checked
+    against the unsharded iteration.  One process, one device."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_world1, args=(chunks, q))
+    pr.start()
+    errs = q.get(timeout=600)
+    pr.join(timeout=600)
+    assert pr.exitcode == 0
+    assert max(errs) <= 5e-11, errs
