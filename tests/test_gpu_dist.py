@@ -152,7 +152,7 @@ def test_ipc_export_and_map(cuda_lib):
     assert float(pool[:1000].abs().max()) == 0.0 and float(pool[1512:].abs().max()) == 0.0
 
 
-def _nccl_world1(chunks, out_q):
+def _nccl_world1(chunks, out_q, p2p=False):
     import os
     import socket
     import torch
@@ -173,8 +173,10 @@ def _nccl_world1(chunks, out_q):
         L = dist.SlabLayout(p.n, p.nt, 1)
         stream = torch.cuda.current_stream()
         ops = dist.GpuOps(p, 0, stream.cuda_stream, 0, p.n, 0, p.n)
-        rk = dist.SlabRank(L, 0, ops, fused=True, chunks=chunks, self_via_comm=True)
+        rk = dist.SlabRank(L, 0, ops, fused=True, chunks=chunks, self_via_comm=not p2p, p2p=p2p)
         comm = dist.TorchComm()
+        if p2p:
+            rk.setup_p2p(comm)            # IPC export + all_gather of the handle, NCCL fences
         U = to_dev(U0, p).reshape(-1).clone()
         u0d = to_dev(u0)
         s = pd.Solver(p)
@@ -191,15 +193,15 @@ def _nccl_world1(chunks, out_q):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunks", [1, 3])
-def test_nccl_async_transposes_world1(cuda_lib, chunks):
+@pytest.mark.parametrize("chunks,p2p", [(1, False), (3, False), (1, True)], ids=["nccl", "nccl-3ranges", "p2p"])
+def test_nccl_async_transposes_world1(cuda_lib, chunks, p2p):
     """A one-rank NCCL world where the kept block also goes through the (asynchronous, per slice
     range) all-to-all: the real collective's stream ordering against the library's kernels, checked
     against the unsharded iteration.  One process, one device."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    pr = ctx.Process(target=_nccl_world1, args=(chunks, q))
+    pr = ctx.Process(target=_nccl_world1, args=(chunks, q, p2p))
     pr.start()
     errs = q.get(timeout=600)
     pr.join(timeout=600)
