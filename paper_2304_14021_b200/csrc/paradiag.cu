@@ -336,7 +336,7 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
       if (dU && h->P.theta != 1.0)
         k_residual_tile<1, true><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
       else if (dU)
-        k_residual_tile<0, true><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
+        k_residual_tile<0, true, 1><<<grd, kResThreads, kResSmemUpd, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.kind == PD_CAHN_HILLIARD_EYRE)
         k_residual_tile<2, false, 2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.theta != 1.0)
@@ -1278,6 +1278,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(allow_smem((k_residual_tile<1, false, 1>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<2, false, 2>), kResSmem));
     PD_TRY(allow_smem(k_residual_tile<0, true>, kResSmemUpd));
+    PD_TRY(allow_smem((k_residual_tile<0, true, 1>), kResSmemUpd));
     PD_TRY(allow_smem(k_residual_tile<1, true>, kResSmemUpd));
     if (const char* f = std::getenv("PARADIAG_PIPELINE")) h->pipe = std::atoi(f) != 0;
     if (can_pipeline(h)) {              // the pipelined solve's second iterate / workspace buffers
