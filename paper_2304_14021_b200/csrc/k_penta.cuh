@@ -233,4 +233,130 @@ __global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ 
   }
 }
 
+// ---- one CTA per bin (short lines, n ≤ kPentaCtaMaxN): the bin's factors, right-hand side and
+// iterate live in shared memory, so the two sequential LU sweeps run at shared-memory latency
+// (one thread; they are recurrences), while the nested residual, the update and the convergence
+// test of every refinement step run row-parallel over the CTA.  Same arithmetic, same stop rule
+// as k_penta_solve.  c2 (n = 1024, 129 bins): 5.2 → see DESIGN.md §5.
+constexpr int kPentaCtaThreads = 256;
+constexpr int kPentaCtaMaxN = 1920;                    // 7 complex arrays × n × 16 B ≤ 210 KB
+inline size_t penta_cta_smem(int n) { return (size_t)7 * n * sizeof(double2); }
+
+PD_DEV double2 ghost_s(const double2* v, int i, int n, int neumann) {
+  if (i < 0 || i >= n) {
+    if (!neumann) return make_double2(0.0, 0.0);
+    i = i < 0 ? -i : 2 * (n - 1) - i;
+  }
+  return v[i];
+}
+
+__global__ void __launch_bounds__(kPentaCtaThreads)
+k_penta_solve_cta(double2* __restrict__ spec, PentaParams P) {
+  extern __shared__ double2 ps[];
+  const int l = blockIdx.x, n = P.n, nb = P.nb, tid = threadIdx.x;
+  double2* s_ = ps;                 // right-hand side ŝ
+  double2* x_ = ps + n;             // iterate
+  double2* w_ = ps + 2 * n;         // residual / correction
+  double2* L1 = ps + 3 * n;
+  double2* L2 = ps + 4 * n;
+  double2* U1 = ps + 5 * n;
+  double2* IU = ps + 6 * n;
+  __shared__ double red[2][kPentaCtaThreads / 32];
+  __shared__ int stop;
+  for (int i = tid; i < n; i += kPentaCtaThreads) {
+    const size_t o = (size_t)i * nb + l;
+    const double2 v = spec[o];
+    s_[i] = v;
+    x_[i] = v;
+    L1[i] = P.l1[o];
+    L2[i] = P.l2[o];
+    U1[i] = P.u1[o];
+    IU[i] = P.iu0[o];
+  }
+  __syncthreads();
+  const double2 d = P.dl[l];
+  const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
+  const double* __restrict__ c2 = P.band + 4 * n;
+  auto lu = [&](double2* v) {                         // one thread: the recurrences
+    if (tid == 0) {
+      double2 y1 = {0, 0}, y2 = {0, 0};
+      for (int i = 0; i < n; ++i) {
+        double2 y = v[i];
+        y = csub(y, cmul(L1[i], y1));
+        y = csub(y, cmul(L2[i], y2));
+        v[i] = y;
+        y2 = y1; y1 = y;
+      }
+      double2 x1 = {0, 0}, x2 = {0, 0};
+      for (int i = n - 1; i >= 0; --i) {
+        double2 x = v[i];
+        x = csub(x, cmul(U1[i], x1));
+        x = csub(x, cscale(cmul(e, x2), __ldg(c2 + i)));
+        x = cmul(x, IU[i]);
+        v[i] = x;
+        x2 = x1; x1 = x;
+      }
+    }
+    __syncthreads();
+  };
+  auto lapx = [&](int i) {                            // L x at i (x with the BC's ghost rule)
+    const double2 xm = ghost_s(x_, i - 1, n, P.neumann), xc = ghost_s(x_, i, n, P.neumann),
+                  xp = ghost_s(x_, i + 1, n, P.neumann);
+    return make_double2(((xm.x + xp.x) - 2.0 * xc.x) * P.inv_h2, ((xm.y + xp.y) - 2.0 * xc.y) * P.inv_h2);
+  };
+  auto lapg = [&](int i) {                            // L x at a possibly-ghost position
+    if (i < 0 || i >= n) {
+      if (!P.neumann) return make_double2(0.0, 0.0);
+      i = i < 0 ? -i : 2 * (n - 1) - i;
+    }
+    return lapx(i);
+  };
+  lu(x_);
+  for (int it = 0; it < kPentaRefine; ++it) {
+    // ρ = s - (d x + A x), A x nested (R#15): ((L_{i-1} + L_{i+1}) - 2 L_i) / h², row-parallel
+    for (int i = tid; i < n; i += kPentaCtaThreads) {
+      const double2 lc = lapx(i), lm = lapg(i - 1), lp = lapg(i + 1);
+      const double2 ll = make_double2(((lm.x + lp.x) - 2.0 * lc.x) * P.inv_h2, ((lm.y + lp.y) - 2.0 * lc.y) * P.inv_h2);
+      double2 Ax;
+      if (P.kind == 0) Ax = ll;
+      else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
+      const double2 x = x_[i], sv = s_[i];
+      const double2 dx = cmul(d, x);
+      const double2 eAx = P.el ? cmul(e, Ax) : Ax;
+      w_[i] = make_double2(sv.x - (dx.x + eAx.x), sv.y - (dx.y + eAx.y));
+    }
+    __syncthreads();
+    lu(w_);
+    double cmax = 0.0, xmax = 0.0;
+    for (int i = tid; i < n; i += kPentaCtaThreads) {
+      const double2 c = w_[i];
+      const double2 x = cadd(x_[i], c);
+      x_[i] = x;
+      cmax = fmax(cmax, fmax(fabs(c.x), fabs(c.y)));
+      xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    }
+    if ((tid & 31) == 0) {
+      red[0][tid >> 5] = cmax;
+      red[1][tid >> 5] = xmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double c = 0.0, x = 0.0;
+      for (int w = 0; w < kPentaCtaThreads / 32; ++w) {
+        c = fmax(c, red[0][w]);
+        x = fmax(x, red[1][w]);
+      }
+      stop = !(c > 1e-15 * x);
+    }
+    __syncthreads();
+    if (stop) break;
+  }
+  for (int i = tid; i < n; i += kPentaCtaThreads) spec[(size_t)i * nb + l] = x_[i];
+}
+
 }  // namespace pd

@@ -155,6 +155,7 @@ struct pd_handle {
   // Gram-Schmidt passes per Arnoldi step: 1 (measured c4t 3.3 s vs 4.7 s with 2, same counts and
   // parity; convergence is only ever declared on the recomputed true residual); PARADIAG_CGS_PASSES=2
   int cgs_passes = 1;
+  bool penta_cta = true;              // PARADIAG_PENTA=0: the thread-per-bin pentadiagonal kernel
   // device-side window loop (paradiag_solve): graph of a conditional WHILE node around one
   // iteration, captured for one U pointer; PARADIAG_GRAPH=0 keeps the host loop
   bool use_graph = true;
@@ -571,7 +572,10 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   const size_t nf = (size_t)h->nx * h->nb;
   PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
   prof_begin(h, K_PENTA);
-  k_penta_solve<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(h->spec, h->w1, h->w2, PP);
+  if (h->nx <= kPentaCtaMaxN && h->penta_cta)        // one CTA per bin, everything in shared memory
+    k_penta_solve_cta<<<h->nb, kPentaCtaThreads, penta_cta_smem(h->nx), h->stream>>>(h->spec, PP);
+  else
+    k_penta_solve<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(h->spec, h->w1, h->w2, PP);
   prof_end(h, K_PENTA);
   PD_LAUNCHED();
   T.amax = dmax;
@@ -1248,6 +1252,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl; PP.el = h->el;
     PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
     k_penta_factor<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(PP);
+    if (const char* f = std::getenv("PARADIAG_PENTA")) h->penta_cta = std::atoi(f) != 0;
+    if (n <= kPentaCtaMaxN) PD_TRY(allow_smem(k_penta_solve_cta, penta_cta_smem(n)));
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(PD_ECUDA, "penta factor launch"));
     if (time_smem(nt, kTime1DWarps) <= kSmemMax) {
       PD_TRY(allow_smem(k_time_fwd_1d<kTime1DWarps>, time_smem(nt, kTime1DWarps)));
