@@ -18,6 +18,7 @@ struct PentaParams {
   const double2* dl;     // d_l
   const double2* el;     // e_l (NULL: θ = 1, e_l = 1)
   double2 *l1, *l2, *iu0, *u1;   // factors [n][nb]
+  int refine;            // refinement cap (kPentaRefine; PARADIAG_PENTA_REFINE for A/B)
 };
 
 // LU factorisation of d_l I + A (no pivoting), one thread per bin.  Done once at init.
@@ -128,9 +129,18 @@ PD_DEV double2 ghost(const double2* v, int i, int l, const PentaParams& P) {
 
 // spec (in: ŝ, out: x), w1, w2 scratch [n][nb].  Refinement repeats (at most kPentaRefine times)
 // until the correction is below 1e-15 of the iterate, per bin — the oracle's criterion (SURVEY
-// §8(c) step 3.3).  One step suffices for c1/c2 (probe p10: 2.6e-7 → 1.8e-12); the condition
-// number grows like m⁴, so longer lines (m = 8191: cond ≈ 1e14) need two or three.
+// §8(c) step 3.3) — or stops shrinking: a correction that is not at most half the previous one
+// is rounding noise of the residual (the floor sits near cond·ε, above 1e-15 for c2), and further
+// steps only stir it (measured: all six steps ran on c2, 0.71 ms of 0.81 per iteration).  One
+// step suffices for c1/c2 (probe p10: 2.6e-7 → 1.8e-12); the condition number grows like m⁴, so
+// longer lines (m = 8191: cond ≈ 1e14) need two or three.
 constexpr int kPentaRefine = 6;
+PD_DEV bool penta_refine_done(double cmax, double xmax, double& rprev) {
+  const double r = cmax / xmax;
+  const bool done = !(cmax > 1e-15 * xmax) || r > 0.5 * rprev;
+  rprev = r;
+  return done;
+}
 
 __global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ w1, double2* __restrict__ w2,
                               PentaParams P) {
@@ -151,7 +161,8 @@ __global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ 
       if (i0 + k < n) w1[(size_t)(i0 + k) * nb + l] = t[k];
   }
   penta_lu_solve(w1, l, P);
-  for (int it = 0; it < kPentaRefine; ++it) {
+  double rprev = INFINITY;
+  for (int it = 0; it < P.refine; ++it) {
     // ρ = s - (d x + A x) into w2, A x in nested form from a sliding window of x values:
     // L x at i uses x_{i-1}, x_i, x_{i+1}; A x at i uses L x at i-1, i, i+1 (ghost rules of the BC)
     auto lap = [&](double2 xm, double2 xc, double2 xp) {
@@ -220,7 +231,7 @@ __global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ 
           xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
         }
     }
-    if (!(cmax > 1e-15 * xmax)) break;
+    if (penta_refine_done(cmax, xmax, rprev)) break;
   }
   for (int i0 = 0; i0 < n; i0 += K) {
     double2 t[K];
@@ -234,68 +245,145 @@ __global__ void k_penta_solve(double2* __restrict__ spec, double2* __restrict__ 
 }
 
 // ---- one CTA per bin (short lines, n ≤ kPentaCtaMaxN): the bin's factors, right-hand side and
-// iterate live in shared memory, so the two sequential LU sweeps run at shared-memory latency
-// (one thread; they are recurrences), while the nested residual, the update and the convergence
-// test of every refinement step run row-parallel over the CTA.  Same arithmetic, same stop rule
-// as k_penta_solve.  c2 (n = 1024, 129 bins): 5.2 → see DESIGN.md §5.
+// iterate live in shared memory; the nested residual, the update and the convergence test of
+// every refinement step run row-parallel over the CTA, and the two LU sweeps (order-2 linear
+// recurrences) run on warp 0 split into 32 row chunks:
+//   pass 1  every lane runs its chunk three times side by side — the particular solution from a
+//           zero entry state and the two homogeneous solutions from the unit entry states — which
+//           gives the chunk's affine transfer map  S_out = p + S_in,1 · h + S_in,2 · g;
+//   combine lane 0 chains the 32 maps (32 short steps instead of n) into every chunk's entry state;
+//   pass 2  every lane re-runs its chunk from the exact entry state with the sequential sweep's
+//           arithmetic, writing the result.
+// The refinement that follows absorbs the (rounding-level) difference to the sequential sweep.
+// Shared arrays are padded (index i + i/32) so the lanes' chunk-strided rows hit distinct banks.
+// Same stop rule as k_penta_solve.
 constexpr int kPentaCtaThreads = 256;
-constexpr int kPentaCtaMaxN = 1920;                    // 7 complex arrays × n × 16 B ≤ 210 KB
-inline size_t penta_cta_smem(int n) { return (size_t)7 * n * sizeof(double2); }
+constexpr int kPentaCtaMaxN = 1920;
+__host__ __device__ inline int pidx(int i) { return i + (i >> 5); }
+inline size_t penta_cta_smem(int n) { return (size_t)7 * (pidx(n) + 1) * sizeof(double2); }
+
+PD_DEV double2 cneg(double2 a) { return make_double2(-a.x, -a.y); }
+
+// forward sweep y_i = (v_i - l1_i y_{i-1}) - l2_i y_{i-2} in place (warp 0)
+PD_DEV void penta_fwd_warp(double2* v, const double2* L1, const double2* L2, int n, int lane, double2 (*mp)[6],
+                           double2 (*st)[2]) {
+  const int C = (n + 31) >> 5, a = lane * C, b = min(n, a + C);
+  const double2 z = make_double2(0.0, 0.0), o = make_double2(1.0, 0.0);
+  double2 p1 = z, p2 = z, h1 = o, h2 = z, g1 = z, g2 = o;     // (state_{i-1}, state_{i-2})
+  for (int i = a; i < b; ++i) {
+    const int q = pidx(i);
+    const double2 l1 = L1[q], l2 = L2[q];
+    const double2 yp = csub(csub(v[q], cmul(l1, p1)), cmul(l2, p2));
+    const double2 yh = cneg(cadd(cmul(l1, h1), cmul(l2, h2)));
+    const double2 yg = cneg(cadd(cmul(l1, g1), cmul(l2, g2)));
+    p2 = p1; p1 = yp; h2 = h1; h1 = yh; g2 = g1; g1 = yg;
+  }
+  mp[lane][0] = p1; mp[lane][1] = p2; mp[lane][2] = h1; mp[lane][3] = h2; mp[lane][4] = g1; mp[lane][5] = g2;
+  __syncwarp();
+  if (lane == 0) {
+    double2 s1 = z, s2 = z;                                   // y_{-1} = y_{-2} = 0
+    for (int k = 0; k < 32; ++k) {
+      st[k][0] = s1; st[k][1] = s2;
+      const double2 o1 = cadd(mp[k][0], cadd(cmul(s1, mp[k][2]), cmul(s2, mp[k][4])));
+      const double2 o2 = cadd(mp[k][1], cadd(cmul(s1, mp[k][3]), cmul(s2, mp[k][5])));
+      s1 = o1; s2 = o2;
+    }
+  }
+  __syncwarp();
+  double2 y1 = st[lane][0], y2 = st[lane][1];
+  for (int i = a; i < b; ++i) {
+    const int q = pidx(i);
+    double2 y = v[q];
+    y = csub(y, cmul(L1[q], y1));
+    y = csub(y, cmul(L2[q], y2));
+    v[q] = y;
+    y2 = y1; y1 = y;
+  }
+  __syncwarp();
+}
+
+// backward sweep x_i = ((y_i - u1_i x_{i+1}) - c2_i e x_{i+2}) / u0_i in place (warp 0)
+PD_DEV void penta_bwd_warp(double2* v, const double2* U1, const double2* IU, const double* __restrict__ c2, double2 e,
+                           int n, int lane, double2 (*mp)[6], double2 (*st)[2]) {
+  const int C = (n + 31) >> 5, a = lane * C, b = min(n, a + C);
+  const double2 z = make_double2(0.0, 0.0), o = make_double2(1.0, 0.0);
+  double2 p1 = z, p2 = z, h1 = o, h2 = z, g1 = z, g2 = o;     // (state_{i+1}, state_{i+2})
+  for (int i = b - 1; i >= a; --i) {
+    const int q = pidx(i);
+    const double2 u1 = U1[q], iu = IU[q];
+    const double c = __ldg(c2 + i);
+    const double2 xp = cmul(csub(csub(v[q], cmul(u1, p1)), cscale(cmul(e, p2), c)), iu);
+    const double2 xh = cmul(cneg(cadd(cmul(u1, h1), cscale(cmul(e, h2), c))), iu);
+    const double2 xg = cmul(cneg(cadd(cmul(u1, g1), cscale(cmul(e, g2), c))), iu);
+    p2 = p1; p1 = xp; h2 = h1; h1 = xh; g2 = g1; g1 = xg;
+  }
+  mp[lane][0] = p1; mp[lane][1] = p2; mp[lane][2] = h1; mp[lane][3] = h2; mp[lane][4] = g1; mp[lane][5] = g2;
+  __syncwarp();
+  if (lane == 0) {
+    double2 s1 = z, s2 = z;                                   // x_n = x_{n+1} = 0
+    for (int k = 31; k >= 0; --k) {
+      st[k][0] = s1; st[k][1] = s2;
+      const double2 o1 = cadd(mp[k][0], cadd(cmul(s1, mp[k][2]), cmul(s2, mp[k][4])));
+      const double2 o2 = cadd(mp[k][1], cadd(cmul(s1, mp[k][3]), cmul(s2, mp[k][5])));
+      s1 = o1; s2 = o2;
+    }
+  }
+  __syncwarp();
+  double2 x1 = st[lane][0], x2 = st[lane][1];
+  for (int i = b - 1; i >= a; --i) {
+    const int q = pidx(i);
+    double2 x = v[q];
+    x = csub(x, cmul(U1[q], x1));
+    x = csub(x, cscale(cmul(e, x2), __ldg(c2 + i)));
+    x = cmul(x, IU[q]);
+    v[q] = x;
+    x2 = x1; x1 = x;
+  }
+  __syncwarp();
+}
 
 PD_DEV double2 ghost_s(const double2* v, int i, int n, int neumann) {
   if (i < 0 || i >= n) {
     if (!neumann) return make_double2(0.0, 0.0);
     i = i < 0 ? -i : 2 * (n - 1) - i;
   }
-  return v[i];
+  return v[pidx(i)];
 }
 
 __global__ void __launch_bounds__(kPentaCtaThreads)
 k_penta_solve_cta(double2* __restrict__ spec, PentaParams P) {
   extern __shared__ double2 ps[];
-  const int l = blockIdx.x, n = P.n, nb = P.nb, tid = threadIdx.x;
+  const int l = blockIdx.x, n = P.n, nb = P.nb, tid = threadIdx.x, lane = tid & 31;
+  const int ld = pidx(n) + 1;
   double2* s_ = ps;                 // right-hand side ŝ
-  double2* x_ = ps + n;             // iterate
-  double2* w_ = ps + 2 * n;         // residual / correction
-  double2* L1 = ps + 3 * n;
-  double2* L2 = ps + 4 * n;
-  double2* U1 = ps + 5 * n;
-  double2* IU = ps + 6 * n;
+  double2* x_ = ps + ld;            // iterate
+  double2* w_ = ps + 2 * ld;        // residual / correction
+  double2* L1 = ps + 3 * ld;
+  double2* L2 = ps + 4 * ld;
+  double2* U1 = ps + 5 * ld;
+  double2* IU = ps + 6 * ld;
+  __shared__ double2 mp[32][6], st[32][2];
   __shared__ double red[2][kPentaCtaThreads / 32];
   __shared__ int stop;
   for (int i = tid; i < n; i += kPentaCtaThreads) {
     const size_t o = (size_t)i * nb + l;
+    const int q = pidx(i);
     const double2 v = spec[o];
-    s_[i] = v;
-    x_[i] = v;
-    L1[i] = P.l1[o];
-    L2[i] = P.l2[o];
-    U1[i] = P.u1[o];
-    IU[i] = P.iu0[o];
+    s_[q] = v;
+    x_[q] = v;
+    L1[q] = P.l1[o];
+    L2[q] = P.l2[o];
+    U1[q] = P.u1[o];
+    IU[q] = P.iu0[o];
   }
   __syncthreads();
   const double2 d = P.dl[l];
   const double2 e = P.el ? P.el[l] : make_double2(1.0, 0.0);
   const double* __restrict__ c2 = P.band + 4 * n;
-  auto lu = [&](double2* v) {                         // one thread: the recurrences
-    if (tid == 0) {
-      double2 y1 = {0, 0}, y2 = {0, 0};
-      for (int i = 0; i < n; ++i) {
-        double2 y = v[i];
-        y = csub(y, cmul(L1[i], y1));
-        y = csub(y, cmul(L2[i], y2));
-        v[i] = y;
-        y2 = y1; y1 = y;
-      }
-      double2 x1 = {0, 0}, x2 = {0, 0};
-      for (int i = n - 1; i >= 0; --i) {
-        double2 x = v[i];
-        x = csub(x, cmul(U1[i], x1));
-        x = csub(x, cscale(cmul(e, x2), __ldg(c2 + i)));
-        x = cmul(x, IU[i]);
-        v[i] = x;
-        x2 = x1; x1 = x;
-      }
+  auto lu = [&](double2* v) {
+    if (tid < 32) {
+      penta_fwd_warp(v, L1, L2, n, lane, mp, st);
+      penta_bwd_warp(v, U1, IU, c2, e, n, lane, mp, st);
     }
     __syncthreads();
   };
@@ -312,26 +400,29 @@ k_penta_solve_cta(double2* __restrict__ spec, PentaParams P) {
     return lapx(i);
   };
   lu(x_);
-  for (int it = 0; it < kPentaRefine; ++it) {
+  double rprev = INFINITY;                            // thread 0's stagnation state
+  for (int it = 0; it < P.refine; ++it) {
     // ρ = s - (d x + A x), A x nested (R#15): ((L_{i-1} + L_{i+1}) - 2 L_i) / h², row-parallel
     for (int i = tid; i < n; i += kPentaCtaThreads) {
+      const int q = pidx(i);
       const double2 lc = lapx(i), lm = lapg(i - 1), lp = lapg(i + 1);
       const double2 ll = make_double2(((lm.x + lp.x) - 2.0 * lc.x) * P.inv_h2, ((lm.y + lp.y) - 2.0 * lc.y) * P.inv_h2);
       double2 Ax;
       if (P.kind == 0) Ax = ll;
       else Ax = make_double2(P.b2 * lc.x + P.e2 * ll.x, P.b2 * lc.y + P.e2 * ll.y);
-      const double2 x = x_[i], sv = s_[i];
+      const double2 x = x_[q], sv = s_[q];
       const double2 dx = cmul(d, x);
       const double2 eAx = P.el ? cmul(e, Ax) : Ax;
-      w_[i] = make_double2(sv.x - (dx.x + eAx.x), sv.y - (dx.y + eAx.y));
+      w_[q] = make_double2(sv.x - (dx.x + eAx.x), sv.y - (dx.y + eAx.y));
     }
     __syncthreads();
     lu(w_);
     double cmax = 0.0, xmax = 0.0;
     for (int i = tid; i < n; i += kPentaCtaThreads) {
-      const double2 c = w_[i];
-      const double2 x = cadd(x_[i], c);
-      x_[i] = x;
+      const int q = pidx(i);
+      const double2 c = w_[q];
+      const double2 x = cadd(x_[q], c);
+      x_[q] = x;
       cmax = fmax(cmax, fmax(fabs(c.x), fabs(c.y)));
       xmax = fmax(xmax, fmax(fabs(x.x), fabs(x.y)));
     }
@@ -351,12 +442,12 @@ k_penta_solve_cta(double2* __restrict__ spec, PentaParams P) {
         c = fmax(c, red[0][w]);
         x = fmax(x, red[1][w]);
       }
-      stop = !(c > 1e-15 * x);
+      stop = penta_refine_done(c, x, rprev);
     }
     __syncthreads();
     if (stop) break;
   }
-  for (int i = tid; i < n; i += kPentaCtaThreads) spec[(size_t)i * nb + l] = x_[i];
+  for (int i = tid; i < n; i += kPentaCtaThreads) spec[(size_t)i * nb + l] = x_[pidx(i)];
 }
 
 }  // namespace pd

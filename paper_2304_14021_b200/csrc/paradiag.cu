@@ -156,6 +156,7 @@ struct pd_handle {
   // parity; convergence is only ever declared on the recomputed true residual); PARADIAG_CGS_PASSES=2
   int cgs_passes = 1;
   bool penta_cta = true;              // PARADIAG_PENTA=0: the thread-per-bin pentadiagonal kernel
+  int penta_refine = kPentaRefine;    // PARADIAG_PENTA_REFINE: refinement cap (A/B only)
   // device-side window loop (paradiag_solve): graph of a conditional WHILE node around one
   // iteration, captured for one U pointer; PARADIAG_GRAPH=0 keeps the host loop
   bool use_graph = true;
@@ -571,6 +572,7 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
   PP.inv_h2 = h->inv_h2; PP.b2 = h->b2; PP.e2 = h->e2; PP.band = h->band; PP.dl = h->dl; PP.el = h->el;
   const size_t nf = (size_t)h->nx * h->nb;
   PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
+  PP.refine = h->penta_refine;
   prof_begin(h, K_PENTA);
   if (h->nx <= kPentaCtaMaxN && h->penta_cta)        // one CTA per bin, everything in shared memory
     k_penta_solve_cta<<<h->nb, kPentaCtaThreads, penta_cta_smem(h->nx), h->stream>>>(h->spec, PP);
@@ -1253,6 +1255,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PP.l1 = h->fac; PP.l2 = h->fac + nf; PP.iu0 = h->fac + 2 * nf; PP.u1 = h->fac + 3 * nf;
     k_penta_factor<<<(h->nb + 63) / 64, 64, 0, h->stream>>>(PP);
     if (const char* f = std::getenv("PARADIAG_PENTA")) h->penta_cta = std::atoi(f) != 0;
+    if (const char* f = std::getenv("PARADIAG_PENTA_REFINE")) h->penta_refine = std::atoi(f);
     if (n <= kPentaCtaMaxN) PD_TRY(allow_smem(k_penta_solve_cta, penta_cta_smem(n)));
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(PD_ECUDA, "penta factor launch"));
     if (time_smem(nt, kTime1DWarps) <= kSmemMax) {
