@@ -47,7 +47,7 @@ struct Dtt3 {
   PD_DEV static int opos(int q) { return q + (q >> 6); }
 
   // Transform the P lines held in xb (line p at p*LDX, buffer index 0..M, hinged ends zero) and
-  // leave the outputs in xb at p*LDO + opos(stored index).  trig[j] = (cos, sin)(πj/M), j ≤ M;
+  // leave the outputs in xb at p*LDO + opos(stored index).  L.trigs / L.trigc: sin / cos pairs;
   // trig2 = (cos, sin)(2πk/M) stored at [j*E + b] for k = 32b + j.
   // g scales every output (the Γ_α / Γ_α⁻¹·normalisation factor of the line's time slice when the
   // y passes carry it for the time pass; 1 otherwise) at no extra arithmetic.
@@ -64,9 +64,12 @@ struct Dtt3 {
         const int n = lane + 32 * e, j0 = 2 * n;
         const double2 a = *reinterpret_cast<const double2*>(x + j0);   // x_{2n}, x_{2n+1}
         const double m0 = x[M - j0], m1 = x[M - j0 - 1];
-        const double2 t0 = __ldg(L.trig + j0), t1 = __ldg(L.trig + j0 + 1);
-        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, t0.y), ymap<NEUMANN>(a.y, m1, t1.y));
-        if (NEUMANN) acc = fma(a.x - m0, t0.x, fma(a.y - m1, t1.x, acc));
+        const double2 sn = __ldg(L.trigs + n);                          // sin(π(2n, 2n+1)/M)
+        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, sn.x), ymap<NEUMANN>(a.y, m1, sn.y));
+        if (NEUMANN) {
+          const double2 cs = __ldg(L.trigc + n);                        // cos(π(2n, 2n+1)/M)
+          acc = fma(a.x - m0, cs.x, fma(a.y - m1, cs.y, acc));
+        }
       }
       x1p[p] = acc;
     }

@@ -45,6 +45,8 @@ struct LineParams {
   int nel;               // stored elements per line: M+1 (Neumann) or M-1 (hinged)
   int M, log2h;          // M = m (intervals); H = M/2 complex points
   const double2* trig;   // trig[j] = (cos(πj/M), sin(πj/M)), j = 0..M
+  const double2* trigs;  // k_dtt.cuh: trigs[n] = (sin(2nπ/M), sin((2n+1)π/M)), n < M/2 (one
+  const double2* trigc;  //   contiguous 16-byte load per lane); trigc[n] likewise with cos
   const double2* tw;     // FFT twiddles exp(-2πik/2^twlog)
   int twlog;
   unsigned long long* amax;   // optional: max |out| (NULL = off)

@@ -108,6 +108,7 @@ struct pd_handle {
   double2* tw = nullptr;
   double2* trig = nullptr;
   double2* trig2 = nullptr;          // (cos, sin)(2πk/M) in the [j][b] layout of k_dtt.cuh
+  double2* trigsc = nullptr;         // k_dtt.cuh pre-processing pairs: [M/2] sin, then [M/2] cos
   double2* trig2p = nullptr;         // (cos, sin)(2πk/M) in the [j][t] layout of k_dttp.cuh (M = 2048)
   // line kernels: 3 = k_dtt.cuh (default), 4 = k_dttp.cuh warp pairs for M = 2048 (opt-in: ncu d5b shows
   // it shared-memory bound, 12.2 vs 10.6 ms), 2 = k_fast.cuh
@@ -375,6 +376,7 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.ns = h->ns;
   L.nel = h->nx;
   L.M = (int)h->P.m; L.log2h = h->log2h; L.trig = h->trig; L.tw = h->tw; L.twlog = h->twlog;
+  L.trigs = h->trigsc; L.trigc = h->trigsc + std::max((int)h->P.m / 2, 1);
   L.amax = amax;
   L.tune = h->tune;
   L.upd = upd;
@@ -1094,6 +1096,13 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     const int b = k / 32, j = k % 32;
     trig2[(size_t)j * E2 + b] = trig[std::min(2 * k, M)];
   }
+  // k_dtt.cuh pre-processing: (sin, sin)(π(2n, 2n+1)/M), then (cos, cos)(π(2n, 2n+1)/M), n < M/2
+  const int HS = std::max(M / 2, 1);
+  std::vector<double2> trigsc(2 * (size_t)HS, make_double2(0.0, 0.0));
+  for (int n = 0; 2 * n + 1 <= M && n < HS; ++n) {
+    trigsc[n] = make_double2(trig[2 * n].y, trig[2 * n + 1].y);
+    trigsc[HS + n] = make_double2(trig[2 * n].x, trig[2 * n + 1].x);
+  }
   // k_dttp.cuh (M = 2048): k = 16t + j stored at j*64 + t
   std::vector<double2> trig2p(M == 2048 ? 1024 : 0);
   for (int k = 0; k < (int)trig2p.size(); ++k) trig2p[(size_t)(k % 16) * 64 + k / 16] = trig[2 * k];
@@ -1135,6 +1144,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
   PD_TRY(dalloc(h, &h->trig2, (size_t)H2));
+  PD_TRY(dalloc(h, &h->trigsc, trigsc.size()));
   if (!trig2p.empty()) PD_TRY(dalloc(h, &h->trig2p, trig2p.size()));
   PD_TRY(dalloc(h, &h->st, 1));
   {
@@ -1165,6 +1175,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       (h->l3 && up(h->l3, l3.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
       up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
       up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)) ||
+      up(h->trigsc, trigsc.data(), trigsc.size() * sizeof(double2)) ||
       (!trig2p.empty() && up(h->trig2p, trig2p.data(), trig2p.size() * sizeof(double2))))
     return cleanup(fail(PD_ECUDA, "table upload failed"));
 
