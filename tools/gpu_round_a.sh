@@ -2,6 +2,9 @@
 # Round evidence, part 1: all GPU tests, the default bench line, the ncu launch list of the bench
 # command.  usage: tools/gpu_round_a.sh TAG   (part 2, the --set full capture: tools/gpu_ncu_c5.sh)
 tag=${1:-r01}
+if [ -n "$(find paper_2304_14021_b200/csrc include -newer paper_2304_14021_b200/lib/libparadiag.so -type f)" ]; then
+  echo "libparadiag.so is older than its sources: rebuild first"; exit 3
+fi
 mkdir -p gpurun_out
 O=gpurun_out
 nvidia-smi > $O/${tag}_smi.txt 2>&1
