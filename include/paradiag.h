@@ -260,6 +260,33 @@ PD_API int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l
  * unpack of the transposes.  Any handle (its stream is used). */
 PD_API int paradiag_copy3d(pd_handle* h, const double* src, double* dst, int64_t n0, int64_t n1, int64_t n2,
                            int64_t s0, int64_t s1, int64_t d0, int64_t d1);
+/* ---------------------------------------------------------------------------------------------
+ * Time slabs — 1D long windows across ranks (SURVEY §8(f) NEXT-3 "frequency sharding with a tiny
+ * spatial problem").  Steps (1)/(3) are per spatial mode and Step (2) per time bin
+ * (P:158-169), the residual couples only u_n and u_{n-1}.  Every rank holds a handle of
+ * the GLOBAL problem (paradiag_init; 1D linear kind, N_t > 4096 or PARADIAG_TLONG, N_x <= 64) and
+ * owns the contiguous time rows [n0, n0 + nn) of U for the residual, the x transforms and the
+ * update, and the column block [c0, c0 + bcols) of x-modes (all N_t rows) for the time pass.
+ * Between the two an all-to-all moves the blocks (dist.py, TimeSlabRank).
+ * Layouts (device, fp64, caller-owned):
+ *   u_prev [N_x]          the row before n0: u0 for n0 = 0, else the previous rank's last row
+ *   U_l [nn][N_x]         the rank's rows
+ *   blocks [pitch/bcols][nn][bcols]   r̂ / δ̂ of the rank's rows, block q = x-modes [q·bcols, ...)
+ *                                     (block q is the all-to-all chunk of rank q)
+ *   cols [N_t][bcols]     the x-modes [c0, c0 + bcols) of every time row
+ * pitch = 2⌈N_x/2⌉ (paradiag_tslab_pitch); bcols even, dividing pitch; modes past N_x are padding.
+ * paradiag_tslab_residual: blocks = T·(b − K U) of the rows (nested stencils R#15).
+ * paradiag_tslab_time: in place Γ_α-scaled DFT, divide per bin and mode, inverse on the
+ *   column block (a block of padding only is a no-op).
+ * paradiag_tslab_update: δ = T·δ̂ from blocks, U_l += δ, fold ‖δ‖∞ / ‖U‖∞ of the rows into the handle's
+ *   statistics (reset / read below; the caller reduces them over ranks).
+ * Errors: PD_EINVAL for another kind of handle, bad bcols / c0 / nn, NULL buffers. */
+PD_API int paradiag_tslab_pitch(const pd_handle* h, int64_t* pitch);
+PD_API int paradiag_tslab_residual(pd_handle* h, const double* u_prev, const double* U_l, int64_t nn, double* blocks,
+                                   int64_t bcols);
+PD_API int paradiag_tslab_time(pd_handle* h, double* cols, int64_t c0, int64_t bcols);
+PD_API int paradiag_tslab_update(pd_handle* h, const double* blocks, int64_t bcols, double* U_l, int64_t nn);
+
 /* Zero the handle's ‖δ‖∞ / ‖U‖∞ statistics (asynchronous) / read them (synchronises the stream). */
 PD_API int paradiag_stats_reset(pd_handle* h);
 PD_API int paradiag_stats_read(pd_handle* h, double* dmax, double* umax);

@@ -62,7 +62,8 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_slab_ypass", "paradiag_slab_xpass_seg", "paradiag_slab_ypass_seg", "paradiag_slab_xrange", "paradiag_slab_yrange",
            "paradiag_slab_update_range", "paradiag_ipc_handle", "paradiag_ipc_open", "paradiag_ipc_close",
            "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
-           "paradiag_stats_read"]
+           "paradiag_stats_read", "paradiag_tslab_pitch", "paradiag_tslab_residual", "paradiag_tslab_time",
+           "paradiag_tslab_update"]
 ABI_VERSION = 3
 
 
@@ -110,6 +111,10 @@ def load(path: str = LIB_PATH):
     lib.paradiag_copy3d.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i64]
     lib.paradiag_stats_reset.argtypes = [vp]
     lib.paradiag_stats_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_double)]
+    lib.paradiag_tslab_pitch.argtypes = [vp, P(i64)]
+    lib.paradiag_tslab_residual.argtypes = [vp, vp, vp, i64, vp, i64]
+    lib.paradiag_tslab_time.argtypes = [vp, vp, i64, i64]
+    lib.paradiag_tslab_update.argtypes = [vp, vp, i64, vp, i64]
     for name in EXPORTS:
         if name not in ("paradiag_destroy",):
             getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
@@ -361,6 +366,26 @@ def paradiag_stats_read(h):
     a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
     _check(load().paradiag_stats_read(h, ctypes.byref(a), ctypes.byref(b)), "paradiag_stats_read")
     return a.value, b.value
+
+
+def paradiag_tslab_pitch(h) -> int:
+    v = ctypes.c_int64(0)
+    _check(load().paradiag_tslab_pitch(h, ctypes.byref(v)), "paradiag_tslab_pitch")
+    return v.value
+
+
+def paradiag_tslab_residual(h, u_prev, U_l, nn, blocks, bcols):
+    _check(load().paradiag_tslab_residual(h, _ptr(u_prev, "u_prev"), _ptr(U_l, "U_l"), int(nn), _ptr(blocks, "blocks"),
+                                          int(bcols)), "paradiag_tslab_residual")
+
+
+def paradiag_tslab_time(h, cols, c0, bcols):
+    _check(load().paradiag_tslab_time(h, _ptr(cols, "cols"), int(c0), int(bcols)), "paradiag_tslab_time")
+
+
+def paradiag_tslab_update(h, blocks, bcols, U_l, nn):
+    _check(load().paradiag_tslab_update(h, _ptr(blocks, "blocks"), int(bcols), _ptr(U_l, "U_l"), int(nn)),
+           "paradiag_tslab_update")
 
 
 def paradiag_destroy(h):

@@ -35,6 +35,11 @@ constexpr size_t kX1Smem = (size_t)(2 * kX1H * kX1BP + kX1Warps * 2 * kX1In) * s
 struct X1Params {
   int nx, nt;
   int ld_in, ld_out;         // row pitches (doubles) of in / out
+  // time-slab mode (multi-rank long windows): the workspace side (MODE 0/1 out,
+  // MODE 2/3 in) in column blocks — column x of row n at (x / bc)·bstride + n·bc + x % bc; bc = 0:
+  // the plain pitch layout
+  int bc;
+  int64_t bstride;
   ResidualParams R;          // stencil coefficients (MODE 0)
   const double* B;           // [2][32][32]: B[0][j][i] = T[2i][j], B[1][j][i] = T[2i+1][j], zero padded
   DevStats* st;
@@ -70,6 +75,9 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
   __syncthreads();
   const int nx = Q.nx, nh = nx >> 1;
   const int nunits = (Q.nt + 7) >> 3;
+  // block offsets of this lane's two columns (time-slab input layout)
+  const int64_t boff0 = Q.bc ? (int64_t)(lane / Q.bc) * Q.bstride + lane % Q.bc : 0;
+  const int64_t boff1 = Q.bc ? (int64_t)((lane + 32) / Q.bc) * Q.bstride + (lane + 32) % Q.bc : 0;
   const int gw = blockIdx.x * kX1Warps + warp, nw = gridDim.x * kX1Warps;
   constexpr int NR = MODE == 0 ? 9 : 8;                             // staged rows per unit
   // cp.async copies of unit `u` (its rows; MODE 0 also row n0-1, = u0 for the first unit) into `b`
@@ -79,9 +87,15 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
     for (int i = 0; i < NR; ++i) {
       const int n = MODE == 0 ? n0 - 1 + i : n0 + i;
       if (n >= n0 + rows) break;
-      const double* src = (MODE == 0 && n < 0) ? u0 : in + (size_t)n * Q.ld_in;
       double* dst = ibuf + b * kX1In + i * kX1RP + 2;
-      for (int x = lane; x < nx; x += 32) cp_async8(dst + x, src + x);
+      if (MODE >= 2 && Q.bc) {
+        const double* src = in + (size_t)n * Q.bc;
+        if (lane < nx) cp_async8(dst + lane, src + boff0);
+        if (lane + 32 < nx) cp_async8(dst + lane + 32, src + boff1);
+      } else {
+        const double* src = (MODE == 0 && n < 0) ? u0 : in + (size_t)n * Q.ld_in;
+        for (int x = lane; x < nx; x += 32) cp_async8(dst + x, src + x);
+      }
     }
   };
   const int g = lane >> 2, q = lane & 3;                            // DMMA fragment coordinates
@@ -171,7 +185,14 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
       for (int t = 0; t < 4; ++t) {
         const int x = 2 * (8 * t + 2 * q);
         const double v[4] = {ae[t][0], ao[t][0], ae[t][1], ao[t][1]};
-        if (MODE <= 1) {                            // workspace: even pitch, all 64 columns (pad = 0)
+        if (MODE <= 1 && Q.bc) {                    // time-slab blocks (bc even: pairs stay in one block)
+          double* bo = out + (size_t)(n0 + g) * Q.bc;
+          if (x < Q.ld_out)
+            *reinterpret_cast<double2*>(bo + (int64_t)(x / Q.bc) * Q.bstride + x % Q.bc) = make_double2(v[0], v[1]);
+          if (x + 2 < Q.ld_out)
+            *reinterpret_cast<double2*>(bo + (int64_t)((x + 2) / Q.bc) * Q.bstride + (x + 2) % Q.bc) =
+                make_double2(v[2], v[3]);
+        } else if (MODE <= 1) {                     // workspace: even pitch, all 64 columns (pad = 0)
           if (x < Q.ld_out) *reinterpret_cast<double2*>(dst + x) = make_double2(v[0], v[1]);
           if (x + 2 < Q.ld_out) *reinterpret_cast<double2*>(dst + x + 2) = make_double2(v[2], v[3]);
         } else {

@@ -303,12 +303,17 @@ ResidualParams residual_params(pd_handle* h) {
 
 // 1D long windows with N_x ≤ 64 (k_x1d.cuh): MODE 0 residual + forward x transform, 1 forward,
 // 2 inverse (‖δ‖∞), 3 inverse + update
-int launch_x1d(pd_handle* h, int mode, const double* u0, const double* in, double* out, int kid) {
+// nrows < 0: all N_t rows; bc > 0: the workspace side in time-slab column blocks of bc columns
+// (block stride nrows·bc, X1Params)
+int launch_x1d(pd_handle* h, int mode, const double* u0, const double* in, double* out, int kid,
+               int64_t nrows = -1, int bc = 0) {
   X1Params Q;
-  Q.nx = h->nx; Q.nt = h->P.nt; Q.R = residual_params(h); Q.B = h->x1T; Q.st = h->st;
+  if (nrows < 0) nrows = h->P.nt;
+  Q.nx = h->nx; Q.nt = (int)nrows; Q.R = residual_params(h); Q.B = h->x1T; Q.st = h->st;
   Q.ld_in = mode <= 1 ? h->nx : (int)x1_pitch(h);       // user arrays: N_x; workspace: even pitch
   Q.ld_out = mode <= 1 ? (int)x1_pitch(h) : h->nx;
-  const int units = (h->P.nt + 7) / 8;
+  Q.bc = bc; Q.bstride = nrows * (int64_t)bc;
+  const int units = (int)((nrows + 7) / 8);
   const unsigned grid = (unsigned)std::min((units + kX1Warps - 1) / kX1Warps, 148 * 2);
   prof_begin(h, kid);
   switch (mode) {
@@ -466,7 +471,9 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
 }
 
 // Long-window time pass (k_tlong.cuh) on spatially transformed data: in → Y → X (divided) → Y → out.
-int tlong_time(pd_handle* h, const double* in, double* out) {
+// bc > 0 (time slabs, 1D): `in`/`out` hold the bc x-modes [c0, c0 + bc) of every time row (row
+// pitch bc); the divide takes their eigenvalues through T.xoff.
+int tlong_time(pd_handle* h, const double* in, double* out, int64_t c0 = 0, int64_t bc = 0) {
   TlongParams Q;
   Q.N = h->P.nt; Q.log2N = h->log2nt;
   Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = 1 << h->log2n1; Q.N2 = 1 << h->log2n2;
@@ -475,6 +482,11 @@ int tlong_time(pd_handle* h, const double* in, double* out) {
   Q.ghi = h->tlg; Q.glo = h->tlg + Q.N1; Q.gihi = h->tlg + Q.N1 + Q.N2; Q.gilo = h->tlg + 2 * Q.N1 + Q.N2;
   Q.tw = h->tw; Q.twlog = h->twlog;
   Q.T = time_params(h, nullptr);
+  if (bc > 0) {
+    const int64_t ncol = std::min<int64_t>(bc, h->ns - c0);        // real modes in the block (pad excluded)
+    Q.ns = ncol; Q.P = (ncol + 1) / 2; Q.nch = (Q.P + kTlPairs - 1) / kTlPairs; Q.ld = bc;
+    Q.T.ns = ncol; Q.T.nx = (int)ncol; Q.T.xoff = (int)c0;
+  }
   double2* Y = h->spec;
   double2* X = h->w1;
   if (h->tlfuse && tlong_fusable(Q)) {                   // A, fused B (+ divide), A⁻¹
@@ -1794,6 +1806,52 @@ int paradiag_slab_update(pd_handle* h, double* U_l, const double* delta_l) {
   prof_end(h, K_UPDATE);
   PD_LAUNCHED();
   return PD_OK;
+}
+
+// ---- time slabs (1D long windows across ranks): contiguous time rows per rank for
+// the residual / x transforms / update, column (x-mode) blocks of all N_t rows for the time pass
+namespace {
+int tslab_check(pd_handle* h, int64_t bcols) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->x1 || !h->tlong || is_ch(h->P.kind) || h->P.jacobian != PD_JACOBIAN_SCALAR)
+    return fail(PD_EINVAL, "time slabs need a 1D linear long-window handle with N_x <= 64 (DMMA x transforms)");
+  const int64_t pitch = x1_pitch(h);
+  if (bcols <= 0 || (bcols & 1) || pitch % bcols) return fail(PD_EINVAL, "bcols must be even and divide the mode pitch");
+  return PD_OK;
+}
+}  // namespace
+
+int paradiag_tslab_pitch(const pd_handle* h, int64_t* pitch) {
+  if (!h || !pitch) return PD_EINVAL;
+  *pitch = h->x1 ? (int64_t)x1_pitch(h) : 0;
+  return PD_OK;
+}
+
+int paradiag_tslab_residual(pd_handle* h, const double* u_prev, const double* U_l, int64_t nn, double* blocks,
+                            int64_t bcols) {
+  int rc = tslab_check(h, bcols);
+  if (rc) return rc;
+  if (!u_prev || !U_l || !blocks) return fail(PD_EINVAL, "NULL buffer");
+  if (nn < 1 || nn > h->P.nt) return fail(PD_EINVAL, "row count out of range");
+  return launch_x1d(h, 0, u_prev, U_l, blocks, K_XRES, nn, (int)bcols);
+}
+
+int paradiag_tslab_time(pd_handle* h, double* cols, int64_t c0, int64_t bcols) {
+  int rc = tslab_check(h, bcols);
+  if (rc) return rc;
+  if (!cols) return fail(PD_EINVAL, "NULL buffer");
+  if (c0 < 0 || c0 % bcols || c0 >= x1_pitch(h)) return fail(PD_EINVAL, "c0 must be a block start inside the pitch");
+  if (c0 >= h->ns) return PD_OK;                 // a block of padding only: nothing to solve
+  return tlong_time(h, cols, cols, c0, bcols);
+}
+
+int paradiag_tslab_update(pd_handle* h, const double* blocks, int64_t bcols, double* U_l, int64_t nn) {
+  int rc = tslab_check(h, bcols);
+  if (rc) return rc;
+  if (!blocks || !U_l) return fail(PD_EINVAL, "NULL buffer");
+  if (nn < 1 || nn > h->P.nt) return fail(PD_EINVAL, "row count out of range");
+  return launch_x1d(h, 3, nullptr, blocks, U_l, K_XUPD, nn, (int)bcols);
 }
 
 int paradiag_copy3d(pd_handle* h, const double* src, double* dst, int64_t n0, int64_t n1, int64_t n2, int64_t s0,

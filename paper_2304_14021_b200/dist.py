@@ -602,3 +602,140 @@ def _alltoall_virtual(ranks, phase, chunk=None):
             c = send_splits[s][q]
             recvs[q][off:off + c].copy_(sends[s][soff[s][q]:soff[s][q] + c])
             off += c
+
+
+# ---------------------------------------------------------------------------------------------
+# Time slabs: 1D long windows across ranks ("frequency sharding with a tiny
+# spatial problem — the other aspect ratio").  With N_x ≤ 64 and N_t up to 2^20 the
+# natural cut is in time: rank r owns the time rows [r·nn, (r+1)·nn) of U (nn = N_t / P) for the
+# residual (row n couples only u_n and u_{n-1}, so the one halo row is the previous
+# rank's last row, u0 on rank 0), the x transforms (DST-I / DCT-I per row) and the update; for
+# Steps (1)-(3) (per spatial mode along the whole window) it owns the x-mode block
+# [r·bc, (r+1)·bc) of every time row (bc = pitch / P, pitch = 2⌈N_x/2⌉).  Per iteration:
+#   halo row → residual + x transform into [P][nn][bc] blocks → all-to-all (block q to rank q;
+#   the received blocks stack to [N_t][bc]) → four-step time pass with the per-bin divide on the
+#   local modes → all-to-all back → inverse x transform + update → max-reduce ‖δ‖∞, ‖U‖∞.
+# Every step is a library call (paradiag_tslab_* of include/paradiag.h) through ``TslabOps``.
+class TslabOps:
+    """The local steps of one time-slab rank: a handle of the GLOBAL problem on this device."""
+
+    def __init__(self, problem, device, stream=None):
+        from . import paradiag_init, make_problem, pd_problem, paradiag_tslab_pitch
+        import torch
+        self.problem = problem if isinstance(problem, pd_problem) else make_problem(problem)
+        self.device = device
+        self.torch = torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self.h = paradiag_init(self.problem, device, stream)
+        self.pitch = paradiag_tslab_pitch(self.h)
+        self.nt = int(self.problem.nt)
+        self.nx = int(self.problem.m) + (1 if int(self.problem.bc) == 0 else -1)
+
+    def empty(self, count):
+        return self.torch.empty(count, dtype=self.torch.float64, device=f"cuda:{self.device}")
+
+    def residual(self, u_prev, U_l, nn, blocks, bc):
+        from . import paradiag_tslab_residual
+        paradiag_tslab_residual(self.h, u_prev, U_l, nn, blocks, bc)
+
+    def time(self, cols, c0, bc):
+        from . import paradiag_tslab_time
+        paradiag_tslab_time(self.h, cols, c0, bc)
+
+    def update(self, blocks, bc, U_l, nn):
+        from . import paradiag_tslab_update
+        paradiag_tslab_update(self.h, blocks, bc, U_l, nn)
+
+    def stats_reset(self):
+        from . import paradiag_stats_reset
+        paradiag_stats_reset(self.h)
+
+    def stats_read(self):
+        from . import paradiag_stats_read
+        return paradiag_stats_read(self.h)
+
+    def close(self):
+        from . import paradiag_destroy
+        if self.h:
+            paradiag_destroy(self.h)
+            self.h = None
+
+
+def tslab_geometry(nt: int, pitch: int, world: int):
+    """(nn, bc): time rows per rank and x-modes per rank; P must divide N_t and pitch/2."""
+    if world < 1 or nt % world or pitch % world or (pitch // world) % 2:
+        raise ValueError(f"time slabs: {world} ranks must divide N_t = {nt} and pitch/2 = {pitch // 2}")
+    return nt // world, pitch // world
+
+
+class TimeSlabRank:
+    """State and phases of one time-slab rank; ``iterate`` runs one defect-correction iteration on
+    the rank's rows U_l [nn][N_x] (flat)."""
+
+    def __init__(self, ops, rank: int, world: int):
+        self.ops, self.r, self.P = ops, rank, world
+        self.nt, self.nx, self.pitch = ops.nt, ops.nx, ops.pitch
+        self.nn, self.bc = tslab_geometry(self.nt, self.pitch, world)
+        self.n0, self.c0 = rank * self.nn, rank * self.bc
+        self.blocks = ops.empty(world * self.nn * self.bc)     # [P][nn][bc]: residual out / update in
+        self.cols = ops.empty(self.nt * self.bc)               # [N_t][bc] = [P][nn][bc]
+        self.halo = ops.empty(self.nx)                         # u_{n0-1} from rank r-1
+        self._dummy = ops.empty(self.nx)
+        self.splits = [self.nn * self.bc] * world
+
+    def last_row(self, U_l):
+        return U_l[(self.nn - 1) * self.nx:self.nn * self.nx]
+
+    def phase_residual(self, u0, U_l):
+        self.ops.stats_reset()
+        self.ops.residual(u0 if self.r == 0 else self.halo, U_l, self.nn, self.blocks, self.bc)
+
+    def phase_time(self):
+        self.ops.time(self.cols, self.c0, self.bc)
+
+    def phase_update(self, U_l):
+        self.ops.update(self.blocks, self.bc, U_l, self.nn)
+
+    def iterate(self, u0, U_l, comm: TorchComm, timer=None):
+        tm = timer or (lambda name: _Null())
+        with tm("halo"):      # last row → rank r+1 (its u_{n0-1}); the lower direction is unused
+            comm.halo(self._dummy, self.last_row(U_l).contiguous(), self.halo, self._dummy)
+        self.phase_residual(u0, U_l)
+        with tm("all_to_all"):
+            comm.all_to_all(self.cols, self.blocks, self.splits, self.splits)
+        self.phase_time()
+        with tm("all_to_all"):
+            comm.all_to_all(self.blocks, self.cols, self.splits, self.splits)
+        self.phase_update(U_l)
+        dmax, umax = self.ops.stats_read()
+        t = self.ops.empty(2)
+        t[0], t[1] = dmax, umax
+        comm.allreduce_max(t)
+        return float(t[0]), float(t[1])
+
+
+def iterate_tslab_virtual(ranks: List[TimeSlabRank], u0, Us):
+    """All P time-slab ranks in ONE process (one GPU): the phases in rank order, the halo and the
+    all-to-alls emulated by copies (no rank waits on another)."""
+    P = len(ranks)
+    for k in range(1, P):
+        ranks[k].halo.copy_(ranks[k - 1].last_row(Us[k - 1]))
+    for k in range(P):
+        ranks[k].phase_residual(u0, Us[k])
+    _tslab_exchange([rk.blocks for rk in ranks], [rk.cols for rk in ranks], ranks[0].splits[0])
+    for k in range(P):
+        ranks[k].phase_time()
+    _tslab_exchange([rk.cols for rk in ranks], [rk.blocks for rk in ranks], ranks[0].splits[0])
+    for k in range(P):
+        ranks[k].phase_update(Us[k])
+    st = [rk.ops.stats_read() for rk in ranks]
+    return max(s[0] for s in st), max(s[1] for s in st)
+
+
+def _tslab_exchange(sends, recvs, c):
+    """all_to_all with equal chunks c: chunk q of rank s's send → chunk s of rank q's receive."""
+    P = len(sends)
+    for q in range(P):
+        for s in range(P):
+            recvs[q][s * c:(s + 1) * c].copy_(sends[s][q * c:(q + 1) * c])
