@@ -324,6 +324,122 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
     return 0
 
 
+def run_tslab(args, p, rank, world, local, dev, stream, u0, cfg, metric):
+    """c6 (1D long window) sharded over the ranks in time slabs (dist.TimeSlabRank): contiguous time
+    rows for the residual / x transforms / update, x-mode column blocks of all N_t rows for the
+    four-step time pass, two NCCL all-to-alls per iteration (strong scaling: the whole window is
+    fixed; value = total dofs / max-rank time)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2304_14021_b200 as pd
+    from paper_2304_14021_b200 import dist as pdist
+    ops = pdist.TslabOps(p, local, stream.cuda_stream)
+    rk = pdist.TimeSlabRank(ops, rank, world)
+    comm = pdist.TorchComm()
+    nn, nx = rk.nn, rk.nx
+    u0_d = torch.from_numpy(np.ascontiguousarray(u0).reshape(-1)).to(dev)
+
+    def fresh_U():
+        if p.init == "zero":
+            return torch.zeros(nn * nx, dtype=torch.float64, device=dev)
+        return u0_d.reshape(1, nx).expand(nn, nx).contiguous().reshape(-1)
+
+    U_l = fresh_U()
+    for _ in range(args.warmup):
+        rk.iterate(u0_d, U_l, comm)
+    timer = EventTimer(stream)
+    pd.paradiag_profile(ops.h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            dmax, umax = rk.iterate(u0_d, U_l, comm, timer)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = pd.paradiag_profile_read(ops.h)
+    pd.paradiag_profile(ops.h, False)
+    coll = timer.collect()
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = p.dofs / (ms_step * 1e-3)
+    local_dofs = nn * nx
+    peak, peak_src = measured_peaks()
+    kernels = {}
+    for name, (n, tot) in prof.items():
+        avg = tot / max(n, 1)
+        bpd = BYTES_PER_DOF.get(name)
+        kernels[name] = {"avg_ms": avg, "share": tot / (ms if ms > 0 else 1),
+                         "gbs": (bpd * local_dofs / (avg * 1e-3) / 1e9) if bpd else None}
+    roof = None
+    if prof:
+        name, (n, tot) = max(prof.items(), key=lambda kv: kv[1][1])
+        avg = tot / n
+        bpd = BYTES_PER_DOF.get(name, 16.0)
+        ach = bpd * local_dofs / (avg * 1e-3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_src, "traffic": None, "algorithmic_bytes_per_launch": bpd * local_dofs,
+                "per": "rank 0 (its time rows / x-mode block)"}
+    sent = 8 * nn * rk.bc * (world - 1)           # bytes this rank sends per all-to-all
+    nvlink = None
+    if world > 1:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(reps):
+            comm.all_to_all(rk.cols, rk.blocks, rk.splits, rk.splits)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        a2a_ms = float(t.item())
+        nvlink = {"achieved": sent / (a2a_ms * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s",
+                  "frac": sent / (a2a_ms * 1e-3) / 1e9 / 770.0, "peak_source": "guide: measured peer copy per direction",
+                  "bytes_per_alltoall": sent, "alltoall_ms": a2a_ms,
+                  "measured": "standalone forward all-to-all of the iteration's blocks (max over ranks)",
+                  "in_iteration_ms": {k: coll[k] for k in coll}}
+    e2e = None
+    if not args.no_e2e:
+        K = p.fixed_iters or 3
+        u0h = torch.from_numpy(np.ascontiguousarray(u0).reshape(-1)).pin_memory()
+        outh = torch.empty(nx, dtype=torch.float64).pin_memory()
+        dist.barrier()
+        t0 = time.perf_counter()
+        u0e = u0h.to(dev, non_blocking=True)
+        Ue = fresh_U()
+        for _ in range(K):
+            rk.iterate(u0e, Ue, comm)
+        outh.copy_(Ue[(nn - 1) * nx:], non_blocking=True)
+        torch.cuda.synchronize()
+        tt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        e2e = {"value": K * p.dofs / te, "unit": "dof/s", "h2d_bytes_per_step": int(nx * 8),
+               "d2h_bytes_per_step": int(nx * 8), "step": f"H2D u0, {K} time-slab iterations, D2H u_Nt (last rank)",
+               "seconds_per_step": te}
+    launches = sum(n for n, _ in prof.values()) + args.steps          # + the stats reset per step
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "dof/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(cfg, parallelism=f"tslab{world}: time rows {nn} per rank (residual, x transforms, "
+                                                 f"update) / x-mode blocks of {rk.bc} (four-step time pass), two NCCL "
+                                                 f"all-to-alls + one halo row per iteration"),
+                "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
+                "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
+                "last_iter": {"delta_max": dmax, "u_max": umax}}
+        print(json.dumps(line), flush=True)
+    ops.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -336,8 +452,9 @@ def main():
     ap.add_argument("--profile", action="store_true", help="per-kernel event timing (on by default)")
     ap.add_argument("--mode", default="solve", choices=["solve", "iterate"],
                     help="time one K-iteration paradiag_solve (pipelined engine) or K paradiag_iterate calls")
-    ap.add_argument("--parallelism", default="auto", choices=["auto", "slab", "replicas"],
-                    help="N > 1: slab-sharded (strong scaling, default for 2D linear configs) or replicas")
+    ap.add_argument("--parallelism", default="auto", choices=["auto", "slab", "tslab", "replicas"],
+                    help="N > 1: slab-sharded (strong scaling, default for 2D linear configs), time slabs "
+                         "(strong scaling, default for the 1D long window c6) or replicas")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -376,7 +493,9 @@ def main():
     torch.cuda.set_device(local)
     sharded = (world > 1 and args.parallelism != "replicas" or args.parallelism == "slab") and p.dim == 2 \
         and p.kind != "cahn_hilliard"
-    if world > 1 or sharded:
+    tslab = (world > 1 and args.parallelism == "auto" or args.parallelism == "tslab") and p.dim == 1 \
+        and p.nt > 4096 and p.nx <= 64
+    if world > 1 or sharded or tslab:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
@@ -387,6 +506,8 @@ def main():
     u0 = make_u0(p)
     if sharded:
         return run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric)
+    if tslab:
+        return run_tslab(args, p, rank, world, local, dev, stream, u0, cfg, metric)
     u0_d = torch.from_numpy(u0).to(dev)
     s = pd.Solver(p, device=local, stream=stream.cuda_stream)
     U = torch.zeros(s.shape, dtype=torch.float64, device=dev)       # U⁰ = 0 (R#5)
