@@ -15,7 +15,7 @@ PD_DEV double stats_omega(const DevStats* st, int damped, double omega_cap, doub
 // caller's buffer from the alternate one).
 __global__ void __launch_bounds__(256)
 k_update(double* U, const double* delta, size_t n, DevStats* st, int damped, double omega_cap, double tau,
-         const double* Usrc = nullptr) {
+         const double* Usrc = nullptr, int want_dmax = 0) {
   if (!Usrc) Usrc = U;
   const double w = stats_omega(st, damped, omega_cap, tau);
   if (blockIdx.x == 0 && threadIdx.x == 0) st->omega = w;
@@ -25,19 +25,27 @@ k_update(double* U, const double* delta, size_t n, DevStats* st, int damped, dou
   const unsigned long long absmask = 0x7fffffffffffffffull;
   if ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(Usrc) | reinterpret_cast<uintptr_t>(delta)) & 15) {
     // a slice range of an odd-sized slab (chunked multi-rank schedule): scalar path
+    unsigned long long db = 0ull;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
       const double u = Usrc[i] + w * delta[i];
       U[i] = u;
       lbits = max(lbits, (unsigned long long)__double_as_longlong(u) & absmask);
+      if (want_dmax) db = max(db, (unsigned long long)__double_as_longlong(delta[i]) & absmask);
     }
     lbits = warp_max_u64(lbits);
     if ((threadIdx.x & 31) == 0 && lbits) atomicMax(&st->umax_bits, lbits);
+    if (want_dmax) {
+      db = warp_max_u64(db);
+      if ((threadIdx.x & 31) == 0 && db) atomicMax(&st->dmax_bits, db);
+    }
     return;
   }
   const size_t n2 = n / 2;
   double2* U2 = reinterpret_cast<double2*>(U);
   const double2* S2 = reinterpret_cast<const double2*>(Usrc);
   const double2* D2 = reinterpret_cast<const double2*>(delta);
+  // want_dmax (ω = 1 only): ‖δ‖∞ here, as a bit-pattern max like ‖U‖∞, instead of in the last line pass
+  unsigned long long dbits = 0ull;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
     double2 u = S2[i];
     const double2 d = __ldg(D2 + i);
@@ -47,14 +55,22 @@ k_update(double* U, const double* delta, size_t n, DevStats* st, int damped, dou
     const unsigned long long bx = (unsigned long long)__double_as_longlong(u.x) & absmask;
     const unsigned long long by = (unsigned long long)__double_as_longlong(u.y) & absmask;
     lbits = max(lbits, max(bx, by));
+    if (want_dmax)
+      dbits = max(dbits, max((unsigned long long)__double_as_longlong(d.x) & absmask,
+                             (unsigned long long)__double_as_longlong(d.y) & absmask));
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const double u = Usrc[n - 1] + w * delta[n - 1];
     U[n - 1] = u;
     lbits = max(lbits, (unsigned long long)__double_as_longlong(u) & absmask);
+    if (want_dmax) dbits = max(dbits, (unsigned long long)__double_as_longlong(delta[n - 1]) & absmask);
   }
   lbits = warp_max_u64(lbits);
   if ((threadIdx.x & 31) == 0 && lbits) atomicMax(&st->umax_bits, lbits);
+  if (want_dmax) {
+    dbits = warp_max_u64(dbits);
+    if ((threadIdx.x & 31) == 0 && dbits) atomicMax(&st->dmax_bits, dbits);
+  }
 }
 
 // U⁰: broadcast u0 to every time slice, or zero (R#5).
