@@ -311,6 +311,73 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
   const int64_t nsl = L.nlines / L.nx;
   const int64_t ngroups = nsl * gx;
   double lmax = 0.0;
+  // thread -> fixed column c = tid % C, rows e = tid / C + k·(NTH / C): pointer increments only
+  constexpr int RSTEP = NTH / C;
+  static_assert(64 % RSTEP == 0, "row step must divide 64");
+  constexpr int PER = 64 / RSTEP;
+  const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
+  const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
+  if constexpr (V == 0) {
+    if (!(L.tune & 8192)) {
+      // Plain pass, software-pipelined over tiles: after the transform every thread copies its
+      // outputs from the line buffers into registers (the transform's registers are dead), the CTA
+      // syncs, the NEXT tile's cp.async loads go into the freed buffers, and the outputs are stored
+      // from registers while those loads are in flight — the store phase of tile G overlaps the
+      // load phase of tile G+1 (ncu r01g: ≈ 16 % / 10 % of the samples waited on each).
+      constexpr int KB = (kNel + 63) / 64;            // 64-row blocks of a line
+      auto issue = [&](int64_t G) {
+        const int64_t n = G / gx;
+        const int x0 = (int)((G - n * gx) * C);
+        const int wcols = min(C, (int)(L.nx - x0));
+        if (c_t < wcols) {
+          double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
+          const double* s = in + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
+          const int64_t rstride = (int64_t)RSTEP * L.nx;
+          for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.nx) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+              if (e0 + j * RSTEP < kNel) cp_async8(lb + j * RSTEP, s + j * rstride);
+          }
+        }
+        cp_async_commit();
+      };
+      if (blockIdx.x < ngroups) issue(blockIdx.x);
+      for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
+        const int64_t n = G / gx;
+        const int x0 = (int)((G - n * gx) * C);
+        const int wcols = min(C, (int)(L.nx - x0));
+        if (!NEUMANN) {                               // ghosts (overwritten by the previous outputs)
+          for (int p = lane; p < D::P; p += 32) {
+            xb[p * D::LDX] = 0.0;
+            xb[p * D::LDX + D::M] = 0.0;
+          }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
+        __syncthreads();
+        double ov[KB * PER];
+        const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            ov[k * PER + j] = (c_t < wcols && e_t + 64 * k + j * RSTEP < kNel) ? ob[65 * k + j * RSTEP] : 0.0;
+        __syncthreads();                              // every output is in registers: buffers free
+        if (G + gridDim.x < ngroups) issue(G + gridDim.x);
+        if (c_t < wcols) {
+          double* d = out + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
+#pragma unroll
+          for (int k = 0; k < KB; ++k)
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+              if (e_t + 64 * k + j * RSTEP < kNel) d[(int64_t)(64 * k + j * RSTEP) * L.nx] = ov[k * PER + j];
+        }
+      }
+      cp_async_wait_all();
+      return;
+    }
+  }
   if (L.stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) __nanosleep(L.stagger_ns);   // see k_time2d_v2
   for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
     const int64_t n = G / gx;
@@ -337,12 +404,6 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
         }
       }
     }
-    // thread -> fixed column c = tid % C, rows e = tid / C + k·(NTH / C): pointer increments only
-    constexpr int RSTEP = NTH / C;
-    static_assert(64 % RSTEP == 0, "row step must divide 64");
-    constexpr int PER = 64 / RSTEP;
-    const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
-    const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
     if (GEN && c_t < wcols && L.sin.n) {                        // transpose blocks: row y lives in block s(y)
       double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
       auto seg_base = [&](int sg) {
