@@ -35,28 +35,14 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   // two CTAs share an SM; starting the second one late puts their load and compute phases out of
   // step, so one streams its tile while the other computes
   if (P.stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) __nanosleep(P.stagger_ns);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // thread -> fixed point c = tid % S, slices t = tid / S + k·TSTEP: pointer increments only
+  // (tiles wider than the CTA, S > 32·NW, only occur for N_t = 32: threads take S/(32·NW) points)
+  constexpr int CPT = S > NW * 32 ? S / (NW * 32) : 1;          // points per thread
+  constexpr int TSTEP = CPT > 1 ? 1 : NW * 32 / S;
+  static_assert(CPT == 1 || S % (NW * 32) == 0, "tile width");
+  const int c_t = CPT > 1 ? threadIdx.x : threadIdx.x % S, t_t = CPT > 1 ? 0 : threadIdx.x / S;
+  auto issue = [&](int64_t tile) {                  // cp.async of one tile into sm (dead points: 0)
     const int64_t s0 = tile * S;
-    if ((P.tune & 4) && tile + gridDim.x < ntiles) {      // (tune bit 2) L2 prefetch of the CTA's next tile (k_dtt.cuh)
-      const int64_t sn = s0 + (int64_t)gridDim.x * S;
-      const int64_t last = min((int64_t)S, P.ns - sn) - 1;
-      if (P.tune & 8) {
-        if (lane == 0)
-          for (int t = warp; t < NT; t += NW)
-            bulk_prefetch_l2(in + (size_t)t * P.ns + sn, (size_t)(last + 1) * 8, in + (size_t)NT * P.ns);
-      } else {
-        for (int t = threadIdx.x; t < NT; t += NW * 32) {
-          prefetch_l2(in + (size_t)t * P.ns + sn);
-          prefetch_l2(in + (size_t)t * P.ns + sn + last);
-        }
-      }
-    }
-    // thread -> fixed point c = tid % S, slices t = tid / S + k·TSTEP: pointer increments only
-    // (tiles wider than the CTA, S > 32·NW, only occur for N_t = 32: threads take S/(32·NW) points)
-    constexpr int CPT = S > NW * 32 ? S / (NW * 32) : 1;          // points per thread
-    constexpr int TSTEP = CPT > 1 ? 1 : NW * 32 / S;
-    static_assert(CPT == 1 || S % (NW * 32) == 0, "tile width");
-    const int c_t = CPT > 1 ? threadIdx.x : threadIdx.x % S, t_t = CPT > 1 ? 0 : threadIdx.x / S;
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
       const int c = c_t + cc * NW * 32;
@@ -71,6 +57,29 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       }
     }
     cp_async_commit();
+  };
+  // software pipeline over tiles (one point per thread): the outputs go from the tile buffer into
+  // registers, the next tile's loads are issued into the freed buffer, then the outputs are stored
+  // — the store phase of one tile overlaps the load phase of the next (as k_cols3)
+  const bool pipe = CPT == 1 && !(P.tune & 8192);
+  if (pipe && blockIdx.x < ntiles) issue(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t s0 = tile * S;
+    if (!pipe && (P.tune & 4) && tile + gridDim.x < ntiles) {      // (tune bit 2) L2 prefetch of the CTA's next tile (k_dtt.cuh)
+      const int64_t sn = s0 + (int64_t)gridDim.x * S;
+      const int64_t last = min((int64_t)S, P.ns - sn) - 1;
+      if (P.tune & 8) {
+        if (lane == 0)
+          for (int t = warp; t < NT; t += NW)
+            bulk_prefetch_l2(in + (size_t)t * P.ns + sn, (size_t)(last + 1) * 8, in + (size_t)NT * P.ns);
+      } else {
+        for (int t = threadIdx.x; t < NT; t += NW * 32) {
+          prefetch_l2(in + (size_t)t * P.ns + sn);
+          prefetch_l2(in + (size_t)t * P.ns + sn + last);
+        }
+      }
+    }
+    if (!pipe) issue(tile);
     cp_async_wait_all();
     __syncthreads();
     double2 v[32];
@@ -147,6 +156,24 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       }
     }
     __syncthreads();
+    if (pipe) {
+      constexpr int NV = NT / TSTEP;
+      double ov[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) ov[k] = sm[(t_t + k * TSTEP) * LD + c_t];
+      __syncthreads();                              // the tile buffer is free
+      if (tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+      if (s0 + c_t < P.ns) {
+        double* g = out + (size_t)t_t * P.ns + s0 + c_t;
+        const size_t gstep = (size_t)TSTEP * P.ns;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          g[k * gstep] = ov[k];
+          if (P.amax) lmax = amax_acc(lmax, ov[k]);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
       const int c = c_t + cc * NW * 32;
@@ -168,6 +195,7 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
     }
     __syncthreads();
   }
+  cp_async_wait_all();
   if (P.amax) warp_atomic_max_abs(P.amax, lmax);
 }
 
