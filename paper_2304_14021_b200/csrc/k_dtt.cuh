@@ -317,9 +317,9 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
   constexpr int PER = 64 / RSTEP;
   const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
   const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
-  if constexpr (V == 0) {
+  if constexpr (V == 0 || V == 2) {
     if (!(L.tune & 8192)) {
-      // Plain pass, software-pipelined over tiles: after the transform every thread copies its
+      // Software-pipelined over tiles (plain and block-addressed passes): after the transform every thread copies its
       // outputs from the line buffers into registers (the transform's registers are dead), the CTA
       // syncs, the NEXT tile's cp.async loads go into the freed buffers, and the outputs are stored
       // from registers while those loads are in flight — the store phase of tile G overlaps the
@@ -329,7 +329,28 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
         const int64_t n = G / gx;
         const int x0 = (int)((G - n * gx) * C);
         const int wcols = min(C, (int)(L.nx - x0));
-        if (c_t < wcols) {
+        if (GEN && c_t < wcols && L.sin.n) {           // transpose blocks: row y lives in block s(y)
+          double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
+          auto seg_base = [&](int sg) {
+            return in + L.sin.off[sg] + ((int64_t)n * L.sin.cnt[sg] - L.sin.e0[sg]) * L.nx + x0 + c_t;
+          };
+          int sg = 0, s_end = L.sin.e0[0] + L.sin.cnt[0];
+          const double* sb = seg_base(0);
+          for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+              const int e = e0 + j * RSTEP;
+              if (e < kNel) {
+                while (e >= s_end) {
+                  ++sg;
+                  sb = seg_base(sg);
+                  s_end = L.sin.e0[sg] + L.sin.cnt[sg];
+                }
+                cp_async8(lb + j * RSTEP, sb + (int64_t)e * L.nx);
+              }
+            }
+          }
+        } else if (c_t < wcols) {
           double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
           const double* s = in + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
           const int64_t rstride = (int64_t)RSTEP * L.nx;
@@ -365,16 +386,42 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
             ov[k * PER + j] = (c_t < wcols && e_t + 64 * k + j * RSTEP < kNel) ? ob[65 * k + j * RSTEP] : 0.0;
         __syncthreads();                              // every output is in registers: buffers free
         if (G + gridDim.x < ngroups) issue(G + gridDim.x);
-        if (c_t < wcols) {
+        if (GEN && c_t < wcols && L.sout.n) {
+          auto seg_base = [&](int sg) {
+            return out + L.sout.off[sg] + ((int64_t)n * L.sout.cnt[sg] - L.sout.e0[sg]) * L.nx + x0 + c_t;
+          };
+          int sg = 0, s_end = L.sout.e0[0] + L.sout.cnt[0];
+          double* sb = seg_base(0);
+#pragma unroll
+          for (int k = 0; k < KB; ++k)
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+              const int e = e_t + 64 * k + j * RSTEP;
+              if (e < kNel) {
+                while (e >= s_end) {
+                  ++sg;
+                  sb = seg_base(sg);
+                  s_end = L.sout.e0[sg] + L.sout.cnt[sg];
+                }
+                sb[(int64_t)e * L.nx] = ov[k * PER + j];
+                if (L.amax) lmax = amax_acc(lmax, ov[k * PER + j]);
+              }
+            }
+        } else if (c_t < wcols) {
           double* d = out + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
 #pragma unroll
           for (int k = 0; k < KB; ++k)
 #pragma unroll
             for (int j = 0; j < PER; ++j)
-              if (e_t + 64 * k + j * RSTEP < kNel) d[(int64_t)(64 * k + j * RSTEP) * L.nx] = ov[k * PER + j];
+              if (e_t + 64 * k + j * RSTEP < kNel) {
+                d[(int64_t)(64 * k + j * RSTEP) * L.nx] = ov[k * PER + j];
+                if (GEN && L.amax) lmax = amax_acc(lmax, ov[k * PER + j]);
+              }
         }
       }
       cp_async_wait_all();
+      if (GEN && L.amax) warp_atomic_max_abs(L.amax, lmax);
+      if (GEN && L.sout.n) __threadfence_system();   // block stores may target a peer GPU
       return;
     }
   }
