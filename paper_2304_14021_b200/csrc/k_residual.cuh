@@ -335,7 +335,8 @@ static_assert(kResIX * kResGroups == kResThreads, "one thread per inner column a
 // UPD (pipelined solve, linear kinds): the previous iteration's update is applied here — the
 // staged tile is U + dU, the outputs also write U_new to P.unew (a different buffer: neighbouring
 // tiles still read the old iterate as their halo) and reduce ‖U_new‖∞.
-// VAR: 0 general (runtime CH / slab-halo checks), 1 linear kind on a single handle, 2 CH kind on a
+// VAR: 0 general (runtime CH / slab-halo checks), 1 linear kind on a single handle, 3 linear kind on
+// a slab (halo rows, no CH branch), 2 CH kind on a
 // single handle — the single-handle variants are compiled without those branches
 template <int MODE, bool UPD = false, int VAR = 0>
 __global__ void __launch_bounds__(kResThreads)
@@ -353,9 +354,9 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
   const int x0 = blockIdx.x * kResTX, y0 = blockIdx.y * kResTY;
   const int n0 = blockIdx.z * kResChunk, n1 = min(n0 + kResChunk, P.nt);
   const size_t ns = (size_t)P.nx * P.ny;
-  const bool ch = VAR == 1 ? false : (VAR == 2 ? true : P.kind >= 2);
+  const bool ch = (VAR == 1 || VAR == 3) ? false : (VAR == 2 ? true : P.kind >= 2);
   constexpr bool eyre = MODE == 2;
-  const bool halos = VAR != 0 ? false : (P.hlo != nullptr || P.hhi != nullptr);
+  const bool halos = (VAR == 1 || VAR == 2) ? false : (P.hlo != nullptr || P.hhi != nullptr);
   // staging map (slice independent): element k of this thread -> smem slot, source buffer
   // (0: U, 1: lower halo, 2: upper halo) and offset within its slice, extension sign
   int soff[kResPer], dpos[kResPer], ssel[kResPer];

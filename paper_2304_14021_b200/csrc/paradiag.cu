@@ -1312,6 +1312,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
     PD_TRY(allow_smem((k_residual_tile<0, false, 1>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<0, false, 2>), kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<0, false, 3>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<1, false, 1>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<2, false, 2>), kResSmem));
     PD_TRY(allow_smem(k_residual_tile<0, true>, kResSmemUpd));
@@ -1587,7 +1588,9 @@ int paradiag_slab_residual(pd_handle* h, const double* u0_l, const double* U_l, 
   R.y0g = h->y0; R.nyg = h->ny; R.hlo = halo_lo; R.hhi = halo_hi; R.theta = 1.0;
   prof_begin(h, K_RESIDUAL);
   dim3 grd((h->nx + kResTX - 1) / kResTX, (h->nyl + kResTY - 1) / kResTY, (h->P.nt + kResChunk - 1) / kResChunk);
-  k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
+  // slab handles are linear kinds with θ = 1 (init_slab): the variant without the CH branch
+  if (is_ch(h->P.kind)) k_residual_tile<0><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
+  else k_residual_tile<0, false, 3><<<grd, kResThreads, kResSmem, h->stream>>>(u0_l, U_l, r_l, R, h->jpart);
   prof_end(h, K_RESIDUAL);
   PD_LAUNCHED();
   return PD_OK;
