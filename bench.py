@@ -617,14 +617,17 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": dict(cfg, parallelism="replicas" if world > 1 else "single-gpu",
-                               step=("one iteration of a K-iteration paradiag_solve (pipelined: update fused "
-                                     "into the next residual)" if args.mode == "solve" else "one paradiag_iterate")),
+                               step=("one iteration of a K-iteration paradiag_solve (device-side loop: CUDA "
+                                     "graph with a conditional node; residual, P_alpha^-1, update)"
+                                     if args.mode == "solve" else "one paradiag_iterate")),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches,
                 "clocks": clk.summary(), "kernels": kernels,
                 "iteration_hbm_frac_at_design_bytes": design_bytes / (ms_step * 1e-3) / 1e9 / peak,
                 "precond": precond_summary(prof, args.steps, p.dofs, peak),
-                "last_iter": {"delta_max": info.delta_max, "u_max": info.u_max}}
+                "last_iter": {"delta_max": (None if args.mode == "solve" else info.delta_max),   # solve: per-window
+                              "u_max": info.u_max,                                               # data only
+                              "last_rel": (float(sinfo.last_rel[0]) if args.mode == "solve" else None)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
