@@ -18,6 +18,7 @@ instead (weak scaling).
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -314,7 +315,7 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
                 "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
                 "precond": precond_summary(prof, args.steps, local_dofs, peak),
                 "last_iter": {"delta_max": dmax, "u_max": umax}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
     if rk.p2p:
         torch.cuda.synchronize()
         dist.barrier()                      # no rank still stores into a peer before unmapping
@@ -434,10 +435,21 @@ def run_tslab(args, p, rank, world, local, dev, stream, u0, cfg, metric):
                 "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
                 "last_iter": {"delta_max": dmax, "u_max": umax}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
     ops.close()
     dist.destroy_process_group()
     return 0
+
+
+def _finite(obj):
+    """The JSON line with non-finite floats as null (strict JSON: no NaN / Infinity tokens)."""
+    if isinstance(obj, float):
+        return obj if math.isfinite(obj) else None
+    if isinstance(obj, dict):
+        return {k: _finite(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_finite(v) for v in obj]
+    return obj
 
 
 def main():
@@ -482,7 +494,7 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
                 "cpu_baseline": {"value": v, "unit": "dof/s", "cores": cores, "kind": "oracle", "sample": desc},
                 "e2e": {"value": v, "unit": "dof/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
         return 0
 
     import numpy as np
@@ -628,7 +640,7 @@ def main():
                 "last_iter": {"delta_max": (None if args.mode == "solve" else info.delta_max),   # solve: per-window
                               "u_max": info.u_max,                                               # data only
                               "last_rel": (float(sinfo.last_rel[0]) if args.mode == "solve" else None)}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

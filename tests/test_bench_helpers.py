@@ -43,3 +43,12 @@ def test_reference_arm_json_line():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_json_line_is_strict():
+    """bench.py prints strict JSON: non-finite floats become null (no NaN / Infinity tokens)."""
+    import json
+    import bench
+    line = {"a": float("nan"), "b": [1.0, float("inf")], "c": {"d": -float("inf"), "e": 2}, "f": "x"}
+    out = json.dumps(bench._finite(line), allow_nan=False)
+    assert json.loads(out) == {"a": None, "b": [1.0, None], "c": {"d": None, "e": 2}, "f": "x"}
