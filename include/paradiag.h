@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PARADIAG_ABI_VERSION 3
+#define PARADIAG_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define PD_API __attribute__((visibility("default")))
@@ -111,7 +111,15 @@ typedef struct pd_iter_info {
   double  rel;           /* delta_max / u_max                                                     */
   double  jbar;          /* J̄ = mean(3U²-1) used by the CH preconditioner (0 for linear)          */
   double  omega;         /* damping factor applied                                                */
+  int32_t growth;        /* consecutive iterations (this window) with ‖δ_k‖∞ > ‖δ_{k-1}‖∞; at
+                            PD_GROWTH_LIMIT the window is flagged diverging          */
 } pd_iter_info;
+
+/* Divergence flag (SURVEY §5.3 failure detection): a window whose undamped increment ‖δ‖∞ grew in
+ * PD_GROWTH_LIMIT consecutive iterations is diverging — e.g. BJ.c5, which violates the hypothesis
+ * of Thm 3.3.  paradiag_solve stops such a window with PD_NOT_CONVERGED (fixed_iters
+ * runs keep iterating and only flag it).  The oracle applies the same rule (oracle/iterate.py). */
+#define PD_GROWTH_LIMIT 3
 
 #define PD_MAX_WINDOWS 64
 typedef struct pd_solve_info {
@@ -120,6 +128,7 @@ typedef struct pd_solve_info {
   int32_t iters[PD_MAX_WINDOWS];
   double  last_rel[PD_MAX_WINDOWS];
   double  seconds;       /* host wall time of the call                                             */
+  int32_t diverging;     /* windows flagged diverging (PD_GROWTH_LIMIT rule, see pd_iter_info)      */
 } pd_solve_info;
 
 /* ABI version (PARADIAG_ABI_VERSION); lets a binding check it loaded the library it expects. */
@@ -168,7 +177,8 @@ PD_API int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_i
 
 /* Full solve: for each window, set U⁰ (broadcast or zero), iterate until ‖δ‖∞ ≤ tol‖U‖∞ (or
  * exactly fixed_iters times), then hand u_{N_t} to the next window.  u0 is not modified;
- * on return U holds the last window's iterate.  PD_NOT_CONVERGED if a window hit max_iter. */
+ * on return U holds the last window's iterate.  PD_NOT_CONVERGED if a window hit max_iter or was
+ * stopped as diverging (info->diverging counts the flagged windows; PD_GROWTH_LIMIT). */
 PD_API int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* info);
 
 /* As paradiag_solve but with HOST buffers: copies u0_host ([ny][nx]) to the device, solves into

@@ -98,8 +98,16 @@ def iterate_once(prob, u0, U):
                        jbar=jbar, omega=omega, imag=imag)
 
 
-def solve_window(prob, u0, U=None, history=None):
-    """Iterate one window until the stop rule (or fixed K / max_iter).  Returns (U, iters, converged)."""
+GROWTH_LIMIT = 3   # ‖δ‖∞ growing in 3 consecutive iterations flags the window diverging
+
+
+def solve_window(prob, u0, U=None, history=None, flags=None):
+    """Iterate one window until the stop rule (or fixed K / max_iter).  Returns (U, iters, converged).
+
+    Failure detection: when the undamped increment ‖δ_k‖∞ exceeds ‖δ_{k-1}‖∞ in
+    GROWTH_LIMIT consecutive iterations the window is diverging (e.g. BJ.c5, outside Thm 3.3's
+    hypothesis): it stops unconverged, or with fixed K is only flagged.  flags (a list)
+    receives True/False per window."""
     u0 = np.asarray(u0, dtype=np.float64)
     if prob.dim == 1:
         u0 = u0.reshape(-1)
@@ -108,6 +116,7 @@ def solve_window(prob, u0, U=None, history=None):
     kmax = prob.fixed_iters if prob.fixed_iters is not None else prob.max_iter
     converged = False
     k = 0
+    growth, prev, diverging = 0, None, False
     for k in range(1, kmax + 1):
         U, info = iterate_once(prob, u0, U)
         if history is not None:
@@ -117,16 +126,24 @@ def solve_window(prob, u0, U=None, history=None):
         if prob.fixed_iters is None and info["delta_max"] <= prob.tol * info["u_max"]:
             converged = True
             break
+        growth = growth + 1 if prev is not None and info["delta_max"] > prev else 0
+        prev = info["delta_max"]
+        if growth >= GROWTH_LIMIT:
+            diverging = True
+            if prob.fixed_iters is None:
+                break
+    if flags is not None:
+        flags.append(diverging)
     return U, k, converged
 
 
-def solve(prob, u0, history=None):
+def solve(prob, u0, history=None, flags=None):
     """All windows.  Returns (U of the last window, [iters per window], [converged], [U_Nt per window])."""
     u0 = np.asarray(u0, dtype=np.float64)
     iters, conv, finals = [], [], []
     U = None
     for _ in range(prob.n_windows):
-        U, k, c = solve_window(prob, u0, history=history)
+        U, k, c = solve_window(prob, u0, history=history, flags=flags)
         iters.append(k)
         conv.append(c)
         finals.append(U[-1].copy())

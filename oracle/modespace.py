@@ -44,3 +44,13 @@ def sample(prob, g: np.ndarray, c0: np.ndarray, pts) -> np.ndarray:
         else:
             out.append(float(T[iy] @ c @ T[ix]) / (2.0 * prob.m) ** 2)
     return np.array(out)
+
+
+def slice_values(prob, g: np.ndarray, c0: np.ndarray, n: int) -> np.ndarray:
+    """The whole time slice u^K_n (array index n, time level n+1) of the iterate: sample() at every
+    spatial point, written as the two transform matmuls T c T / (2m)² (T symmetric)."""
+    T = spatial.transform_matrix(prob.m, prob.bc)
+    c = c0 * g ** (n + 1)
+    if prob.dim == 1:
+        return (T @ c) / (2.0 * prob.m)
+    return (T @ c @ T.T) / (2.0 * prob.m) ** 2

@@ -41,13 +41,13 @@ class pd_problem(ctypes.Structure):
 class pd_iter_info(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("delta_max", ctypes.c_double),
                 ("u_max", ctypes.c_double), ("rel", ctypes.c_double), ("jbar", ctypes.c_double),
-                ("omega", ctypes.c_double)]
+                ("omega", ctypes.c_double), ("growth", ctypes.c_int32)]
 
 
 class pd_solve_info(ctypes.Structure):
     _fields_ = [("windows_done", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("iters", ctypes.c_int32 * MAX_WINDOWS), ("last_rel", ctypes.c_double * MAX_WINDOWS),
-                ("seconds", ctypes.c_double)]
+                ("seconds", ctypes.c_double), ("diverging", ctypes.c_int32)]
 
 
 class pd_kernel_time(ctypes.Structure):
@@ -64,7 +64,8 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read", "paradiag_tslab_pitch", "paradiag_tslab_residual", "paradiag_tslab_time",
            "paradiag_tslab_update"]
-ABI_VERSION = 3
+ABI_VERSION = 4
+GROWTH_LIMIT = 3          # PD_GROWTH_LIMIT
 
 
 def load(path: str = LIB_PATH):
@@ -179,6 +180,17 @@ def _ptr(t, name):
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise ParadiagError(PD_EINVAL, name, "expected a contiguous float64 CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _check_tensor(t, name, numel, device):
+    """The C ABI receives raw pointers: refuse a tensor of the wrong size or on another device
+    before the library would read or write out of bounds."""
+    _ptr(t, name)
+    if t.numel() != numel:
+        raise ParadiagError(PD_EINVAL, name, f"has {t.numel()} elements, expected {numel}")
+    if t.device.index != device:
+        raise ParadiagError(PD_EINVAL, name, f"is on cuda:{t.device.index}, the handle on cuda:{device}")
+    return t
 
 
 # ---------------------------------------------------------------- thin C-ABI mirrors
@@ -409,20 +421,26 @@ class Solver:
         import torch
         return torch.empty(self.shape, dtype=torch.float64, device=f"cuda:{self.device}")
 
+    def _full(self, t, name):
+        return _check_tensor(t, name, self.shape[0] * self.shape[1] * self.shape[2], self.device)
+
+    def _slice(self, t, name):
+        return _check_tensor(t, name, self.shape[1] * self.shape[2], self.device)
+
     def residual(self, u0, U, r, want_jbar=False):
-        return paradiag_residual(self.h, u0, U, r, want_jbar)
+        return paradiag_residual(self.h, self._slice(u0, "u0"), self._full(U, "U"), self._full(r, "r"), want_jbar)
 
     def apply_precond(self, r, delta, jbar=0.0):
-        paradiag_apply_precond(self.h, r, delta, jbar)
+        paradiag_apply_precond(self.h, self._full(r, "r"), self._full(delta, "delta"), jbar)
 
     def apply_precond_jt(self, r, delta, jt):
-        return paradiag_apply_precond_jt(self.h, r, delta, jt)
+        return paradiag_apply_precond_jt(self.h, self._full(r, "r"), self._full(delta, "delta"), self._slice(jt, "jt"))
 
     def iterate(self, u0, U, info=None):
-        return paradiag_iterate(self.h, u0, U, info)
+        return paradiag_iterate(self.h, self._slice(u0, "u0"), self._full(U, "U"), info)
 
     def solve(self, u0, U):
-        return paradiag_solve(self.h, u0, U)
+        return paradiag_solve(self.h, self._slice(u0, "u0"), self._full(U, "U"))
 
     def solve_host(self, u0_host):
         uT = np.empty((self.ny, self.nx), dtype=np.float64)

@@ -13,7 +13,7 @@
 namespace pd {
 
 constexpr int kFastTimeWarps = 4;  // k_time2d_v2: warps per CTA
-constexpr int kFastRowWarps = 4;   // k_rows3 / k_rows_v2: warps per CTA (independent)
+constexpr int kFastRowWarps = 4;   // k_rows3: warps per CTA (independent)
 // column kernels: warps per CTA (C = warps·32/E adjacent columns per tile)
 constexpr int fast_col_warps(int E) { return E == 1 ? 2 : E == 2 ? 4 : 8; }
 
@@ -24,7 +24,7 @@ struct FastLaunch {
   int64_t ns;             // points per slice
   const double2* trig2;   // k_dtt.cuh split table
   const double2* trig2p;  // k_dttp.cuh split table (M = 2048 only)
-  int dtt_ver;            // 4 = k_dttp.cuh (M = 2048), 3 = k_dtt.cuh, 2 = k_fast.cuh line kernels
+  int dtt_ver;            // 4 = k_dttp.cuh (M = 2048, opt-in), otherwise k_dtt.cuh
 };
 
 template <int E>
@@ -38,11 +38,6 @@ void fast_time(const double* in, double* out, const TimeParams& T, const FastLau
 inline size_t fast_time_smem(int E, int nw = kFastTimeWarps) {
   const size_t S = 2 * (32 / E) * nw, tile = (size_t)32 * E * (S + 1);
   return std::max(tile, (size_t)nw * kWarpBufD) * sizeof(double);
-}
-inline size_t fast_rows_smem() { return (size_t)kFastRowWarps * kWarpBufD * sizeof(double); }
-inline size_t fast_cols_smem(int E) {
-  const size_t nw = fast_col_warps(E);
-  return (nw * kWarpBufD + 66 * (nw * (32 / E) + 1)) * sizeof(double);
 }
 constexpr int kPairsPerRowCta = 2;
 inline size_t dttp_rows_smem() { return (size_t)kPairsPerRowCta * DttPair<1>::BUF * sizeof(double); }
@@ -65,10 +60,6 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 2>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 3>), fast_time_smem(E));
   if (fast_time_smem(E, 8) <= 227 * 1024) PD_ATTR((k_time2d_v2<E, 8>), fast_time_smem(E, 8));
-  PD_ATTR((k_rows_v2<1, E, kFastRowWarps>), fast_rows_smem());
-  PD_ATTR((k_rows_v2<0, E, kFastRowWarps>), fast_rows_smem());
-  PD_ATTR((k_cols_v2<1, E, fast_col_warps(E)>), fast_cols_smem(E));
-  PD_ATTR((k_cols_v2<0, E, fast_col_warps(E)>), fast_cols_smem(E));
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 1>), dtt3_rows_smem<E>() + 100 * 1024);
@@ -108,40 +99,28 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
     }
     return;
   }
-  if (F.dtt_ver >= 3) {
-    if (axis == 0) {
-      const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
-      const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
-      // tune 256: pad the dynamic smem so only one CTA (4 warps) fits per SM (occupancy probe)
-      const size_t smem = dtt3_rows_smem<E>() + ((L.tune & 256) ? 100 * 1024 : 0);
-      const bool gen = L.sin.n || L.sout.n;
-      if (gen) k_rows3<NEUMANN, E, kFastRowWarps, 2><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
-      else if (L.upd) k_rows3<NEUMANN, E, kFastRowWarps, 3><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
-      else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
-      else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
-    } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
-      constexpr int C4 = 4 * (32 / E);
-      const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);
-      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 2);
-      k_cols3<NEUMANN, E, 4><<<grid, 128, (size_t)4 * Dtt3<1, E>::BUF * sizeof(double), F.stream>>>(in, out, L, F.trig2);
-    } else {
-      const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
-      const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
-      if (L.sin.n || L.sout.n || L.amax)
-        k_cols3<NEUMANN, E, NW, 2><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
-      else
-        k_cols3<NEUMANN, E, NW, 0><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
-    }
-    return;
-  }
   if (axis == 0) {
     const int64_t groups = (L.nlines + (32 / E) - 1) / (32 / E);
-    const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 16);
-    k_rows_v2<NEUMANN, E, kFastRowWarps><<<grid, kFastRowWarps * 32, fast_rows_smem(), F.stream>>>(in, out, L);
+    const unsigned grid = (unsigned)std::min<int64_t>((groups + kFastRowWarps - 1) / kFastRowWarps, 148 * 2);
+    // tune 256: pad the dynamic smem so only one CTA (4 warps) fits per SM (occupancy probe)
+    const size_t smem = dtt3_rows_smem<E>() + ((L.tune & 256) ? 100 * 1024 : 0);
+    const bool gen = L.sin.n || L.sout.n;
+    if (gen) k_rows3<NEUMANN, E, kFastRowWarps, 2><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+    else if (L.upd) k_rows3<NEUMANN, E, kFastRowWarps, 3><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+    else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+    else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+  } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
+    constexpr int C4 = 4 * (32 / E);
+    const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);
+    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 2);
+    k_cols3<NEUMANN, E, 4><<<grid, 128, (size_t)4 * Dtt3<1, E>::BUF * sizeof(double), F.stream>>>(in, out, L, F.trig2);
   } else {
     const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
-    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148 * 16);
-    k_cols_v2<NEUMANN, E, NW><<<grid, NW * 32, fast_cols_smem(E), F.stream>>>(in, out, L);
+    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+    if (L.sin.n || L.sout.n || L.amax)
+      k_cols3<NEUMANN, E, NW, 2><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+    else
+      k_cols3<NEUMANN, E, NW, 0><<<grid, NW * 32, dtt3_cols_smem<E>(), F.stream>>>(in, out, L, F.trig2);
   }
 }
 

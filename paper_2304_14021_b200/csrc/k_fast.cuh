@@ -199,198 +199,4 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   if (P.amax) warp_atomic_max_abs(P.amax, lmax);
 }
 
-// ------------------------------------------------------------------ DCT-I / DST-I, 2D lines
-// Shared per-warp core: PL = 32/E lines of length M = 64E held at xb + p·LDX (x_0..x_M, hinged
-// zeros explicit).  Pre-process into registers, FFT (H = M/2 = 32E complex), write the spectrum
-// in natural order over xb, then run the post-processing (prefix scans) through `emit`.
-template <int NEUMANN, int E>
-struct DttWarp {
-  static constexpr int PL = 32 / E, M = 64 * E, H = 32 * E, LDX = M + 2;
-  static constexpr int LOG2H = 5 + ilog2_c(E);
-
-  template <class Emit, class ChunkEnd>
-  PD_DEV static void run(double* xb, int nl, const LineParams& P, int lane, Emit emit, ChunkEnd chunk_end) {
-    double2 v[32];
-    double x1p[PL];
-#pragma unroll
-    for (int p = 0; p < PL; ++p) {
-      double acc = 0.0;
-      const double* x = xb + p * LDX;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int n = lane + 32 * e, j0 = 2 * n;
-        const double2 a = *reinterpret_cast<const double2*>(x + j0);   // x_{2n}, x_{2n+1}
-        const double m0 = x[M - j0], m1 = x[M - j0 - 1];
-        const double2 t0 = __ldg(P.trig + j0), t1 = __ldg(P.trig + j0 + 1);
-        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, t0.y), ymap<NEUMANN>(a.y, m1, t1.y));
-        if (NEUMANN) acc += (a.x - m0) * t0.x + (a.y - m1) * t1.x;
-      }
-      x1p[p] = acc;
-    }
-    if (NEUMANN) {
-#pragma unroll
-      for (int p = 0; p < PL; ++p) x1p[p] = warp_sum(x1p[p]);
-    }
-    __syncwarp();
-    double2* T = reinterpret_cast<double2*>(xb);
-    fft4_s1_to_s2<E, -1>(v, T, LOG2H, P.tw, P.twlog, lane);
-    {
-      const int pl = lane / E, k1 = lane - pl * E;
-#pragma unroll
-      for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * H + k1 + E * k2)] = v[k2];
-    }
-    __syncwarp();
-    double carry[PL];
-#pragma unroll
-    for (int p = 0; p < PL; ++p) carry[p] = 0.0;
-    for (int k0 = 0; k0 < H; k0 += 32) {
-#pragma unroll
-      for (int p = 0; p < PL; ++p) {
-        const int k = k0 + lane;
-        const double2 Zk = T[tpad(p * H + k)];
-        const double2 Zm = T[tpad(p * H + ((H - k) & (H - 1)))];
-        const double2 Ev = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
-        const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
-        const double2 t2 = __ldg(P.trig + 2 * k);
-        const double2 Y = make_double2(Ev.x + t2.x * O.x + t2.y * O.y, Ev.y + t2.x * O.y - t2.y * O.x);
-        double ev, scanv;
-        if (NEUMANN) {
-          ev = 2.0 * Y.x;
-          scanv = k == 0 ? 0.0 : Y.y;
-        } else {
-          ev = -2.0 * Y.y;
-          scanv = k == 0 ? Y.x : 2.0 * Y.x;
-        }
-        double incl = scanv;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const double S = carry[p] + incl;
-        carry[p] += __shfl_sync(0xffffffffu, incl, 31);
-        if (p < nl) {
-          if (NEUMANN) {
-            emit(p, 2 * k, ev, k0);
-            emit(p, 2 * k + 1, x1p[p] - 2.0 * S, k0);
-            if (k0 + 32 >= H && lane == 0) {
-              const double2 Z0 = T[tpad(p * H)];
-              emit(p, M, 2.0 * (Z0.x - Z0.y), k0);
-            }
-          } else {
-            emit(p, 2 * k, S, k0);
-            if (k > 0) emit(p, 2 * k - 1, ev, k0);
-          }
-        }
-      }
-      chunk_end(k0);
-    }
-    __syncwarp();
-  }
-};
-
-// Rows: each warp takes PL consecutive rows (contiguous in memory) per step.
-template <int NEUMANN, int E, int NW>
-__global__ void __launch_bounds__(NW * 32, 2)
-k_rows_v2(const double* in, double* out, LineParams P) {
-  using D = DttWarp<NEUMANN, E>;
-  extern __shared__ double2 smem2[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* xb = reinterpret_cast<double*>(smem2) + (size_t)warp * kWarpBufD;
-  double lmax = 0.0;
-  const int64_t ngroups = (P.nlines + D::PL - 1) / D::PL;
-  for (int64_t g = (int64_t)blockIdx.x * NW + warp; g < ngroups; g += (int64_t)gridDim.x * NW) {
-    const int64_t L0 = g * D::PL;
-    const int64_t rem = P.nlines - L0;
-    const int nl = rem < D::PL ? (int)rem : D::PL;
-    const double* src = in + L0 * P.nx;
-    for (int i = lane; i < nl * P.nel; i += 32) {
-      const int p = i / P.nel, e = i - p * P.nel;
-      cp_async8(xb + p * D::LDX + bidx<NEUMANN>(e), src + i);
-    }
-    cp_async_commit();
-    if (!NEUMANN) {
-      for (int p = lane; p < D::PL; p += 32) {
-        xb[p * D::LDX] = 0.0;
-        xb[p * D::LDX + D::M] = 0.0;
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    double* dst = out + L0 * P.nx;
-    D::run(xb, nl, P, lane,
-           [&](int p, int idx, double v, int) {
-             dst[p * P.nx + idx] = v;
-             lmax = fmax(lmax, fabs(v));
-           },
-           [](int) {});
-  }
-  if (P.amax) warp_atomic_max_abs(P.amax, lmax);
-}
-
-// Columns: CTA = NW warps x PL columns = C adjacent columns of one slice; rows are loaded C
-// doubles at a time and outputs staged [66][C] per 32-k chunk for coalesced row stores.
-template <int NEUMANN, int E, int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
-k_cols_v2(const double* in, double* out, LineParams P) {
-  using D = DttWarp<NEUMANN, E>;
-  constexpr int C = NW * D::PL;
-  constexpr int SP = C + 1;                    // staging row pitch (bank skew)
-  extern __shared__ double2 smem2[];
-  double* base = reinterpret_cast<double*>(smem2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* xb = base + (size_t)warp * kWarpBufD;
-  double* stage = base + (size_t)NW * kWarpBufD;
-  const int64_t gx = (P.nx + C - 1) / C;
-  const int64_t ngroups = (P.nlines / P.nx) * gx;
-  double lmax = 0.0;
-  for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
-    const int64_t n = G / gx;
-    const int x0 = (int)((G - n * gx) * C);
-    const int wcols = min(C, (int)(P.nx - x0));
-    const double* src = in + n * P.ns + x0;
-    double* dst = out + n * P.ns + x0;
-    for (int i = threadIdx.x; i < P.nel * C; i += NW * 32) {
-      const int e = i / C, c = i - e * C;
-      if (c < wcols) {
-        const int w = c / D::PL, p = c - w * D::PL;
-        cp_async8(base + (size_t)w * kWarpBufD + p * D::LDX + bidx<NEUMANN>(e), src + (int64_t)e * P.nx + c);
-      }
-    }
-    cp_async_commit();
-    if (!NEUMANN) {
-      for (int p = lane; p < D::PL; p += 32) {
-        xb[p * D::LDX] = 0.0;
-        xb[p * D::LDX + D::M] = 0.0;
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    const int nl = max(0, min(D::PL, wcols - warp * D::PL));
-    D::run(xb, nl, P, lane,
-           [&](int p, int idx, double v, int k0) { stage[(idx - 2 * k0 + 1) * SP + warp * D::PL + p] = v; },
-           [&](int k0) {
-             __syncthreads();
-             int lo, hi;
-             if (NEUMANN) {
-               lo = 2 * k0;
-               hi = k0 + 32 >= D::H ? D::M + 1 : 2 * (k0 + 32);
-             } else {
-               lo = max(2 * k0 - 1, 0);
-               hi = min(2 * k0 + 63, P.nel);
-             }
-             for (int i = threadIdx.x; i < (hi - lo) * C; i += NW * 32) {
-               const int r = i / C, c = i - r * C;
-               if (c < wcols) {
-                 const double v = stage[(lo + r - 2 * k0 + 1) * SP + c];
-                 dst[(int64_t)(lo + r) * P.nx + c] = v;
-                 lmax = fmax(lmax, fabs(v));
-               }
-             }
-             __syncthreads();
-           });
-  }
-  if (P.amax) warp_atomic_max_abs(P.amax, lmax);
-}
-
 }  // namespace pd

@@ -111,7 +111,7 @@ struct pd_handle {
   double2* trigsc = nullptr;         // k_dtt.cuh pre-processing pairs: [M/2] sin, then [M/2] cos
   double2* trig2p = nullptr;         // (cos, sin)(2πk/M) in the [j][t] layout of k_dttp.cuh (M = 2048)
   // line kernels: 3 = k_dtt.cuh (default), 4 = k_dttp.cuh warp pairs for M = 2048 (opt-in: ncu d5b shows
-  // it shared-memory bound, 12.2 vs 10.6 ms), 2 = k_fast.cuh
+  // it shared-memory bound, 12.2 vs 10.6 ms)
   int dtt_ver = 3;
   int tune = 0;                       // PARADIAG_TUNE: A/B switches for measurements
   int stagger_ns = 0;                 // PARADIAG_STAGGER: phase offset of co-resident CTAs (ns)
@@ -809,7 +809,9 @@ int iteration(pd_handle* h, const double* u0, double* U, pd_iter_info* info) {
 // to host or graph conditional"): the body is one iteration's kernels plus k_loop_decide, which
 // applies the stop rule on the device — no host round trip per iteration
 struct LoopCtl {
-  int iters, limit, fixed, status;   // status: 0 running, 1 converged, 2 iteration limit, 3 non-finite
+  int iters, limit, fixed, status;   // status: 0 running, 1 converged, 2 iteration limit, 3 non-finite,
+                                     // 4 diverging (PD_GROWTH_LIMIT consecutive growths of ‖δ‖∞)
+  int growth, diverging;
   double tol, rel, dmax, umax;
 };
 
@@ -819,7 +821,10 @@ __global__ void k_loop_decide(const DevStats* st, LoopCtl* c, cudaGraphCondition
   const int it = ++c->iters;
   const bool finite = isfinite(dmax) && isfinite(umax);
   const bool conv = c->fixed <= 0 && dmax <= c->tol * umax;           // R#4, as the host loop
-  c->status = !finite ? 3 : conv ? 1 : (it >= c->limit ? 2 : 0);
+  c->growth = (it > 1 && dmax > c->dmax) ? c->growth + 1 : 0;
+  if (c->growth >= PD_GROWTH_LIMIT) c->diverging = 1;
+  const bool stop_div = c->diverging && c->fixed <= 0 && !conv;
+  c->status = !finite ? 3 : conv ? 1 : stop_div ? 4 : (it >= c->limit ? 2 : 0);
   c->rel = umax > 0 ? dmax / umax : 0.0;
   c->dmax = dmax;
   c->umax = umax;
@@ -880,7 +885,7 @@ int build_graph(pd_handle* h, double* U) {
 }
 
 // One window on the device: reset the loop control, launch the graph, read the outcome.
-int graph_window(pd_handle* h, int* iters, bool* conv, double* rel) {
+int graph_window(pd_handle* h, int* iters, bool* conv, double* rel, bool* div) {
   LoopCtl* c = static_cast<LoopCtl*>(h->ctl_host);
   *c = LoopCtl{};
   c->fixed = h->P.fixed_iters;
@@ -893,6 +898,7 @@ int graph_window(pd_handle* h, int* iters, bool* conv, double* rel) {
   *iters = c->iters;
   *conv = c->status == 1;
   *rel = c->rel;
+  *div = c->diverging != 0;
   if (c->status == 3) return fail(PD_EDIVERGED, "non-finite increment or iterate");
   return PD_OK;
 }
@@ -918,7 +924,8 @@ int read_stats(pd_handle* h, double* dmax, double* umax) {
 //   end:     U^K = U^{K-1} + δ_K into the caller's buffer
 // which saves the separate update pass (24 B/dof).  The stop test of iteration k-1 (needs ‖U^{k-1}‖)
 // runs after step k; on convergence step k's δ is discarded.
-int solve_window_pipelined(pd_handle* h, const double* u0, double* U, int* iters, bool* conv, double* rel) {
+int solve_window_pipelined(pd_handle* h, const double* u0, double* U, int* iters, bool* conv, double* rel,
+                           bool* div) {
   if (!h->Ub) {
     int rc;
     if ((rc = dalloc(h, &h->Ub, (size_t)h->total)) || (rc = dalloc(h, &h->work2, (size_t)h->total))) return rc;
@@ -937,6 +944,8 @@ int solve_window_pipelined(pd_handle* h, const double* u0, double* U, int* iters
   if ((rc = read_stats(h, &dprev, &umax))) return rc;
   if (!std::isfinite(dprev)) return fail(PD_EDIVERGED, "non-finite increment");
   *conv = false;
+  *div = false;
+  int growth = 0;
   for (int k = 2; k <= kmax; ++k) {
     k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
     PD_LAUNCHED();
@@ -954,7 +963,24 @@ int solve_window_pipelined(pd_handle* h, const double* u0, double* U, int* iters
         PD_CUDA(cudaMemcpyAsync(U, Ubuf[cu], (size_t)h->total * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
       return PD_OK;
     }
+    growth = dmax > dprev ? growth + 1 : 0;                      // SURVEY §5.3 (PD_GROWTH_LIMIT)
     dprev = dmax;
+    if (growth >= PD_GROWTH_LIMIT) {
+      *div = true;
+      if (!fixed) {                                             // stop: U^k = U^{k-1} + δ_k below
+        *iters = k;
+        break;
+      }
+    }
+  }
+  if (*div && !fixed) {
+    k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
+    PD_LAUNCHED();
+    k_update<<<148 * 8, 256, 0, h->stream>>>(U, Wbuf[cw], (size_t)h->total, h->st, 0, 1.0, 1.0, Ubuf[cu]);
+    PD_LAUNCHED();
+    if ((rc = read_stats(h, &dmax, &umax))) return rc;
+    *rel = umax > 0 ? dprev / umax : 0.0;
+    return PD_OK;
   }
   k_reset_stats<<<1, 1, 0, h->stream>>>(h->st);
   PD_LAUNCHED();
@@ -1324,7 +1350,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       PD_TRY(dalloc(h, &h->work2, (size_t)h->total));
     }
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
-    if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f);
+    if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f) == 4 ? 4 : 3;
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_STAGGER")) h->stagger_ns = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
@@ -1383,6 +1409,7 @@ int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_info* in
   rc = iteration(h, u0, U, &tmp);
   tmp.iters = info->iters + 1;
   tmp.converged = (h->P.fixed_iters <= 0) && tmp.delta_max <= h->P.tol * tmp.u_max;
+  tmp.growth = (info->iters > 0 && tmp.delta_max > info->delta_max) ? info->growth + 1 : 0;   // PD_GROWTH_LIMIT
   *info = tmp;
   return rc;
 }
@@ -1400,14 +1427,15 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
   for (int w = 0; w < h->P.n_windows; ++w) {
     if (can_pipeline(h)) {
       int iters = 0;
-      bool conv = false;
+      bool conv = false, div = false;
       double rel = 0.0;
-      if ((rc = solve_window_pipelined(h, cur_u0, U, &iters, &conv, &rel))) {
+      if ((rc = solve_window_pipelined(h, cur_u0, U, &iters, &conv, &rel, &div))) {
         info->windows_done = w;
         return rc;
       }
       info->iters[w] = iters;
       info->last_rel[w] = rel;
+      info->diverging += div ? 1 : 0;
       info->windows_done = w + 1;
       all_conv = all_conv && conv;
       if (!conv && h->P.fixed_iters <= 0) status = PD_NOT_CONVERGED;
@@ -1431,11 +1459,12 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
     if (graph_ok(h) && h->gexec && h->gU == U) {
       if ((rc = init_iterate(h, U, cur_u0))) return rc;
       int iters = 0;
-      bool conv = false;
+      bool conv = false, div = false;
       double rel = 0.0;
-      rc = graph_window(h, &iters, &conv, &rel);
+      rc = graph_window(h, &iters, &conv, &rel, &div);
       info->iters[w] = iters;
       info->last_rel[w] = rel;
+      info->diverging += div ? 1 : 0;
       if (rc) {
         info->windows_done = w;
         return rc;
@@ -1452,8 +1481,9 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
     }
     if ((rc = init_iterate(h, U, cur_u0))) return rc;
     const int kmax = h->P.fixed_iters > 0 ? h->P.fixed_iters : h->P.max_iter;
-    bool conv = false;
-    int k = 0;
+    bool conv = false, div = false;
+    int k = 0, growth = 0;
+    double dprev = 0.0;
     pd_iter_info it{};
     for (k = 1; k <= kmax; ++k) {
       if ((rc = iteration(h, cur_u0, U, &it))) {
@@ -1465,7 +1495,14 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
         conv = true;
         break;
       }
+      growth = (k > 1 && it.delta_max > dprev) ? growth + 1 : 0;       // SURVEY §5.3 (PD_GROWTH_LIMIT)
+      dprev = it.delta_max;
+      if (growth >= PD_GROWTH_LIMIT) {
+        div = true;
+        if (h->P.fixed_iters <= 0) break;
+      }
     }
+    info->diverging += div ? 1 : 0;
     info->iters[w] = std::min(k, kmax);
     info->last_rel[w] = it.rel;
     info->windows_done = w + 1;

@@ -236,6 +236,19 @@ class TorchComm:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
 
+    def shift_up(self, send, recv):
+        """One-directional neighbour exchange: send -> rank+1, recv <- rank-1 (separate buffers, no
+        message in the unused direction)."""
+        ops = []
+        P2P = self.dist.P2POp
+        if self.rank < self.world - 1:
+            ops.append(P2P(self.dist.isend, send, self.rank + 1, self.group))
+        if self.rank > 0:
+            ops.append(P2P(self.dist.irecv, recv, self.rank - 1, self.group))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
     def allreduce_max(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
 
@@ -681,7 +694,6 @@ class TimeSlabRank:
         self.blocks = ops.empty(world * self.nn * self.bc)     # [P][nn][bc]: residual out / update in
         self.cols = ops.empty(self.nt * self.bc)               # [N_t][bc] = [P][nn][bc]
         self.halo = ops.empty(self.nx)                         # u_{n0-1} from rank r-1
-        self._dummy = ops.empty(self.nx)
         self.splits = [self.nn * self.bc] * world
 
     def last_row(self, U_l):
@@ -699,8 +711,8 @@ class TimeSlabRank:
 
     def iterate(self, u0, U_l, comm: TorchComm, timer=None):
         tm = timer or (lambda name: _Null())
-        with tm("halo"):      # last row → rank r+1 (its u_{n0-1}); the lower direction is unused
-            comm.halo(self._dummy, self.last_row(U_l).contiguous(), self.halo, self._dummy)
+        with tm("halo"):      # last row → rank r+1 (its u_{n0-1}), one direction only
+            comm.shift_up(self.last_row(U_l).contiguous(), self.halo)
         self.phase_residual(u0, U_l)
         with tm("all_to_all"):
             comm.all_to_all(self.cols, self.blocks, self.splits, self.splits)

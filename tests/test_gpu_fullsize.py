@@ -98,3 +98,7 @@ def test_c5_full_fixed_K(cuda_lib):
     gm, c0 = modespace.mode_iterates(p, u0, 3)
     ref = modespace.sample(p, gm, c0, pts)
     assert np.abs(got - ref).max() <= 1e-10 * umax
+    # whole slices, every spatial point (first, second, middle and last time level)
+    for n in (0, 1, p.nt // 2 - 1, p.nt - 1):
+        ref_n = modespace.slice_values(p, gm, c0, n)
+        assert np.abs(U[n].cpu().numpy() - ref_n).max() <= 1e-10 * umax, n

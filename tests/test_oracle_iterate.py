@@ -186,3 +186,96 @@ def test_ch_mass_and_energy():
     assert np.abs(masses - m0).max() <= 1e-12 * max(abs(m0), 1e-3)
     E = np.array([diagnostics.energy(p, v) for v in traj])
     assert np.all(np.diff(E) <= 1e-14)
+
+
+# ---------------------------------------------------------------- pins added in round 2
+@pytest.mark.parametrize("dim", [1, 2])
+def test_energy_single_cosine_mode_closed_form(dim):
+    """diagnostics.energy on u = A cos(kπx)(cos(lπy)) against its closed form (R#13).
+
+    Trapezoid sums on m intervals are exact for these trigonometric polynomials:
+    h Σ w cos² = 1/2, h Σ w cos⁴ = 3/8 (k, l ∉ {0, m/2, m}); each edge difference is
+    -2A sin(kπ/2m) sin(kπ(2j+1)/2m), so Σ_j (δu)² = 2A² m sin²(kπ/2m).  Hence
+      1D: E = ¼(3A⁴/8 - A² + 1) + ε² A² m² sin²(kπ/2m)
+      2D: E = ¼(9A⁴/64 - A²/2 + 1) + (ε²/2) A² m² (sin²(kπ/2m) + sin²(lπ/2m))
+    (each 2D gradient sum carries the other axis' Σ w cos² = m/2 and no h factor, h^{d-2} = 1).
+    A wrong scale on the bulk or the gradient term, or a dropped weight, fails this."""
+    from dataclasses import replace
+    p = _ch_twin(m=32)
+    if dim == 1:
+        p = replace(p, dim=1)
+    A, k, l = 0.7, 3, 5
+    m, e2 = p.m, p.eps * p.eps
+    x = np.arange(m + 1) / m
+    sk, sl = np.sin(k * np.pi / (2 * m)) ** 2, np.sin(l * np.pi / (2 * m)) ** 2
+    if dim == 1:
+        u = A * np.cos(k * np.pi * x)
+        ref = 0.25 * (3 * A ** 4 / 8 - A * A + 1) + e2 * A * A * m * m * sk
+    else:
+        u = A * np.outer(np.cos(l * np.pi * x), np.cos(k * np.pi * x))
+        ref = 0.25 * (9 * A ** 4 / 64 - A * A / 2 + 1) + 0.5 * e2 * A * A * m * m * (sk + sl)
+    assert abs(diagnostics.energy(p, u) - ref) <= 1e-14 * abs(ref)
+
+
+@pytest.mark.parametrize("name,expect", [("c1", 2.03e-7), ("c2", 4.40e-2), ("c3", 1.33e-12), ("c5", 3.66)])
+def test_modewise_factor_survey_probe_values(name, expect):
+    """theory.modewise_factor against the survey's independent scratch probe p1."""
+    f = theory.modewise_factor(config(name)).max()
+    assert abs(f - expect) <= 0.005 * expect
+
+
+def test_modewise_factor_is_the_per_mode_increment_ratio():
+    """Per spatial mode the WR error contracts by exactly -αg^N/(1-αg^N): from the second
+    iteration on both iterates are WR trajectories, so the increments δ^k_N of the physical-space
+    oracle iteration, projected on the eigenmodes, have |δ^3_N / δ^2_N| = theory.modewise_factor
+    mode by mode (random U⁰ excites every mode; modes whose increment is at rounding level skipped)."""
+    from dataclasses import replace
+    for name, kw, theta in (("c5", dict(m=16, nt=8), 1.0), ("c5", dict(m=16, nt=8), 0.5),
+                            ("c2", dict(m=31, nt=8), 0.5)):
+        p = replace(twin(name, theta=theta, **kw), fixed_iters=3)
+        u0 = make_u0(p)
+        u0 = u0.reshape(-1) if p.dim == 1 else u0
+        U = np.random.default_rng(3).uniform(-1, 1, (p.nt,) + u0.shape)
+        inc = []
+        for _ in range(3):
+            U_new, _ = iterate.iterate_once(p, u0, U)
+            inc.append(U_new[-1] - U[-1])
+            U = U_new
+        a, b = sequential.to_modes(p, inc[1]), sequential.to_modes(p, inc[2])
+        f = theory.modewise_factor(p).reshape(a.shape)
+        live = np.abs(a) > 1e-6 * np.abs(a).max()
+        assert live.sum() >= 20
+        assert np.allclose(np.abs(b[live] / a[live]), f[live], rtol=1e-4)
+
+
+@pytest.mark.parametrize("name,kw,K", [("c5", dict(m=32, nt=16), 3), ("c3", dict(m=16, nt=8), 2)])
+def test_modespace_slice_values_equal_physical_iterate(name, kw, K):
+    """modespace.slice_values (the whole-slice form used at full c5 size) = the physical-space
+    K-th iterate of the oracle at every point of every slice."""
+    from dataclasses import replace
+    p = replace(twin(name, **kw), fixed_iters=K)
+    u0 = make_u0(p)
+    U, _, _, _ = iterate.solve(p, u0)
+    g, c0 = modespace.mode_iterates(p, u0, K)
+    for n in range(p.nt):
+        assert np.abs(modespace.slice_values(p, g, c0, n) - U[n]).max() <= 1e-12 * np.abs(U).max()
+
+
+def test_divergence_rule_stops_c5_twin():
+    """BJ.c5's physics violates Thm 3.3: from U⁰ = 0 the increments grow ≈3x per
+    iteration, so the SURVEY §5.3 rule stops the window unconverged after PD_GROWTH_LIMIT growths
+    (iterations 1 < 2 < 3 < 4); with fixed K it only flags it.  Converging twins never trip it."""
+    from dataclasses import replace
+    p = replace(twin("c5", m=32, nt=16), fixed_iters=None, max_iter=50)
+    hist, flags = [], []
+    U, iters, conv, _ = iterate.solve(p, make_u0(p), hist, flags)
+    d = [h["delta_max"] for h in hist]
+    assert iters == [1 + iterate.GROWTH_LIMIT] and conv == [False] and flags == [True]
+    assert all(b > a for a, b in zip(d, d[1:]))
+    flags = []
+    iterate.solve(replace(p, fixed_iters=6), make_u0(p), None, flags)
+    assert flags == [True]
+    flags = []
+    q = twin("c3", m=16, nt=8)
+    _, _, conv, _ = iterate.solve(q, make_u0(q), None, flags)
+    assert conv == [True] and flags == [False]
