@@ -33,8 +33,22 @@ template <int E>
 void fast_line(int neumann, int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F);
 template <int E>
 void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F);
+// TMA-staged three-stage time pass (k_time2d_v4), in place on the buffer tmap describes: [N_t][ps]
+// with ps = N_s rounded up to even, box {16, min(N_t, 256)}.  Returns false when this E has none.
+template <int E>
+bool fast_time_tma(double* buf, const TimeParams& T, const FastLaunch& F, const CUtensorMap* tmap);
 
 #ifdef PD_FAST_DEFINE
+template <int E>
+constexpr size_t fast_time3_smem() {
+  constexpr size_t S = 2 * (32 / E) * 4, tile = (size_t)32 * E * (S + 1), scr = (size_t)4 * kWarpBufD;
+  return (3 * (((tile > scr ? tile : scr) + 1) & ~(size_t)1)) * 8 + (size_t)2 * 32 * E * 16 + 3 * 8;
+}
+template <int E>
+constexpr size_t fast_time4_smem() {
+  constexpr size_t S = 2 * (32 / E) * 4, tile = (size_t)S * 32 * E * 8, scr = (size_t)4 * kWarpBufD * 8;
+  return 3 * (((tile > scr ? tile : scr) + 1023) & ~(size_t)1023) + (size_t)2 * 32 * E * 16 + 3 * 8;
+}
 inline size_t fast_time_smem(int E, int nw = kFastTimeWarps) {
   const size_t S = 2 * (32 / E) * nw, tile = (size_t)32 * E * (S + 1);
   return std::max(tile, (size_t)nw * kWarpBufD) * sizeof(double);
@@ -55,6 +69,18 @@ size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * s
 
 template <int E>
 cudaError_t fast_attrs() {
+  if constexpr (E <= 16 && fast_time4_smem<E>() <= 227 * 1024) {
+    PD_ATTR((k_time2d_v4<E, 0>), fast_time4_smem<E>());
+    PD_ATTR((k_time2d_v4<E, 1>), fast_time4_smem<E>());
+    PD_ATTR((k_time2d_v4<E, 2>), fast_time4_smem<E>());
+    PD_ATTR((k_time2d_v4<E, 3>), fast_time4_smem<E>());
+  }
+  if constexpr (fast_time3_smem<E>() <= 227 * 1024) {
+    PD_ATTR((k_time2d_v3<E, 0>), fast_time3_smem<E>());
+    PD_ATTR((k_time2d_v3<E, 1>), fast_time3_smem<E>());
+    PD_ATTR((k_time2d_v3<E, 2>), fast_time3_smem<E>());
+    PD_ATTR((k_time2d_v3<E, 3>), fast_time3_smem<E>());
+  }
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 0>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 1>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 2>), fast_time_smem(E));
@@ -141,8 +167,21 @@ void fast_time(const double* in, double* out, const TimeParams& T, const FastLau
   }
   constexpr int S = 2 * (32 / E) * kFastTimeWarps;
   const int64_t tiles = (F.ns + S - 1) / S;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
   const int flags = ((!T.el && !T.l3) ? 1 : 0) | (T.gamma_folded ? 2 : 0);
+  if constexpr (fast_time3_smem<E>() <= 227 * 1024) {
+    if (!(T.tune & 65536) && !T.amax) {     // 3-stage two-group schedule (tune 65536: the 2-CTA kernel)
+      const unsigned grid3 = (unsigned)std::min<int64_t>((tiles + 1) / 2, 148);
+      constexpr size_t sm3 = fast_time3_smem<E>();
+      switch (flags) {
+        case 3: k_time2d_v3<E, 3><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
+        case 2: k_time2d_v3<E, 2><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
+        case 1: k_time2d_v3<E, 1><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
+        default: k_time2d_v3<E, 0><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
+      }
+      return;
+    }
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
   const size_t sm = fast_time_smem(E);
   constexpr int NWT = kFastTimeWarps;
   switch (flags) {
@@ -153,7 +192,30 @@ void fast_time(const double* in, double* out, const TimeParams& T, const FastLau
   }
 }
 
+template <int E>
+bool fast_time_tma(double* buf, const TimeParams& T, const FastLaunch& F, const CUtensorMap* tmap) {
+  if constexpr (E > 16) {
+    return false;
+  } else if constexpr (fast_time4_smem<E>() <= 227 * 1024) {      // 3-stage, two groups (k_time2d_v4)
+    constexpr int S = 2 * (32 / E) * 4;
+    const int64_t tiles = (F.ns + S - 1) / S;
+    const unsigned grid = (unsigned)std::min<int64_t>((tiles + 1) / 2, 148);     // tile pairs per CTA
+    const int flags = ((!T.el && !T.l3) ? 1 : 0) | (T.gamma_folded ? 2 : 0);
+    constexpr size_t sm = fast_time4_smem<E>();
+    switch (flags) {
+      case 3: k_time2d_v4<E, 3><<<grid, 256, sm, F.stream>>>(*tmap, T); break;
+      case 2: k_time2d_v4<E, 2><<<grid, 256, sm, F.stream>>>(*tmap, T); break;
+      case 1: k_time2d_v4<E, 1><<<grid, 256, sm, F.stream>>>(*tmap, T); break;
+      default: k_time2d_v4<E, 0><<<grid, 256, sm, F.stream>>>(*tmap, T); break;
+    }
+    return true;
+  } else {
+    return false;
+  }
+}
+
 #define PD_FAST_INSTANTIATE(E)                                                                       \
+  template bool fast_time_tma<E>(double*, const TimeParams&, const FastLaunch&, const CUtensorMap*); \
   template cudaError_t fast_attrs<E>();                                                             \
   template void fast_line<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&); \
   template void fast_time<E>(const double*, double*, const TimeParams&, const FastLaunch&);

@@ -102,14 +102,14 @@ PD_DEV void dft_reg(double2* v) {
 // Powers w^k, k < K (K ≤ 32), of w = W_N^{base} (conjugated for SIGN = +1), from the table
 // tw[j] = exp(-2πi j/2^twlog): w^{1,2,4} and w^{8,16} are loaded exactly, w^k = lo[k&7]·hi[k>>3]
 // with lo/hi composed by at most one multiply — every power carries ≤ 3 roundings.
-template <int K, int SIGN>
+template <int K, int SIGN, bool SMEMTAB = false>
 struct TwPow {
   static constexpr int NL = K < 8 ? K : 8;
   static constexpr int NH = K <= 8 ? 1 : K / 8;
   double2 lo[NL];
   double2 hi[NH];
   PD_DEV double2 ld(const double2* __restrict__ tw, int e, int N, int sh) {
-    double2 t = __ldg(tw + ((e & (N - 1)) << sh));
+    double2 t = SMEMTAB ? tw[(e & (N - 1)) << sh] : __ldg(tw + ((e & (N - 1)) << sh));
     if (SIGN > 0) t.y = -t.y;
     return t;
   }
@@ -140,11 +140,11 @@ PD_DEV int tpad(int q) { return q + (q >> 5); }
 constexpr int kWarpScratch = 1024 + 32;   // complex slots per warp (tpad(1023) = 1054)
 
 // Forward (SIGN=-1) or inverse-direction (SIGN=+1) transform: stage-1 layout in, stage-2 out.
-template <int E, int SIGN>
+template <int E, int SIGN, bool SMEMTAB = false>
 PD_DEV void fft4_s1_to_s2(double2 (&v)[32], double2* T, int log2N, const double2* __restrict__ tw,
                           int twlog, int lane) {
   constexpr int P = 32 / E;
-  const TwPow<E, SIGN> w(lane, log2N, tw, twlog);           // W_N^{l·k1}, l = lane
+  const TwPow<E, SIGN, SMEMTAB> w(lane, log2N, tw, twlog);           // W_N^{l·k1}, l = lane
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     dft_reg<E, SIGN>(v + p * E);
@@ -160,13 +160,13 @@ PD_DEV void fft4_s1_to_s2(double2 (&v)[32], double2* T, int log2N, const double2
 
 // Stage-2 layout in, stage-1 layout out (the reverse of fft4_s1_to_s2 with the same SIGN
 // convention for its roots).  Used with SIGN=+1 to invert a forward transform.
-template <int E, int SIGN>
+template <int E, int SIGN, bool SMEMTAB = false>
 PD_DEV void fft4_s2_to_s1(double2 (&v)[32], double2* T, int log2N, const double2* __restrict__ tw,
                           int twlog, int lane) {
   constexpr int P = 32 / E;
   dft_reg<32, SIGN>(v);                                     // over k2 -> index l
   {
-    const TwPow<32, SIGN> w(lane % E, log2N, tw, twlog);    // W_N^{l·k1}, l = register index
+    const TwPow<32, SIGN, SMEMTAB> w(lane % E, log2N, tw, twlog);    // W_N^{l·k1}, l = register index
 #pragma unroll
     for (int l = 0; l < 32; ++l) T[tpad(lane * 32 + l)] = w.apply(v[l], l);
   }

@@ -253,7 +253,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
             const double* s = in + L.sin.off[q] + (L0 + p) * L.sin.cnt[q] - e0;
             for (int e = e0 + lane; e < e1; e += 32) cp_async8(x + e, s + e);
           }
-        } else {
+        } else if (!(L.tune & 16384)) {           // (A/B) tune 16384: no loads
           const double* s = src + p * L.nx;
           for (int e = lane; e < L.nel; e += 32) cp_async8(x + e, s + e);
         }
@@ -278,7 +278,7 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
         else if (GEN && L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (GEN && L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (V == 1 || (GEN && L.amax)) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
-        else store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
+        else if (!(L.tune & 32768)) store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
       }
     }
     __syncwarp();
@@ -328,7 +328,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
       auto issue = [&](int64_t G) {
         const int64_t n = G / gx;
         const int x0 = (int)((G - n * gx) * C);
-        const int wcols = min(C, (int)(L.nx - x0));
+        const int wcols = (L.tune & 16384) ? 0 : min(C, (int)(L.nx - x0));   // (A/B) tune 16384: no loads
         if (GEN && c_t < wcols && L.sin.n) {           // transpose blocks: row y lives in block s(y)
           double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
           auto seg_base = [&](int sg) {
@@ -352,7 +352,7 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
           }
         } else if (c_t < wcols) {
           double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
-          const double* s = in + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
+          const double* s = in + n * L.ps_in + x0 + (int64_t)e_t * L.nx + c_t;
           const int64_t rstride = (int64_t)RSTEP * L.nx;
           for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.nx) {
 #pragma unroll
@@ -407,8 +407,8 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
                 if (L.amax) lmax = amax_acc(lmax, ov[k * PER + j]);
               }
             }
-        } else if (c_t < wcols) {
-          double* d = out + n * L.ns + x0 + (int64_t)e_t * L.nx + c_t;
+        } else if (c_t < wcols && !(L.tune & 32768)) {   // (A/B) tune 32768: no stores
+          double* d = out + n * L.ps_out + x0 + (int64_t)e_t * L.nx + c_t;
 #pragma unroll
           for (int k = 0; k < KB; ++k)
 #pragma unroll
@@ -430,15 +430,15 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
     const int64_t n = G / gx;
     const int x0 = (int)((G - n * gx) * C);
     const int wcols = min(C, (int)(L.nx - x0));
-    const double* src = in + n * L.ns + x0;
-    double* dst = out + n * L.ns + x0;
+    const double* src = in + n * L.ps_in + x0;
+    double* dst = out + n * L.ps_out + x0;
     {
       const int64_t Gn = G + gridDim.x;
       if ((L.tune & 2) && Gn < ngroups) {
         const int64_t nn = Gn / gx;
         const int xn = (int)((Gn - nn * gx) * C);
         const int wn = min(C, (int)(L.nx - xn));
-        const double* s = in + nn * L.ns + xn;
+        const double* s = in + nn * L.ps_in + xn;
         const double* lim = in + L.nlines * L.nx;
         if (L.tune & 8) {      // one bulk prefetch per row segment, lane 0 of each warp
           if (lane == 0)

@@ -10,10 +10,66 @@
 #include "fft4.cuh"
 #include "k_spatial.cuh"
 #include "k_time.cuh"
+#include "tma.cuh"
 
 namespace pd {
 
 constexpr int kWarpBufD = 2 * kWarpScratch + 2;   // doubles per warp buffer (16-B aligned, bank-skewed)
+
+// Forward time FFT of the warp's PP pencil pairs (stage-1 layout in v), the per-mode divide of
+// Step-(2) (Hermitian-paired), and the inverse FFT back to the stage-1 layout.  sw = spatial
+// index of the warp's first pencil pair; T = the warp's scratch (kWarpScratch complex).
+// tw/twlog, dl: the FFT root table and the d_l table (global, or shared-memory copies).
+template <int E, int PP, int FLAGS, bool SMEMTAB = false>
+PD_DEV void time_solve_regs(double2 (&v)[32], double2* T, int64_t sw, int lane, const TimeParams& P, double jbar,
+                            const double2* tw, int twlog, const double2* dl) {
+  constexpr int NT = 32 * E;
+  constexpr int LOG2NT = 5 + ilog2_c(E);
+  fft4_s1_to_s2<E, -1, SMEMTAB>(v, T, LOG2NT, tw, twlog, lane);
+  // ---- per-mode divide (Step-(2)).  lane = (pair pl, k1), v[k2] = Z[l], l = k1 + E k2.  The
+  // spectrum is parked in natural order in the warp scratch so every lane reads its Z_{N-l}
+  // with the same code path (no divergence, no register hazards).
+  const int pl = lane / E, k1 = lane - pl * E;
+  const int64_t sa = sw + 2 * pl;
+  const double mua = sa < P.ns ? mode_mu(sa, P, jbar) : 0.0;
+  const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
+  const double lama = P.l3 && sa < P.ns ? mode_lam(sa, P) : 0.0;            // PinT-II only
+  const double lamb = P.l3 && sa + 1 < P.ns ? mode_lam(sa + 1, P) : lama;
+#pragma unroll
+  for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * NT + k1 + E * k2)] = v[k2];
+  __syncwarp();
+  // Hermitian pairing: d_{N-l} = conj(d_l) and μ is real, so with Af = A_l/(d_l+μa),
+  // Bf = B_l/(d_l+μb) the mirror bin is X_{N-l} = conj(Af) + i conj(Bf) — one pair of complex
+  // reciprocals serves both bins.  Lane (pl, k1) handles its bins k2 < 16 and their mirrors, which
+  // live in the upper half (k2 >= 16) of lane E-k1 (itself for k1 = 0, E/2); the mirrors go
+  // through the parked slots.  Bin N/2 (lane k1 = 0, k2 = 16) is its own mirror.
+#pragma unroll
+  for (int k2 = 0; k2 <= 16; ++k2) {
+    if (k2 == 16 && k1 != 0) break;
+    const int l = k1 + E * k2;
+    const int m = (NT - l) & (NT - 1);
+    const double2 Zl = k2 < 16 ? v[k2] : T[tpad(pl * NT + l)];
+    const double2 Zm = T[tpad(pl * NT + m)];
+    const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
+    const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
+    const double2 d = SMEMTAB ? dl[l] : __ldg(dl + l);
+    double2 Af, Bf;
+    if (FLAGS & 1) {
+      Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
+      Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
+    } else {
+      Af = cmul(A, cinv_fast(shifted(d, P.el, l, mua, P.l3, lama)));
+      Bf = cmul(B, cinv_fast(shifted(d, P.el, l, mub, P.l3, lamb)));
+    }
+    if (k2 < 16) v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);       // X_l = Af + i Bf
+    T[tpad(pl * NT + m)] = make_double2(Af.x + Bf.y, Bf.x - Af.y);      // X_{N-l}
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k2 = 16; k2 < 32; ++k2) v[k2] = T[tpad(pl * NT + k1 + E * k2)];
+  __syncwarp();
+  fft4_s2_to_s1<E, +1, SMEMTAB>(v, T, LOG2NT, tw, twlog, lane);
+}
 
 // ------------------------------------------------------------------ fused 2D time pass
 // CTA = NW warps; warp w owns PP = 32/E pencil pairs = 2·PP spatial points; tile = NT x S.
@@ -43,6 +99,10 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   const int c_t = CPT > 1 ? threadIdx.x : threadIdx.x % S, t_t = CPT > 1 ? 0 : threadIdx.x / S;
   auto issue = [&](int64_t tile) {                  // cp.async of one tile into sm (dead points: 0)
     const int64_t s0 = tile * S;
+    if (P.tune & 16384) {                           // (A/B) timing decomposition: no tile loads
+      cp_async_commit();
+      return;
+    }
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
       const int c = c_t + cc * NW * 32;
@@ -94,50 +154,7 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       }
     }
     __syncthreads();
-    fft4_s1_to_s2<E, -1>(v, T, LOG2NT, P.tw, P.twlog, lane);
-    // ---- per-mode divide (Step-(2)).  lane = (pair pl, k1), v[k2] = Z[l], l = k1 + E k2.  The
-    // spectrum is parked in natural order in the warp scratch so every lane reads its Z_{N-l}
-    // with the same code path (no divergence, no register hazards).
-    const int pl = lane / E, k1 = lane - pl * E;
-    const int64_t sa = s0 + 2 * (warp * PP + pl);
-    const double mua = sa < P.ns ? mode_mu(sa, P, jbar) : 0.0;
-    const double mub = sa + 1 < P.ns ? mode_mu(sa + 1, P, jbar) : mua;
-    const double lama = P.l3 && sa < P.ns ? mode_lam(sa, P) : 0.0;            // PinT-II only
-    const double lamb = P.l3 && sa + 1 < P.ns ? mode_lam(sa + 1, P) : lama;
-#pragma unroll
-    for (int k2 = 0; k2 < 32; ++k2) T[tpad(pl * NT + k1 + E * k2)] = v[k2];
-    __syncwarp();
-    // Hermitian pairing: d_{N-l} = conj(d_l) and μ is real, so with Af = A_l/(d_l+μa),
-    // Bf = B_l/(d_l+μb) the mirror bin is X_{N-l} = conj(Af) + i conj(Bf) — one pair of complex
-    // reciprocals serves both bins.  Lane (pl, k1) handles its bins k2 < 16 and their mirrors, which
-    // live in the upper half (k2 >= 16) of lane E-k1 (itself for k1 = 0, E/2); the mirrors go
-    // through the parked slots.  Bin N/2 (lane k1 = 0, k2 = 16) is its own mirror.
-#pragma unroll
-    for (int k2 = 0; k2 <= 16; ++k2) {
-      if (k2 == 16 && k1 != 0) break;
-      const int l = k1 + E * k2;
-      const int m = (NT - l) & (NT - 1);
-      const double2 Zl = k2 < 16 ? v[k2] : T[tpad(pl * NT + l)];
-      const double2 Zm = T[tpad(pl * NT + m)];
-      const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
-      const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
-      const double2 d = __ldg(P.dl + l);
-      double2 Af, Bf;
-      if (FLAGS & 1) {
-        Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
-        Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
-      } else {
-        Af = cmul(A, cinv_fast(shifted(d, P.el, l, mua, P.l3, lama)));
-        Bf = cmul(B, cinv_fast(shifted(d, P.el, l, mub, P.l3, lamb)));
-      }
-      if (k2 < 16) v[k2] = make_double2(Af.x - Bf.y, Af.y + Bf.x);       // X_l = Af + i Bf
-      T[tpad(pl * NT + m)] = make_double2(Af.x + Bf.y, Bf.x - Af.y);      // X_{N-l}
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k2 = 16; k2 < 32; ++k2) v[k2] = T[tpad(pl * NT + k1 + E * k2)];
-    __syncwarp();
-    fft4_s2_to_s1<E, +1>(v, T, LOG2NT, P.tw, P.twlog, lane);
+    time_solve_regs<E, PP, FLAGS>(v, T, s0 + 2 * warp * PP, lane, P, jbar, P.tw, P.twlog, P.dl);
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < PP; ++p) {
@@ -163,7 +180,7 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
       for (int k = 0; k < NV; ++k) ov[k] = sm[(t_t + k * TSTEP) * LD + c_t];
       __syncthreads();                              // the tile buffer is free
       if (tile + gridDim.x < ntiles) issue(tile + gridDim.x);
-      if (s0 + c_t < P.ns) {
+      if (s0 + c_t < P.ns && !(P.tune & 32768)) {   // (A/B) tune 32768: no tile stores
         double* g = out + (size_t)t_t * P.ns + s0 + c_t;
         const size_t gstep = (size_t)TSTEP * P.ns;
 #pragma unroll
@@ -197,6 +214,247 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
   }
   cp_async_wait_all();
   if (P.amax) warp_atomic_max_abs(P.amax, lmax);
+}
+
+
+
+// ------------------------------------------------------------------ fused 2D time pass, 3-stage
+// Same mathematics and per-group tiling as k_time2d_v2 (a group of 4 warps owns an NT x S tile),
+// but one CTA per SM runs TWO groups over THREE tile buffers so the HBM traffic of one tile
+// overlaps the FFTs of the others: tile k of the CTA belongs to group k % 2 and buffer k % 3; after
+// group g has read tile k's outputs back into registers it issues the cp.async loads of tile k + 3
+// into the freed buffer (completion tracked by an mbarrier through cp.async.mbarrier.arrive, so
+// the OTHER group can wait for them) and then stores its outputs.  Measured without loads/stores
+// (tune 49152) the c5 time pass takes 8.2 ms against 12.1 ms with them: the 3.9 ms of exposed
+// memory phases is what this schedule hides.  Groups synchronise on named barriers only.
+template <int E, int FLAGS>
+__global__ void __launch_bounds__(256, 1)
+k_time2d_v3(const double* in, double* out, TimeParams P) {
+  constexpr int GW = 4;                                       // warps per group
+  constexpr int NT = 32 * E, PP = 32 / E, S = 2 * PP * GW, LD = S + 1;
+  constexpr int CPT = S > GW * 32 ? S / (GW * 32) : 1;        // points per thread (N_t = 32)
+  constexpr int TSTEP = CPT > 1 ? 1 : GW * 32 / S;
+  constexpr size_t TILED = (size_t)NT * LD, SCRD = (size_t)GW * kWarpBufD;
+  constexpr size_t BUFD = ((TILED > SCRD ? TILED : SCRD) + 1) & ~(size_t)1;   // doubles per buffer
+  extern __shared__ double2 smem2[];
+  double* bufs = reinterpret_cast<double*>(smem2);
+  // the FFT roots W_NT^i and d_l live in shared memory: the three tile buffers leave only ~8 KB of
+  // L1, in which the tables would thrash (measured: 16.7 ms with them in global vs 12.3 for v2)
+  double2* s_tw = reinterpret_cast<double2*>(bufs + 3 * BUFD);
+  double2* s_dl = s_tw + NT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_dl + NT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / GW, gw = warp - g * GW, gt = threadIdx.x - g * GW * 32;
+  {
+    const int sh = P.twlog - (5 + ilog2_c(E));
+    for (int i = threadIdx.x; i < NT; i += 256) {
+      s_tw[i] = __ldg(P.tw + ((size_t)i << sh));
+      s_dl[i] = __ldg(P.dl + i);
+    }
+  }
+  const int64_t ntiles = (P.ns + S - 1) / S;
+  const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;   // tiles of this CTA
+  const double jbar = P.kind >= 2 ? P.st->jbar : 0.0;
+  const int c_t = CPT > 1 ? gt : gt % S, t_t = CPT > 1 ? 0 : gt / S;
+  auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GW * 32) : "memory"); };
+  // cp.async of the CTA's k-th tile into buffer k % 3 by the calling group's 128 threads, then one
+  // deferred arrival each on full[k % 3] (count 128).  Dead points (past N_s) copy the last live
+  // point (finite data; their outputs are never stored).
+  auto issue = [&](int64_t k) {
+    const int64_t s0 = (blockIdx.x + k * gridDim.x) * S;
+    double* sm = bufs + (size_t)(k % 3) * BUFD;
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = c_t + cc * GW * 32;
+      const int64_t sc = s0 + c < P.ns ? s0 + c : P.ns - 1;
+      double* d = sm + t_t * LD + c;
+      const double* src = in + (size_t)t_t * P.ns + sc;
+      const size_t gstep = (size_t)TSTEP * P.ns;
+#pragma unroll 4
+      for (int t = t_t; t < NT; t += TSTEP, d += TSTEP * LD, src += gstep) cp_async8(d, src);
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + k % 3)) : "memory");
+  };
+  if (threadIdx.x < 3) mbar_init(full + threadIdx.x, GW * 32);
+  if (threadIdx.x == 0) fence_mbar_init();
+  __syncthreads();
+  if (g == 0)
+    for (int64_t k = 0; k < 3 && k < mine; ++k) issue(k);
+  for (int64_t k = g; k < mine; k += 2) {
+    const int64_t s0 = (blockIdx.x + k * gridDim.x) * S;
+    double* sm = bufs + (size_t)(k % 3) * BUFD;
+    mbar_wait(full + k % 3, (unsigned)((k / 3) & 1));
+    double2 v[32];
+#pragma unroll
+    for (int p = 0; p < PP; ++p) {
+      const int c = 2 * (gw * PP + p);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = lane + 32 * e;
+        const double gm = (FLAGS & 2) ? 1.0 : (P.gamma_folded ? 1.0 : __ldg(P.gam + t));
+        v[p * E + e] = make_double2(sm[t * LD + c] * gm, sm[t * LD + c + 1] * gm);
+      }
+    }
+    gbar();                                                   // tile in registers: scratch may reuse it
+    time_solve_regs<E, PP, FLAGS, true>(v, reinterpret_cast<double2*>(sm) + (size_t)gw * (kWarpBufD / 2),
+                                        s0 + 2 * gw * PP, lane, P, jbar, s_tw, 5 + ilog2_c(E), s_dl);
+    gbar();
+#pragma unroll
+    for (int p = 0; p < PP; ++p) {
+      const int c = 2 * (gw * PP + p);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = lane + 32 * e;
+        const double gi = ((FLAGS & 2) || P.gamma_folded) ? 1.0 : __ldg(P.ginv + t);
+        sm[t * LD + c] = v[p * E + e].x * gi;
+        sm[t * LD + c + 1] = v[p * E + e].y * gi;
+      }
+    }
+    gbar();
+    constexpr int NV = NT / TSTEP;
+    double ov[CPT][NV];
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) ov[cc][i] = sm[(t_t + i * TSTEP) * LD + c_t + cc * GW * 32];
+    gbar();                                                   // buffer k % 3 is free
+    if (k + 3 < mine) issue(k + 3);
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = c_t + cc * GW * 32;
+      if (s0 + c < P.ns) {
+        double* dst = out + (size_t)t_t * P.ns + s0 + c;
+        const size_t gstep = (size_t)TSTEP * P.ns;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) dst[i * gstep] = ov[cc][i];
+      }
+    }
+  }
+  cp_async_wait_all();
+}
+
+
+// ------------------------------------------------------------------ fused 2D time pass, 3-stage TMA
+// k_time2d_v3's schedule (two groups of 4 warps over three tile buffers, one CTA per SM) with the
+// tiles moved by the Tensor Memory Accelerator: the pass runs in place on the handle's second
+// workspace W2, whose slice pitch ps = N_s rounded up to even makes every tile row 16-byte aligned
+// (tma.cuh: an unaligned box start is an illegal instruction).  A tile is NT/RB x S/16 boxes of
+// {16 points, RB = min(NT, 256) slices}, SWIZZLE_128B, so the 16-byte pencil-pair reads of 8
+// consecutive slices hit 8 distinct bank groups.  One leader thread per group issues the bulk tensor
+// stores of its tile and, once they have read shared memory, the loads of the CTA's tile k + 3
+// into the same buffer (mbarrier transaction count).  The ragged last tile needs no special case:
+// loads past the pitch are zero-filled and stores clipped; the pad column (index N_s) is kept
+// finite (zeroed at init) because it shares a complex pencil with point N_s - 1.  The profiling
+// of k_time2d_v3 showed 33% of its stall samples in the 8-byte cp.async issue loop.
+template <int E, int FLAGS>
+__global__ void __launch_bounds__(256, 1)
+k_time2d_v4(const __grid_constant__ CUtensorMap tmap, TimeParams P) {
+  constexpr int GW = 4;
+  constexpr int NT = 32 * E, PP = 32 / E, S = 2 * PP * GW;
+  constexpr int RB = NT < 256 ? NT : 256, NRB = NT / RB, NCH = S / 16;
+  constexpr unsigned BOXB = 16u * RB * 8u, TILEB = (unsigned)S * NT * 8u;
+  constexpr size_t SCRB = (size_t)GW * kWarpBufD * 8;
+  constexpr size_t BUFB = ((TILEB > SCRB ? TILEB : SCRB) + 1023) & ~(size_t)1023;
+  static_assert(S % 16 == 0, "TMA time tile");
+  extern __shared__ __align__(1024) unsigned char smem_tma[];   // 1024-byte aligned: SWIZZLE_128B boxes
+  unsigned char* base = smem_tma;
+  double2* s_tw = reinterpret_cast<double2*>(base + 3 * BUFB);
+  double2* s_dl = s_tw + NT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_dl + NT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / GW, gw = warp - g * GW, gt = threadIdx.x - g * GW * 32;
+  const int64_t ntiles = (P.ns + S - 1) / S;
+  // tiles 2j, 2j+1 of pair j = blockIdx.x + i·gridDim.x; the CTA's k-th tile is tile_of(k) (< ntiles)
+  const int64_t npairs = (ntiles + 1) / 2;
+  const int64_t mypairs = npairs > blockIdx.x ? (npairs - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t mine = 2 * mypairs - ((ntiles & 1) && (npairs - 1) % gridDim.x == blockIdx.x ? 1 : 0);
+  const double jbar = P.kind >= 2 ? P.st->jbar : 0.0;
+  auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GW * 32) : "memory"); };
+  auto off = [&](int t, int c) -> unsigned {
+    return (unsigned)(((c >> 4) * NRB + t / RB) * BOXB) + sw128(t % RB, c & 15);
+  };
+  // the two groups take neighbouring tiles (2j, 2j+1) of the CTA's pair j: their 128-byte rows share
+  // the 256-byte segments the L2 promotes on the first load
+  auto tile_of = [&](int64_t k) { return 2 * ((int64_t)blockIdx.x + (k >> 1) * gridDim.x) + (k & 1); };
+  auto issue = [&](int64_t k) {                               // one thread: tile k -> buffer k % 3
+    unsigned char* buf = base + (size_t)(k % 3) * BUFB;
+    mbar_expect_tx(full + k % 3, TILEB);
+    const int s0 = (int)(tile_of(k) * S);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb) tma_load_2d(buf + (ch * NRB + rb) * BOXB, &tmap, s0 + 16 * ch, rb * RB, full + k % 3);
+  };
+  {
+    const int sh = P.twlog - (5 + ilog2_c(E));
+    for (int i = threadIdx.x; i < NT; i += 256) {
+      s_tw[i] = __ldg(P.tw + ((size_t)i << sh));
+      s_dl[i] = __ldg(P.dl + i);
+    }
+  }
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int b = 0; b < 3; ++b) mbar_init(full + b, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int64_t k = 0; k < 3 && k < mine; ++k) issue(k);
+  // the leader waits for its stores to have read the buffer (and issues the next load into it) only
+  // after its group has taken the NEXT tile into registers, so the group never waits on the store
+  int64_t pend = -1;
+  auto flush = [&]() {
+    if (gt == 0 && pend >= 0) {
+      tma_wait_read_all();
+      issue(pend);
+    }
+    pend = -1;
+  };
+  for (int64_t k = g; k < mine; k += 2) {
+    const int64_t s0 = tile_of(k) * S;
+    unsigned char* buf = base + (size_t)(k % 3) * BUFB;
+    mbar_wait(full + k % 3, (unsigned)((k / 3) & 1));
+    double2 v[32];
+#pragma unroll
+    for (int p = 0; p < PP; ++p) {
+      const int c = 2 * (gw * PP + p);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = lane + 32 * e;
+        const double2 x = *reinterpret_cast<const double2*>(buf + off(t, c));
+        const double gm = (FLAGS & 2) ? 1.0 : (P.gamma_folded ? 1.0 : __ldg(P.gam + t));
+        v[p * E + e] = make_double2(x.x * gm, x.y * gm);
+      }
+    }
+    gbar();                                                   // tile in registers: scratch may reuse it
+    flush();
+    time_solve_regs<E, PP, FLAGS, true>(v, reinterpret_cast<double2*>(buf) + (size_t)gw * (kWarpBufD / 2),
+                                        s0 + 2 * gw * PP, lane, P, jbar, s_tw, 5 + ilog2_c(E), s_dl);
+    gbar();
+#pragma unroll
+    for (int p = 0; p < PP; ++p) {
+      const int c = 2 * (gw * PP + p);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = lane + 32 * e;
+        const double gi = ((FLAGS & 2) || P.gamma_folded) ? 1.0 : __ldg(P.ginv + t);
+        *reinterpret_cast<double2*>(buf + off(t, c)) = make_double2(v[p * E + e].x * gi, v[p * E + e].y * gi);
+      }
+    }
+    fence_proxy_async();
+    gbar();
+    if (gt == 0) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb)
+          tma_store_2d(&tmap, (int)s0 + 16 * ch, rb * RB, buf + (ch * NRB + rb) * BOXB);
+      tma_commit();
+    }
+    if (k + 3 < mine) pend = k + 3;                          // buffer k % 3 -> tile k + 3 (see flush)
+  }
+  flush();
+  if (gt == 0) tma_wait_all();
 }
 
 }  // namespace pd

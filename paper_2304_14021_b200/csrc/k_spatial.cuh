@@ -56,6 +56,7 @@ struct LineParams {
   const double* oscale;  // k_cols3 only: outputs of slice n scaled by oscale[n] (NULL = 1)
   int stagger_ns;        // k_cols3: start delay of the second CTA of each SM (phase offset)
   SegMap sin, sout;      // k_rows3 / k_cols3: transpose-block input / output (n = 0: plain)
+  int64_t ps_in, ps_out; // k_cols3: slice pitch of in / out (ns, or the even pitch of the TMA workspace)
 };
 
 // buffer index of stored element e: Neumann x_e = node e; hinged x_{e+1} = interior node e+1

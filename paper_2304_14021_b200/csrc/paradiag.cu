@@ -4,6 +4,8 @@
 // update U ← U + ω δ.  2D pass order (spatial-first):
 //   x-DTT (r → δ) · y-DTT · fused time pass (Γ_α·DFT · per-mode divide · IDFT·Γ_α⁻¹) · y-DTT · x-DTT
 // 1D: time DFT → batched pentadiagonal solves per bin → inverse time DFT.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -76,6 +78,31 @@ constexpr int kLineWarps = 4;   // spatial DTT rows: one warp per row, 4 rows pe
 constexpr int kColW = PD_COLW;  // spatial DTT columns: adjacent columns per CTA (one warp each)
 
 bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// 2D tensor map of an [outer][pitch] fp64 array (inner extent `inner` <= pitch), boxes {box_w,
+// box_h}, SWIZZLE_128B, 256-byte L2 promotion (measured faster than none for 128-byte box rows even
+// though it over-reads when the neighbouring row segment is not used soon, ncu r02h).  The encoder is the driver's cuTensorMapEncodeTiled, resolved through the
+// runtime (no -lcuda).  TMA needs 16-byte aligned rows: pitch even (tma.cuh).
+bool make_map_2d(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t pitch, unsigned box_w,
+                 unsigned box_h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !enc) {
+      enc = nullptr;
+      return false;
+    }
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (pitch & 1) || box_h > 256 || box_w * 8 > 128) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)(pitch * 8)};
+  const cuuint32_t box[2] = {box_w, box_h};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 int ilog2(int64_t v) {
   int l = 0;
   while ((int64_t(1) << l) < v) ++l;
@@ -93,6 +120,11 @@ struct pd_handle {
   int log2nt = 0, log2h = 0, twlog = 0, nb = 0;
   bool neumann = true;
   bool fast = true;                   // register-FFT kernels (k_fast.cuh) where sizes allow
+  bool tma = true;                    // PARADIAG_TMA=0: cp.async-staged time pass instead of TMA (A/B)
+  // TMA time pass (k_time2d_v4): second workspace [nt][ps], ps = ns rounded up to even (16-byte rows);
+  // the forward y pass writes it, the time pass runs in place on it, the inverse y pass reads it
+  double* wt = nullptr;
+  int64_t ps = 0;
   double inv_dt = 0, inv_h2 = 0, b2 = 0, e2 = 0;
   // device buffers
   double* work = nullptr;             // 2D: δ/r workspace [nt][ns]; 1D: r [nt][nx]
@@ -390,6 +422,7 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.umax = upd ? &h->st->umax_bits : nullptr;
   L.sin.n = 0;
   L.sout.n = 0;
+  L.ps_in = L.ps_out = h->ns;
   return L;
 }
 
@@ -415,9 +448,11 @@ bool fast_line_any(pd_handle* h, const double* in, double* out, int axis, const 
 }
 
 int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid,
-                 double* upd = nullptr, const double* oscale = nullptr) {
+                 double* upd = nullptr, const double* oscale = nullptr, int64_t ps_in = 0, int64_t ps_out = 0) {
   LineParams L = line_params(h, axis, amax, upd);
   L.oscale = oscale;
+  if (ps_in) L.ps_in = ps_in;
+  if (ps_out) L.ps_out = ps_out;
   prof_begin(h, kid);
   const bool fast = h->fast && fast_line_any(h, in, out, axis, L);
   if (!fast) {
@@ -534,11 +569,34 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     // Γ_α (forward outputs) and Γ_α⁻¹·1/(N_t (2m)²) (inverse outputs) for the time pass
     const bool fold = !h->tlong && h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
                       h->P.nt <= 1024;
+    const bool use_wt = h->wt && h->dtt_ver == 3 && !(h->tune & 65536);
+    double* yb = use_wt ? h->wt : delta;          // y-pass output / time-pass buffer
+    const int64_t yps = use_wt ? h->ps : h->ns;
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
-    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) return rc;
+    if ((rc = launch_lines(h, delta, yb, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr, h->ns, yps))) return rc;
     TimeParams T = time_params(h, nullptr);
     T.gamma_folded = fold ? 1 : 0;
-    if (h->tlong) {
+    bool done = false;
+    if (use_wt) {                                 // TMA-staged three-stage time pass (k_time2d_v4)
+      CUtensorMap m;
+      const unsigned rb = (unsigned)std::min<int64_t>(h->P.nt, 256);
+      if (!make_map_2d(&m, h->wt, h->ps, h->P.nt, h->ps, 16, rb)) return fail(PD_ECUDA, "tensor map encode failed");
+      const FastLaunch F = fast_launch(h);
+      prof_begin(h, K_TIME);
+      switch (h->P.nt) {
+        case 32: done = fast_time_tma<1>(h->wt, T, F, &m); break;
+        case 64: done = fast_time_tma<2>(h->wt, T, F, &m); break;
+        case 128: done = fast_time_tma<4>(h->wt, T, F, &m); break;
+        case 256: done = fast_time_tma<8>(h->wt, T, F, &m); break;
+        case 512: done = fast_time_tma<16>(h->wt, T, F, &m); break;
+        default: break;
+      }
+      prof_end(h, K_TIME);
+      PD_LAUNCHED();
+      if (!done) return fail(PD_EINVAL, "TMA time pass: unsupported N_t");
+    }
+    if (done) {
+    } else if (h->tlong) {
       if ((rc = tlong_time(h, delta, delta))) return rc;
     } else {
     prof_begin(h, K_TIME);
@@ -556,7 +614,7 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     }
-    if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) return rc;
+    if ((rc = launch_lines(h, yb, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr, yps, h->ns))) return rc;
     if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
     if ((rc = launch_lines(h, delta, delta, 0, want_dmax ? dmax : nullptr, K_XINV))) return rc;
     return PD_OK;
@@ -1037,6 +1095,8 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
   else if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
+  // TMA time pass workspace (2D, 32 <= nt <= 512, 64 <= m <= 2048): one more iterate-sized array
+  if (p->dim == 2 && !tl && p->nt >= 32 && p->nt <= 512 && p->m >= 64 && p->m <= 2048) b += p->nt * (ns + 1) * sizeof(double);
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
   if (p->jacobian == PD_JACOBIAN_TIME_AVG) b += (size_t)(kKryM + 2) * total * sizeof(double) + 2 * ns * sizeof(double);
   *bytes = b;
@@ -1351,9 +1411,17 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     }
     if (const char* f = std::getenv("PARADIAG_FAST")) h->fast = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_DTT")) h->dtt_ver = std::atoi(f) == 4 ? 4 : 3;
+    if (const char* f = std::getenv("PARADIAG_TMA")) h->tma = std::atoi(f) != 0;
     if (const char* f = std::getenv("PARADIAG_TUNE")) h->tune = std::atoi(f);
     if (const char* f = std::getenv("PARADIAG_STAGGER")) h->stagger_ns = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
+    if (h->tma && h->fast && !slab && !h->tlong && nt >= 32 && nt <= 512 && p->m >= 64 && p->m <= 2048) {
+      h->ps = (h->ns + 1) & ~(int64_t)1;
+      PD_TRY(dalloc(h, &h->wt, (size_t)nt * h->ps));
+      // the pad column shares a complex pencil with point ns-1 in the time pass: keep it finite
+      if (cudaMemsetAsync(h->wt, 0, (size_t)nt * h->ps * sizeof(double), h->stream) != cudaSuccess)
+        return cleanup(fail(PD_ECUDA, "wt memset"));
+    }
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));
 #undef PD_TRY

@@ -38,11 +38,8 @@ def sample_points(p, count, seed):
     return pts
 
 
-def rounding_floor_1d(p, r, d_lu):
-    """The rounding floor of this P_α⁻¹ instance: the oracle's own Step (2) solved a second, equally
-    exact way (the eigenbasis divide the GPU uses, as oracle.precond.step2_2d does in 2D) differs
-    from its banded-LU result by this much; 1D Neumann instances near the growing modes of linear
-    CH (μ < 0, P:389) sit at ~3e-12."""
+def eigenbasis_precond_1d(p, r):
+    """The oracle's Step (2) solved in the eigenbasis (the method the GPU's long-window path uses)."""
     from oracle import circulant, spatial
     S1 = circulant.step1(r, p.alpha)
     d = circulant.eig_d(p.nt, p.alpha, circulant.inv_dt(p))
@@ -51,4 +48,12 @@ def rounding_floor_1d(p, r, d_lu):
     mu = spatial.mu(spatial.Lam_grid(p), p).reshape(-1)
     S2 = ((S1 @ T.T) / (d[:, None] + e[:, None] * mu[None, :])) @ T.T / (2.0 * p.m)
     d_sp, _ = circulant.step3(S2, p.alpha)
-    return rel_err(d_sp, d_lu)
+    return d_sp
+
+
+def rounding_floor_1d(p, r, d_lu):
+    """The rounding floor of this P_α⁻¹ instance: the oracle's own Step (2) solved a second, equally
+    exact way (the eigenbasis divide the GPU uses, as oracle.precond.step2_2d does in 2D) differs
+    from its banded-LU result by this much; 1D Neumann instances near the growing modes of linear
+    CH (μ < 0, P:389) sit at ~3e-12."""
+    return rel_err(eigenbasis_precond_1d(p, r), d_lu)
