@@ -31,6 +31,11 @@ template <int E>
 cudaError_t fast_attrs();
 template <int E>
 void fast_line(int neumann, int axis, const double* in, double* out, const LineParams& L, const FastLaunch& F);
+// y pass between the natural layout and the column-major workspace (k_cols_cm): dir 0 natural -> wt,
+// dir 1 wt -> natural; lp = wt line pitch
+template <int E>
+void fast_cols_cm(int neumann, int dir, const double* in, double* out, const LineParams& L, const FastLaunch& F,
+                  int64_t lp);
 template <int E>
 void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F);
 // TMA-staged three-stage time pass (k_time2d_v4), in place on the buffer tmap describes: [N_t][ps]
@@ -39,11 +44,6 @@ template <int E>
 bool fast_time_tma(double* buf, const TimeParams& T, const FastLaunch& F, const CUtensorMap* tmap);
 
 #ifdef PD_FAST_DEFINE
-template <int E>
-constexpr size_t fast_time3_smem() {
-  constexpr size_t S = 2 * (32 / E) * 4, tile = (size_t)32 * E * (S + 1), scr = (size_t)4 * kWarpBufD;
-  return (3 * (((tile > scr ? tile : scr) + 1) & ~(size_t)1)) * 8 + (size_t)2 * 32 * E * 16 + 3 * 8;
-}
 template <int E>
 constexpr size_t fast_time4_smem() {
   constexpr size_t S = 2 * (32 / E) * 4, tile = (size_t)S * 32 * E * 8, scr = (size_t)4 * kWarpBufD * 8;
@@ -75,12 +75,6 @@ cudaError_t fast_attrs() {
     PD_ATTR((k_time2d_v4<E, 2>), fast_time4_smem<E>());
     PD_ATTR((k_time2d_v4<E, 3>), fast_time4_smem<E>());
   }
-  if constexpr (fast_time3_smem<E>() <= 227 * 1024) {
-    PD_ATTR((k_time2d_v3<E, 0>), fast_time3_smem<E>());
-    PD_ATTR((k_time2d_v3<E, 1>), fast_time3_smem<E>());
-    PD_ATTR((k_time2d_v3<E, 2>), fast_time3_smem<E>());
-    PD_ATTR((k_time2d_v3<E, 3>), fast_time3_smem<E>());
-  }
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 0>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 1>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 2>), fast_time_smem(E));
@@ -94,6 +88,10 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
+  PD_ATTR((k_cols_cm<1, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols_cm<0, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols_cm<1, E, fast_col_warps(E), 1>), dtt3_cols_smem<E>());
+  PD_ATTR((k_cols_cm<0, E, fast_col_warps(E), 1>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<1, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<0, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols3<1, E, fast_col_warps(E), 2>), dtt3_cols_smem<E>());
@@ -168,19 +166,6 @@ void fast_time(const double* in, double* out, const TimeParams& T, const FastLau
   constexpr int S = 2 * (32 / E) * kFastTimeWarps;
   const int64_t tiles = (F.ns + S - 1) / S;
   const int flags = ((!T.el && !T.l3) ? 1 : 0) | (T.gamma_folded ? 2 : 0);
-  if constexpr (fast_time3_smem<E>() <= 227 * 1024) {
-    if (!(T.tune & 65536) && !T.amax) {     // 3-stage two-group schedule (tune 65536: the 2-CTA kernel)
-      const unsigned grid3 = (unsigned)std::min<int64_t>((tiles + 1) / 2, 148);
-      constexpr size_t sm3 = fast_time3_smem<E>();
-      switch (flags) {
-        case 3: k_time2d_v3<E, 3><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
-        case 2: k_time2d_v3<E, 2><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
-        case 1: k_time2d_v3<E, 1><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
-        default: k_time2d_v3<E, 0><<<grid3, 256, sm3, F.stream>>>(in, out, T); break;
-      }
-      return;
-    }
-  }
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
   const size_t sm = fast_time_smem(E);
   constexpr int NWT = kFastTimeWarps;
@@ -214,7 +199,25 @@ bool fast_time_tma(double* buf, const TimeParams& T, const FastLaunch& F, const 
   }
 }
 
+template <int E>
+void fast_cols_cm(int neumann, int dir, const double* in, double* out, const LineParams& L, const FastLaunch& F,
+                  int64_t lp) {
+  constexpr int NW = fast_col_warps(E);
+  constexpr int C = NW * (32 / E);
+  const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+  const size_t sm = dtt3_cols_smem<E>();
+  if (neumann) {
+    if (dir == 0) k_cols_cm<1, E, NW, 0><<<grid, NW * 32, sm, F.stream>>>(in, out, L, F.trig2, lp);
+    else k_cols_cm<1, E, NW, 1><<<grid, NW * 32, sm, F.stream>>>(in, out, L, F.trig2, lp);
+  } else {
+    if (dir == 0) k_cols_cm<0, E, NW, 0><<<grid, NW * 32, sm, F.stream>>>(in, out, L, F.trig2, lp);
+    else k_cols_cm<0, E, NW, 1><<<grid, NW * 32, sm, F.stream>>>(in, out, L, F.trig2, lp);
+  }
+}
+
 #define PD_FAST_INSTANTIATE(E)                                                                       \
+  template void fast_cols_cm<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&, int64_t); \
   template bool fast_time_tma<E>(double*, const TimeParams&, const FastLaunch&, const CUtensorMap*); \
   template cudaError_t fast_attrs<E>();                                                             \
   template void fast_line<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&); \

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "fft4.cuh"
 #include "k_spatial.cuh"
+#include "tma.cuh"
 
 namespace pd {
 
@@ -542,6 +543,161 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
   }
   if (V == 1 || (GEN && L.amax)) warp_atomic_max_abs(L.amax, lmax);
   if (GEN && L.sout.n) __threadfence_system();   // block stores may target a peer GPU (peer-memory transposes)
+}
+
+
+// ---------------------------------------------------------------- columns <-> column-major workspace
+// The y passes next to the TMA time pass (k_time2d_v4) exchange data with the second workspace wt,
+// which holds every slice COLUMN-MAJOR: line x (all y) at wt + n·ps + x·lp, line pitch lp = N_y
+// rounded up to even (16-byte aligned lines), slice pitch ps = N_x·lp.  The time pass is pointwise
+// in space, and on a square grid the mode eigenvalue λ_p + λ_q is symmetric in (p, q), so it runs
+// on this layout unchanged (TimeParams.nx = lp decodes the mode; pads are finite, their output is
+// never read).  What changes is the y pass's wt side: one whole contiguous line per warp
+// (coalesced, like a row pass) instead of a 64-byte-wide column tile — the forward pass stores its
+// lines with store_line, the inverse pass loads them with one 8-byte cp.async per lane and
+// element.  The natural-layout side keeps k_cols3's column-tile staging.
+// DIR 0: in natural [n][y][x] (slice pitch L.ps_in) -> out column-major wt;
+// DIR 1: in column-major wt -> out natural [n][y][x] (slice pitch L.ps_out).  L.upd unused.
+template <int NEUMANN, int E, int NW, int DIR>
+__global__ void __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1)
+k_cols_cm(const double* in, double* out, LineParams L, const double2* __restrict__ trig2, int64_t lp) {
+  using D = Dtt3<NEUMANN, E>;
+  constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;
+  constexpr int C = NW * D::P;
+  constexpr int NTH = NW * 32;
+  constexpr int RSTEP = NTH / C;
+  static_assert(64 % RSTEP == 0, "row step must divide 64");
+  constexpr int PER = 64 / RSTEP;
+  constexpr int KB = (kNel + 63) / 64;
+  extern __shared__ double2 smem2[];
+  double* base = reinterpret_cast<double*>(smem2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xb = base + (size_t)warp * D::BUF;
+  const int64_t gx = (L.nx + C - 1) / C;
+  const int64_t nsl = L.nlines / L.nx;
+  const int64_t ngroups = nsl * gx;
+  const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
+  const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
+  const int64_t cps = (int64_t)L.nx * lp;                       // column-major slice pitch
+  // DIR 1, Neumann: each wt line (lp doubles, pad included, 16-byte aligned) is ONE bulk copy into
+  // its line buffer, completion on an mbarrier (no per-element cp.async issue loop)
+  constexpr bool BULK = DIR == 1 && NEUMANN;
+  __shared__ uint64_t bar;
+  unsigned phase = 0;
+  if (BULK) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  auto issue = [&](int64_t G) {
+    const int64_t n = G / gx;
+    const int x0 = (int)((G - n * gx) * C);
+    const int wcols = min(C, (int)(L.nx - x0));
+    if (DIR == 0) {                                               // natural columns -> line buffers
+      if (c_t < wcols) {
+        double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
+        const double* s = in + n * L.ps_in + x0 + (int64_t)e_t * L.nx + c_t;
+        const int64_t rstride = (int64_t)RSTEP * L.nx;
+        for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.nx) {
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            if (e0 + j * RSTEP < kNel) cp_async8(lb + j * RSTEP, s + j * rstride);
+        }
+      }
+    } else if (BULK) {
+      if (threadIdx.x == 0) {
+        const int nl = min(C, (int)(L.nx - x0));
+        fence_proxy_async();                                      // the buffers' generic reads come first
+        mbar_expect_tx(&bar, (unsigned)(nl * lp * 8));
+        for (int c = 0; c < nl; ++c) {
+          const int w = c / D::P, p = c - w * D::P;
+          const double* src = in + n * cps + (int64_t)(x0 + c) * lp;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(base + (size_t)w * D::BUF + p * D::LDX)), "l"(src), "r"((unsigned)(lp * 8)),
+                         "r"(smem_u32(&bar)) : "memory");
+        }
+      }
+    } else {                                                      // contiguous wt lines, warp by warp
+#pragma unroll
+      for (int p = 0; p < D::P; ++p) {
+        const int x = x0 + warp * D::P + p;
+        if (x < L.nx) {
+          double* lb = xb + p * D::LDX + (NEUMANN ? 0 : 1);
+          const double* s = in + n * cps + (int64_t)x * lp;
+          for (int e = lane; e < kNel; e += 32) cp_async8(lb + e, s + e);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  if (blockIdx.x < ngroups) issue(blockIdx.x);
+  for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
+    const int64_t n = G / gx;
+    const int x0 = (int)((G - n * gx) * C);
+    const int wcols = min(C, (int)(L.nx - x0));
+    if (!NEUMANN) {
+      for (int p = lane; p < D::P; p += 32) {
+        xb[p * D::LDX] = 0.0;
+        xb[p * D::LDX + D::M] = 0.0;
+      }
+    }
+    if (BULK) {
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
+    if (DIR == 0) {
+      // each warp takes its staged line(s) into registers (the transform's registers are dead), the
+      // CTA syncs, the next tile's loads are issued into the freed buffers, then the lines are stored
+      // contiguously into wt (coalesced) while those loads are in flight
+      constexpr int NJ = (kNel + 31) / 32;
+      double ov[D::P][NJ];
+#pragma unroll
+      for (int p = 0; p < D::P; ++p)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int q = lane + 32 * j;
+          ov[p][j] = q < kNel ? xb[p * D::LDO + q + (q >> 6)] : 0.0;      // opos(q)
+        }
+      __syncthreads();
+      if (G + gridDim.x < ngroups) issue(G + gridDim.x);
+#pragma unroll
+      for (int p = 0; p < D::P; ++p) {
+        const int x = x0 + warp * D::P + p;
+        if (x < L.nx) {
+          double* d = out + n * cps + (int64_t)x * lp + lane;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (lane + 32 * j < kNel) d[32 * j] = ov[p][j];
+        }
+      }
+    } else {
+      __syncthreads();
+      double ov[KB * PER];
+      const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+          ov[k * PER + j] = (c_t < wcols && e_t + 64 * k + j * RSTEP < kNel) ? ob[65 * k + j * RSTEP] : 0.0;
+      __syncthreads();
+      if (G + gridDim.x < ngroups) issue(G + gridDim.x);
+      if (c_t < wcols) {
+        double* d = out + n * L.ps_out + x0 + (int64_t)e_t * L.nx + c_t;
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            if (e_t + 64 * k + j * RSTEP < kNel) d[(int64_t)(64 * k + j * RSTEP) * L.nx] = ov[k * PER + j];
+      }
+    }
+  }
+  cp_async_wait_all();
 }
 
 }  // namespace pd

@@ -218,125 +218,15 @@ k_time2d_v2(const double* in, double* out, TimeParams P) {
 
 
 
-// ------------------------------------------------------------------ fused 2D time pass, 3-stage
-// Same mathematics and per-group tiling as k_time2d_v2 (a group of 4 warps owns an NT x S tile),
-// but one CTA per SM runs TWO groups over THREE tile buffers so the HBM traffic of one tile
-// overlaps the FFTs of the others: tile k of the CTA belongs to group k % 2 and buffer k % 3; after
-// group g has read tile k's outputs back into registers it issues the cp.async loads of tile k + 3
-// into the freed buffer (completion tracked by an mbarrier through cp.async.mbarrier.arrive, so
-// the OTHER group can wait for them) and then stores its outputs.  Measured without loads/stores
-// (tune 49152) the c5 time pass takes 8.2 ms against 12.1 ms with them: the 3.9 ms of exposed
-// memory phases is what this schedule hides.  Groups synchronise on named barriers only.
-template <int E, int FLAGS>
-__global__ void __launch_bounds__(256, 1)
-k_time2d_v3(const double* in, double* out, TimeParams P) {
-  constexpr int GW = 4;                                       // warps per group
-  constexpr int NT = 32 * E, PP = 32 / E, S = 2 * PP * GW, LD = S + 1;
-  constexpr int CPT = S > GW * 32 ? S / (GW * 32) : 1;        // points per thread (N_t = 32)
-  constexpr int TSTEP = CPT > 1 ? 1 : GW * 32 / S;
-  constexpr size_t TILED = (size_t)NT * LD, SCRD = (size_t)GW * kWarpBufD;
-  constexpr size_t BUFD = ((TILED > SCRD ? TILED : SCRD) + 1) & ~(size_t)1;   // doubles per buffer
-  extern __shared__ double2 smem2[];
-  double* bufs = reinterpret_cast<double*>(smem2);
-  // the FFT roots W_NT^i and d_l live in shared memory: the three tile buffers leave only ~8 KB of
-  // L1, in which the tables would thrash (measured: 16.7 ms with them in global vs 12.3 for v2)
-  double2* s_tw = reinterpret_cast<double2*>(bufs + 3 * BUFD);
-  double2* s_dl = s_tw + NT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_dl + NT);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = warp / GW, gw = warp - g * GW, gt = threadIdx.x - g * GW * 32;
-  {
-    const int sh = P.twlog - (5 + ilog2_c(E));
-    for (int i = threadIdx.x; i < NT; i += 256) {
-      s_tw[i] = __ldg(P.tw + ((size_t)i << sh));
-      s_dl[i] = __ldg(P.dl + i);
-    }
-  }
-  const int64_t ntiles = (P.ns + S - 1) / S;
-  const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;   // tiles of this CTA
-  const double jbar = P.kind >= 2 ? P.st->jbar : 0.0;
-  const int c_t = CPT > 1 ? gt : gt % S, t_t = CPT > 1 ? 0 : gt / S;
-  auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GW * 32) : "memory"); };
-  // cp.async of the CTA's k-th tile into buffer k % 3 by the calling group's 128 threads, then one
-  // deferred arrival each on full[k % 3] (count 128).  Dead points (past N_s) copy the last live
-  // point (finite data; their outputs are never stored).
-  auto issue = [&](int64_t k) {
-    const int64_t s0 = (blockIdx.x + k * gridDim.x) * S;
-    double* sm = bufs + (size_t)(k % 3) * BUFD;
-#pragma unroll
-    for (int cc = 0; cc < CPT; ++cc) {
-      const int c = c_t + cc * GW * 32;
-      const int64_t sc = s0 + c < P.ns ? s0 + c : P.ns - 1;
-      double* d = sm + t_t * LD + c;
-      const double* src = in + (size_t)t_t * P.ns + sc;
-      const size_t gstep = (size_t)TSTEP * P.ns;
-#pragma unroll 4
-      for (int t = t_t; t < NT; t += TSTEP, d += TSTEP * LD, src += gstep) cp_async8(d, src);
-    }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + k % 3)) : "memory");
-  };
-  if (threadIdx.x < 3) mbar_init(full + threadIdx.x, GW * 32);
-  if (threadIdx.x == 0) fence_mbar_init();
-  __syncthreads();
-  if (g == 0)
-    for (int64_t k = 0; k < 3 && k < mine; ++k) issue(k);
-  for (int64_t k = g; k < mine; k += 2) {
-    const int64_t s0 = (blockIdx.x + k * gridDim.x) * S;
-    double* sm = bufs + (size_t)(k % 3) * BUFD;
-    mbar_wait(full + k % 3, (unsigned)((k / 3) & 1));
-    double2 v[32];
-#pragma unroll
-    for (int p = 0; p < PP; ++p) {
-      const int c = 2 * (gw * PP + p);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int t = lane + 32 * e;
-        const double gm = (FLAGS & 2) ? 1.0 : (P.gamma_folded ? 1.0 : __ldg(P.gam + t));
-        v[p * E + e] = make_double2(sm[t * LD + c] * gm, sm[t * LD + c + 1] * gm);
-      }
-    }
-    gbar();                                                   // tile in registers: scratch may reuse it
-    time_solve_regs<E, PP, FLAGS, true>(v, reinterpret_cast<double2*>(sm) + (size_t)gw * (kWarpBufD / 2),
-                                        s0 + 2 * gw * PP, lane, P, jbar, s_tw, 5 + ilog2_c(E), s_dl);
-    gbar();
-#pragma unroll
-    for (int p = 0; p < PP; ++p) {
-      const int c = 2 * (gw * PP + p);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int t = lane + 32 * e;
-        const double gi = ((FLAGS & 2) || P.gamma_folded) ? 1.0 : __ldg(P.ginv + t);
-        sm[t * LD + c] = v[p * E + e].x * gi;
-        sm[t * LD + c + 1] = v[p * E + e].y * gi;
-      }
-    }
-    gbar();
-    constexpr int NV = NT / TSTEP;
-    double ov[CPT][NV];
-#pragma unroll
-    for (int cc = 0; cc < CPT; ++cc)
-#pragma unroll
-      for (int i = 0; i < NV; ++i) ov[cc][i] = sm[(t_t + i * TSTEP) * LD + c_t + cc * GW * 32];
-    gbar();                                                   // buffer k % 3 is free
-    if (k + 3 < mine) issue(k + 3);
-#pragma unroll
-    for (int cc = 0; cc < CPT; ++cc) {
-      const int c = c_t + cc * GW * 32;
-      if (s0 + c < P.ns) {
-        double* dst = out + (size_t)t_t * P.ns + s0 + c;
-        const size_t gstep = (size_t)TSTEP * P.ns;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) dst[i * gstep] = ov[cc][i];
-      }
-    }
-  }
-  cp_async_wait_all();
-}
-
-
 // ------------------------------------------------------------------ fused 2D time pass, 3-stage TMA
-// k_time2d_v3's schedule (two groups of 4 warps over three tile buffers, one CTA per SM) with the
-// tiles moved by the Tensor Memory Accelerator: the pass runs in place on the handle's second
+// Same mathematics and per-group tiling as k_time2d_v2 (a group of 4 warps owns an NT x S tile), but
+// one CTA per SM runs TWO groups over THREE tile buffers so the HBM traffic of one tile overlaps the
+// FFTs of the others: the CTA's tile k belongs to group k % 2 and buffer k % 3, and after group g has
+// stored tile k the buffer receives tile k + 3 (consumed by the other group).  Without loads and
+// stores (tune 49152) the c5 time pass takes 8.2 ms against 12.1 ms for k_time2d_v2: the exposed
+// memory phases are what this schedule hides.  The tiles move by the Tensor Memory Accelerator
+// (with 8-byte cp.async the issue loop took a third of the stall samples and the pass was slower
+// than v2, ncu r02f): the pass runs in place on the handle's second
 // workspace W2, whose slice pitch ps = N_s rounded up to even makes every tile row 16-byte aligned
 // (tma.cuh: an unaligned box start is an illegal instruction).  A tile is NT/RB x S/16 boxes of
 // {16 points, RB = min(NT, 256) slices}, SWIZZLE_128B, so the 16-byte pencil-pair reads of 8
@@ -344,8 +234,7 @@ k_time2d_v3(const double* in, double* out, TimeParams P) {
 // stores of its tile and, once they have read shared memory, the loads of the CTA's tile k + 3
 // into the same buffer (mbarrier transaction count).  The ragged last tile needs no special case:
 // loads past the pitch are zero-filled and stores clipped; the pad column (index N_s) is kept
-// finite (zeroed at init) because it shares a complex pencil with point N_s - 1.  The profiling
-// of k_time2d_v3 showed 33% of its stall samples in the 8-byte cp.async issue loop.
+// finite (zeroed at init) because it shares a complex pencil with point N_s - 1.
 template <int E, int FLAGS>
 __global__ void __launch_bounds__(256, 1)
 k_time2d_v4(const __grid_constant__ CUtensorMap tmap, TimeParams P) {

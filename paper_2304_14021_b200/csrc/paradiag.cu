@@ -121,10 +121,11 @@ struct pd_handle {
   bool neumann = true;
   bool fast = true;                   // register-FFT kernels (k_fast.cuh) where sizes allow
   bool tma = true;                    // PARADIAG_TMA=0: cp.async-staged time pass instead of TMA (A/B)
-  // TMA time pass (k_time2d_v4): second workspace [nt][ps], ps = ns rounded up to even (16-byte rows);
-  // the forward y pass writes it, the time pass runs in place on it, the inverse y pass reads it
+  // TMA time pass (k_time2d_v4): second workspace wt [nt][nx][lp], each slice COLUMN-MAJOR with the
+  // line pitch lp = ny rounded up to even (k_cols_cm); the forward y pass writes it, the time pass
+  // runs in place on it, the inverse y pass reads it
   double* wt = nullptr;
-  int64_t ps = 0;
+  int64_t ps = 0, lp = 0;             // wt slice pitch (nx·lp) and column-major line pitch
   double inv_dt = 0, inv_h2 = 0, b2 = 0, e2 = 0;
   // device buffers
   double* work = nullptr;             // 2D: δ/r workspace [nt][ns]; 1D: r [nt][nx]
@@ -480,6 +481,27 @@ int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned
   return PD_OK;
 }
 
+// y pass between the natural layout and the column-major wt (k_cols_cm): dir 0 forward, 1 inverse
+int launch_cols_cm(pd_handle* h, int dir, const double* in, double* out, int kid, const double* oscale) {
+  LineParams L = line_params(h, 1, nullptr);
+  L.oscale = oscale;
+  const FastLaunch F = fast_launch(h);
+  const int nm = h->neumann ? 1 : 0;
+  prof_begin(h, kid);
+  switch (L.M) {
+    case 64: fast_cols_cm<1>(nm, dir, in, out, L, F, h->lp); break;
+    case 128: fast_cols_cm<2>(nm, dir, in, out, L, F, h->lp); break;
+    case 256: fast_cols_cm<4>(nm, dir, in, out, L, F, h->lp); break;
+    case 512: fast_cols_cm<8>(nm, dir, in, out, L, F, h->lp); break;
+    case 1024: fast_cols_cm<16>(nm, dir, in, out, L, F, h->lp); break;
+    case 2048: fast_cols_cm<32>(nm, dir, in, out, L, F, h->lp); break;
+    default: return fail(PD_EINVAL, "column-major y pass: unsupported line length");
+  }
+  prof_end(h, kid);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
 bool fast_time_any(pd_handle* h, const double* in, double* out, const TimeParams& T) {
   if (!h->fast) return false;
   const FastLaunch F = fast_launch(h);
@@ -569,18 +591,23 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     // Γ_α (forward outputs) and Γ_α⁻¹·1/(N_t (2m)²) (inverse outputs) for the time pass
     const bool fold = !h->tlong && h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
                       h->P.nt <= 1024;
-    const bool use_wt = h->wt && h->dtt_ver == 3 && !(h->tune & 65536);
-    double* yb = use_wt ? h->wt : delta;          // y-pass output / time-pass buffer
-    const int64_t yps = use_wt ? h->ps : h->ns;
+    const bool use_wt = h->wt && h->dtt_ver == 3 && !(h->tune & 65536);   // tune 65536 (A/B): the in-place v2 time pass
     if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
-    if ((rc = launch_lines(h, delta, yb, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr, h->ns, yps))) return rc;
+    if (use_wt) {
+      if ((rc = launch_cols_cm(h, 0, delta, h->wt, K_YFWD, fold ? h->gam : nullptr))) return rc;
+    } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) {
+      return rc;
+    }
     TimeParams T = time_params(h, nullptr);
     T.gamma_folded = fold ? 1 : 0;
     bool done = false;
     if (use_wt) {                                 // TMA-staged three-stage time pass (k_time2d_v4)
+      T.nx = (int)h->lp;                          // column-major wt: mode s = x·lp + y (Λ symmetric)
+      T.ns = h->ps;
       CUtensorMap m;
       const unsigned rb = (unsigned)std::min<int64_t>(h->P.nt, 256);
       if (!make_map_2d(&m, h->wt, h->ps, h->P.nt, h->ps, 16, rb)) return fail(PD_ECUDA, "tensor map encode failed");
+      // (T.nx, T.ns) = (lp, ps): every point of the padded column-major slice is a tile point
       const FastLaunch F = fast_launch(h);
       prof_begin(h, K_TIME);
       switch (h->P.nt) {
@@ -614,7 +641,11 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     }
-    if ((rc = launch_lines(h, yb, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr, yps, h->ns))) return rc;
+    if (use_wt) {
+      if ((rc = launch_cols_cm(h, 1, h->wt, delta, K_YINV, fold ? h->ginv : nullptr))) return rc;
+    } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) {
+      return rc;
+    }
     if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
     if ((rc = launch_lines(h, delta, delta, 0, want_dmax ? dmax : nullptr, K_XINV))) return rc;
     return PD_OK;
@@ -1243,7 +1274,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     if (l > 0 && l < nt - l) l3[nt - l] = make_double2(l3[l].x, -l3[l].y);
   }
   if (p->kind == PD_CAHN_HILLIARD_EYRE) PD_TRY(dalloc(h, &h->l3, nt));
-  PD_TRY(dalloc(h, &h->lam, h->nx));
+  PD_TRY(dalloc(h, &h->lam, h->nx + 1));   // + one finite entry: the pad lines of the column-major wt
   PD_TRY(dalloc(h, &h->tw, TWN));
   PD_TRY(dalloc(h, &h->trig, (size_t)M + 1));
   PD_TRY(dalloc(h, &h->trig2, (size_t)H2));
@@ -1275,7 +1306,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   auto up = [&](void* d, const void* s, size_t b) { return cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, h->stream); };
   if (up(h->gam, gam.data(), nt * sizeof(double)) || up(h->ginv, ginv.data(), nt * sizeof(double)) ||
       up(h->dl, dl.data(), nt * sizeof(double2)) || (h->el && up(h->el, el.data(), nt * sizeof(double2))) ||
-      (h->l3 && up(h->l3, l3.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) ||
+      (h->l3 && up(h->l3, l3.data(), nt * sizeof(double2))) || up(h->lam, lam.data(), h->nx * sizeof(double)) || up(h->lam + h->nx, lam.data() + h->nx - 1, sizeof(double)) ||
       up(h->tw, tw.data(), TWN * sizeof(double2)) || up(h->trig, trig.data(), (M + 1) * sizeof(double2)) ||
       up(h->trig2, trig2.data(), (size_t)H2 * sizeof(double2)) ||
       up(h->trigsc, trigsc.data(), trigsc.size() * sizeof(double2)) ||
@@ -1416,7 +1447,8 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     if (const char* f = std::getenv("PARADIAG_STAGGER")) h->stagger_ns = std::atoi(f);
     PD_TRY(setup_fast_attrs(h));
     if (h->tma && h->fast && !slab && !h->tlong && nt >= 32 && nt <= 512 && p->m >= 64 && p->m <= 2048) {
-      h->ps = (h->ns + 1) & ~(int64_t)1;
+      h->lp = (h->ny + 1) & ~(int64_t)1;        // column-major lines, 16-byte aligned
+      h->ps = (int64_t)h->nx * h->lp;
       PD_TRY(dalloc(h, &h->wt, (size_t)nt * h->ps));
       // the pad column shares a complex pencil with point ns-1 in the time pass: keep it finite
       if (cudaMemsetAsync(h->wt, 0, (size_t)nt * h->ps * sizeof(double), h->stream) != cudaSuccess)
