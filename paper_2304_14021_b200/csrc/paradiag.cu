@@ -412,6 +412,7 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.nlines = (int64_t)h->P.nt * (axis == 0 ? h->ny : h->nx);
   L.nx = h->nx;
   L.ns = h->ns;
+  L.ps_in = L.ps_out = L.ns;
   L.nel = h->nx;
   L.M = (int)h->P.m; L.log2h = h->log2h; L.trig = h->trig; L.tw = h->tw; L.twlog = h->twlog;
   L.trigs = h->trigsc; L.trigc = h->trigsc + std::max((int)h->P.m / 2, 1);
@@ -1867,6 +1868,7 @@ int paradiag_slab_yrange(pd_handle* h, const double* in, double* cols, double* o
   L.nlines = nn * h->nxl;
   L.nx = h->nxl;
   L.ns = slice;
+  L.ps_in = L.ps_out = L.ns;
   L.nel = h->ny;
   F.nt = (int)nn;
   SegMap S;
