@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PARADIAG_ABI_VERSION 4
+#define PARADIAG_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define PD_API __attribute__((visibility("default")))
@@ -140,15 +140,43 @@ PD_API const char* paradiag_strerror(int code);
 /* Detail message of the last failing call on this host thread ("" if none). */
 PD_API const char* paradiag_last_error(void);
 
-/* Device workspace the handle will allocate for `p` (bytes, excluding the caller's U/r/δ).
- * Returns PD_EINVAL if the problem is not supported. */
-PD_API int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes);
+/* Device workspace the handle will allocate for `p` (bytes, excluding the caller's U/r/δ), per
+ * rank when nranks > 1.  Returns PD_EINVAL if the problem is not supported. */
+PD_API int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes);
 
 /* Create a handle on CUDA device `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL =
  * legacy default stream).  Validates the problem (PD_EINVAL), checks the shifted systems for
  * singularity (PD_ESINGULAR), builds the Γ_α / d_l / Λ / twiddle tables and, in 1D, factorises
- * the N_t/2+1 pentadiagonal matrices d_l I + A (no pivoting).  On success *out owns all workspace. */
-PD_API int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle** out);
+ * the N_t/2+1 pentadiagonal matrices d_l I + A (no pivoting).  On success *out owns all workspace.
+ *
+ * Multi-GPU (one process per GPU): with nccl_id != NULL the handle
+ * is rank `rank` of `nranks` (≤ 8) of a slab-sharded 2D linear problem (θ = 1, the register-FFT
+ * sizes 64 ≤ m ≤ 2048, 32 ≤ N_t ≤ 1024; "Step-(2) is fully parallel").  The library creates
+ * and owns the NCCL communicator (ncclCommInitRank with the NCCL the process has loaded — torch's)
+ * and runs the halo exchange, the two all-to-all transposes per P_α⁻¹ and the max all-reduce of
+ * the stop rule itself; the caller passes only its row slab (paradiag_local_rows): u0 [ny_l][nx],
+ * U / r / δ [nt][ny_l][nx].  Every rank must make the same calls in the same order.
+ * nccl_id = NULL and nranks ≤ 1: a single-GPU handle (rank ignored). */
+PD_API int paradiag_init(const pd_problem* p, int device, void* cuda_stream, const unsigned char* nccl_id,
+                         int rank, int nranks, pd_handle** out);
+
+/* A fresh NCCL unique id (128 bytes) for paradiag_init: call on rank 0 only and broadcast it (e.g.
+ * with torch.distributed).  PD_ENCCL if NCCL cannot be resolved (import torch first). */
+PD_API int paradiag_nccl_unique_id(unsigned char id[128]);
+
+/* The rows [y0, y0 + ny_local) of the grid this handle's rank owns (single GPU: 0 and ny). */
+PD_API int paradiag_local_rows(const pd_handle* h, int64_t* y0, int64_t* ny_local);
+
+/* Verification hook of the sharded engine without a multi-GPU box: nranks VIRTUAL ranks in one
+ * process on one device (out[nranks] receives their handles), driven phase by phase in rank order
+ * with the collectives emulated by device copies — no rank ever waits on another.  Same layouts and
+ * kernels as the NCCL path; iterate / solve take the ranks' row-slab pointers in rank order.
+ * Destroy every handle with paradiag_destroy. */
+PD_API int paradiag_init_virtual(const pd_problem* p, int device, void* cuda_stream, int nranks, pd_handle** out);
+PD_API int paradiag_iterate_virtual(pd_handle* const* hs, int nranks, const double* const* u0_l,
+                                    double* const* U_l, pd_iter_info* info);
+PD_API int paradiag_solve_virtual(pd_handle* const* hs, int nranks, const double* const* u0_l,
+                                  double* const* U_l, pd_solve_info* info);
 
 /* Residual r = b - K(U) of the all-at-once system (P:127-149 linear; -G(U) of P:460-463 for CH,
  * mixed form v = U³ - U - ε²Δ_h U, r = Δ_h v - (U_n - U_{n-1})/Δt), with U_0 := u0, stencils in

@@ -63,8 +63,9 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_slab_update_range", "paradiag_ipc_handle", "paradiag_ipc_open", "paradiag_ipc_close",
            "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read", "paradiag_tslab_pitch", "paradiag_tslab_residual", "paradiag_tslab_time",
-           "paradiag_tslab_update"]
-ABI_VERSION = 4
+           "paradiag_tslab_update", "paradiag_nccl_unique_id", "paradiag_local_rows", "paradiag_init_virtual",
+           "paradiag_iterate_virtual", "paradiag_solve_virtual"]
+ABI_VERSION = 5
 GROWTH_LIMIT = 3          # PD_GROWTH_LIMIT
 
 
@@ -81,8 +82,13 @@ def load(path: str = LIB_PATH):
     lib.paradiag_strerror.restype = ctypes.c_char_p
     lib.paradiag_strerror.argtypes = [ctypes.c_int]
     lib.paradiag_last_error.restype = ctypes.c_char_p
-    lib.paradiag_workspace_bytes.argtypes = [P(pd_problem), P(ctypes.c_size_t)]
-    lib.paradiag_init.argtypes = [P(pd_problem), ctypes.c_int, vp, P(vp)]
+    lib.paradiag_workspace_bytes.argtypes = [P(pd_problem), ctypes.c_int, P(ctypes.c_size_t)]
+    lib.paradiag_init.argtypes = [P(pd_problem), ctypes.c_int, vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, P(vp)]
+    lib.paradiag_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.paradiag_local_rows.argtypes = [vp, P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.paradiag_init_virtual.argtypes = [P(pd_problem), ctypes.c_int, vp, ctypes.c_int, P(vp)]
+    lib.paradiag_iterate_virtual.argtypes = [P(vp), ctypes.c_int, P(vp), P(vp), P(pd_iter_info)]
+    lib.paradiag_solve_virtual.argtypes = [P(vp), ctypes.c_int, P(vp), P(vp), P(pd_solve_info)]
     lib.paradiag_residual.argtypes = [vp, vp, vp, vp, P(ctypes.c_double)]
     lib.paradiag_apply_precond.argtypes = [vp, vp, vp, ctypes.c_double]
     lib.paradiag_apply_precond_jt.argtypes = [vp, vp, vp, vp]
@@ -194,20 +200,67 @@ def _check_tensor(t, name, numel, device):
 
 
 # ---------------------------------------------------------------- thin C-ABI mirrors
-def paradiag_workspace_bytes(problem: pd_problem) -> int:
+def paradiag_workspace_bytes(problem: pd_problem, nranks: int = 1) -> int:
     b = ctypes.c_size_t(0)
-    _check(load().paradiag_workspace_bytes(ctypes.byref(problem), ctypes.byref(b)), "paradiag_workspace_bytes")
+    _check(load().paradiag_workspace_bytes(ctypes.byref(problem), int(nranks), ctypes.byref(b)),
+           "paradiag_workspace_bytes")
     return b.value
 
 
-def paradiag_init(problem: pd_problem, device: int = 0, stream=None) -> ctypes.c_void_p:
+def paradiag_init(problem: pd_problem, device: int = 0, stream=None, nccl_id: bytes = None, rank: int = 0,
+                  nranks: int = 1) -> ctypes.c_void_p:
     import torch
     if stream is None:
         stream = torch.cuda.current_stream(device).cuda_stream
+    if nccl_id is not None and len(nccl_id) != 128:
+        raise ParadiagError(PD_EINVAL, "paradiag_init", "nccl_id must be 128 bytes")
     h = ctypes.c_void_p()
-    _check(load().paradiag_init(ctypes.byref(problem), int(device), ctypes.c_void_p(stream), ctypes.byref(h)),
-           "paradiag_init")
+    _check(load().paradiag_init(ctypes.byref(problem), int(device), ctypes.c_void_p(stream), nccl_id, int(rank),
+                                int(nranks), ctypes.byref(h)), "paradiag_init")
     return h
+
+
+def paradiag_nccl_unique_id() -> bytes:
+    """128-byte NCCL id for a sharded paradiag_init (rank 0 only; broadcast it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().paradiag_nccl_unique_id(buf), "paradiag_nccl_unique_id")
+    return buf.raw
+
+
+def paradiag_local_rows(h):
+    y0, n = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load().paradiag_local_rows(h, ctypes.byref(y0), ctypes.byref(n)), "paradiag_local_rows")
+    return y0.value, n.value
+
+
+def paradiag_init_virtual(problem: pd_problem, nranks: int, device: int = 0, stream=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device).cuda_stream
+    hs = (ctypes.c_void_p * nranks)()
+    _check(load().paradiag_init_virtual(ctypes.byref(problem), int(device), ctypes.c_void_p(stream), int(nranks), hs),
+           "paradiag_init_virtual")
+    return [ctypes.c_void_p(h) for h in hs]
+
+
+def _ptr_array(ts, name):
+    return (ctypes.c_void_p * len(ts))(*[_ptr(t, name).value for t in ts])
+
+
+def paradiag_iterate_virtual(hs, u0s, Us, info: pd_iter_info = None) -> pd_iter_info:
+    info = info or pd_iter_info()
+    arr = (ctypes.c_void_p * len(hs))(*[h.value for h in hs])
+    _check(load().paradiag_iterate_virtual(arr, len(hs), _ptr_array(u0s, "u0_l"), _ptr_array(Us, "U_l"),
+                                           ctypes.byref(info)), "paradiag_iterate_virtual")
+    return info
+
+
+def paradiag_solve_virtual(hs, u0s, Us):
+    info = pd_solve_info()
+    arr = (ctypes.c_void_p * len(hs))(*[h.value for h in hs])
+    rc = _check(load().paradiag_solve_virtual(arr, len(hs), _ptr_array(u0s, "u0_l"), _ptr_array(Us, "U_l"),
+                                              ctypes.byref(info)), "paradiag_solve_virtual")
+    return rc, info
 
 
 def paradiag_residual(h, u0, U, r, want_jbar=False):
@@ -406,15 +459,17 @@ def paradiag_destroy(h):
 
 
 class Solver:
-    """Owns a handle; shapes follow the C ABI ([nt][ny][nx] iterates, [ny][nx] u0)."""
+    """Owns a handle; shapes follow the C ABI ([nt][ny][nx] iterates, [ny][nx] u0).  With an NCCL id
+    the handle is one rank of a sharded problem and every buffer is the rank's row slab
+    (self.y0, self.ny rows; see paradiag_init in include/paradiag.h)."""
 
-    def __init__(self, problem, device: int = 0, stream=None):
+    def __init__(self, problem, device: int = 0, stream=None, nccl_id: bytes = None, rank: int = 0, nranks: int = 1):
         self.problem = problem if isinstance(problem, pd_problem) else make_problem(problem)
         self.device = device
-        self.h = paradiag_init(self.problem, device, stream)
+        self.h = paradiag_init(self.problem, device, stream, nccl_id, rank, nranks)
         n = self.problem.m + 1 if self.problem.bc == 0 else self.problem.m - 1
         self.nx = n
-        self.ny = n if self.problem.dim == 2 else 1
+        self.y0, self.ny = paradiag_local_rows(self.h) if self.problem.dim == 2 else (0, 1)
         self.shape = (self.problem.nt, self.ny, self.nx)
 
     def empty(self):

@@ -9,9 +9,22 @@ LIB = os.path.join(HERE, "lib", "libparadiag.so")
 SRC = os.path.join(HERE, "csrc", "paradiag.cu")
 OBJ = os.path.join(HERE, "lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def nccl_include() -> str:
+    """nccl.h of the NCCL torch ships (pip nvidia-nccl): types only — the library resolves the
+    functions at run time from the copy the process has loaded (shard.cu)."""
+    import glob
+    for base in sys.path:
+        hits = glob.glob(os.path.join(base, "nvidia", "nccl", "include", "nccl.h"))
+        if hits:
+            return os.path.dirname(hits[0])
+    return "/usr/include"
+
+
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", nccl_include()]
 
 
 def units():
@@ -54,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed building libparadiag.so")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
-           "-o", LIB + ".tmp"] + objs
+           "-o", LIB + ".tmp"] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -29,6 +29,7 @@
 #include "tlong.h"
 #include "k_x1d.cuh"
 #include "k_krylov.cuh"
+#include "shard.h"
 
 using namespace pd;
 
@@ -113,6 +114,7 @@ int ilog2(int64_t v) {
 
 struct pd_handle {
   pd_problem P{};
+  pd_shard* shard = nullptr;          // multi-rank slab sharding (shard.cu), NULL on a single-GPU handle
   int device = 0;
   cudaStream_t stream = nullptr;
   int nx = 0, ny = 0;
@@ -1114,10 +1116,18 @@ const char* paradiag_strerror(int code) {
 
 const char* paradiag_last_error(void) { return g_last_error.c_str(); }
 
-int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
+int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes) {
   int rc = validate(p);
   if (rc) return rc;
   if (!bytes) return fail(PD_EINVAL, "bytes is NULL");
+  if (nranks > 1) {                  // per rank: row slab, column slab, transpose buffer, halos, tables
+    int nx, ny;
+    geometry(p, &nx, &ny);
+    const size_t per = (size_t)p->nt * nx * ((ny + nranks - 1) / nranks);
+    *bytes = (5 * per + 4 * (size_t)p->nt * 2 * nx) * sizeof(double) +
+             (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
+    return PD_OK;
+  }
   int nx, ny;
   geometry(p, &nx, &ny);
   const size_t ns = (size_t)nx * ny, total = ns * p->nt, nb = p->nt / 2 + 1;
@@ -1137,9 +1147,27 @@ int paradiag_workspace_bytes(const pd_problem* p, size_t* bytes) {
 
 int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** out, bool slab);
 
-int paradiag_init(const pd_problem* p, int device, void* cuda_stream, pd_handle** out) {
-  return init_impl(p, device, cuda_stream, out, false);
+int paradiag_init(const pd_problem* p, int device, void* cuda_stream, const unsigned char* nccl_id, int rank,
+                  int nranks, pd_handle** out) {
+  if (!nccl_id && nranks <= 1) return init_impl(p, device, cuda_stream, out, false);
+  return shard_init(p, device, cuda_stream, nccl_id, rank, nranks, out);
 }
+
+int paradiag_nccl_unique_id(unsigned char id[128]) { return shard_unique_id(id); }
+
+int paradiag_local_rows(const pd_handle* h, int64_t* y0, int64_t* ny_local) {
+  if (!h) return fail(PD_EINVAL, "handle is NULL");
+  if (h->shard) return shard_local_rows(h, y0, ny_local);
+  if (y0) *y0 = 0;
+  if (ny_local) *ny_local = h->ny;
+  return PD_OK;
+}
+
+// internal accessors for shard.cu
+pd_shard*& pd_handle_shard(pd_handle* h) { return h->shard; }
+cudaStream_t pd_handle_stream(const pd_handle* h) { return h->stream; }
+unsigned long long* pd_handle_stats_dev(pd_handle* h) { return &h->st->dmax_bits; }
+int pd_set_error(int code, const char* msg) { return fail(code, msg); }
 
 int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** out, bool slab) {
   if (!out) return fail(PD_EINVAL, "out is NULL");
@@ -1465,6 +1493,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
 int paradiag_residual(pd_handle* h, const double* u0, const double* U, double* r, double* jbar_out) {
   int rc = check_handle(h);
   if (rc) return rc;
+  if (h->shard) return fail(PD_EINVAL, "residual: single-GPU handles only (sharded ranks need the halo exchange)");
   if (!u0 || !U || !r) return fail(PD_EINVAL, "NULL buffer");
   if (r == U) return fail(PD_EINVAL, "r must not alias U");
   if ((rc = launch_residual(h, u0, U, r))) return rc;
@@ -1480,6 +1509,7 @@ int paradiag_apply_precond(pd_handle* h, const double* r, double* delta, double 
   int rc = check_handle(h);
   if (rc) return rc;
   if (!r || !delta) return fail(PD_EINVAL, "NULL buffer");
+  if (h->shard) return shard_apply_precond(h, r, delta);
   if (is_ch(h->P.kind)) {
     k_set_jbar<<<1, 1, 0, h->stream>>>(h->st, jbar);
     PD_LAUNCHED();
@@ -1505,6 +1535,7 @@ int paradiag_iterate(pd_handle* h, const double* u0, double* U, pd_iter_info* in
   int rc = check_handle(h);
   if (rc) return rc;
   if (!u0 || !U || !info) return fail(PD_EINVAL, "NULL argument");
+  if (h->shard) return shard_iterate(h, u0, U, info);
   if (reinterpret_cast<uintptr_t>(U) % 16) return fail(PD_EINVAL, "U must be 16-byte aligned");
   pd_iter_info tmp = *info;
   rc = iteration(h, u0, U, &tmp);
@@ -1519,6 +1550,7 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
   int rc = check_handle(h);
   if (rc) return rc;
   if (!u0 || !U || !info) return fail(PD_EINVAL, "NULL argument");
+  if (h->shard) return shard_solve(h, u0, U, info);
   if (reinterpret_cast<uintptr_t>(U) % 16) return fail(PD_EINVAL, "U must be 16-byte aligned");
   const auto t0 = std::chrono::steady_clock::now();
   std::memset(info, 0, sizeof(*info));
@@ -1624,6 +1656,7 @@ int paradiag_solve(pd_handle* h, const double* u0, double* U, pd_solve_info* inf
 int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd_solve_info* info) {
   int rc = check_handle(h);
   if (rc) return rc;
+  if (h->shard) return fail(PD_EINVAL, "solve_host: single-GPU handles only (a sharded rank owns device slabs)");
   if (!u0_host || !uT_host || !info) return fail(PD_EINVAL, "NULL argument");
   if (!h->Uint && (rc = dalloc(h, &h->Uint, (size_t)h->total))) return rc;
   // window 1's u0 is staged in the hand-off buffer; it is only overwritten after window 1 ends
@@ -2037,6 +2070,7 @@ void paradiag_destroy(pd_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->shard) shard_destroy(h->shard);
   for (int i = 0; i < PD_NKERNELS; ++i)
     for (int j = 0; j < 2; ++j)
       if (h->ev[i][j]) cudaEventDestroy(h->ev[i][j]);

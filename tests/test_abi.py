@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.paradiag_abi_version() == pd.ABI_VERSION == 4
+    assert lib.paradiag_abi_version() == pd.ABI_VERSION == 5
     assert pd.strerror(pd.PD_EINVAL).startswith("PD_EINVAL")
     assert pd.strerror(pd.PD_ESINGULAR).startswith("PD_ESINGULAR")
 
@@ -101,5 +101,24 @@ def test_init_without_device_fails_loudly(lib):
     if torch.cuda.is_available():
         pytest.skip("GPU present")
     h = ctypes.c_void_p()
-    rc = lib.paradiag_init(ctypes.byref(pd.make_problem(config("c1"))), 0, None, ctypes.byref(h))
+    rc = lib.paradiag_init(ctypes.byref(pd.make_problem(config("c1"))), 0, None, None, 0, 1, ctypes.byref(h))
     assert rc == pd.PD_ECUDA and not h.value
+
+
+def test_sharded_init_validates_before_any_collective(lib):
+    """paradiag_init with nranks > 1 rejects unsupported problems / ranks with PD_EINVAL before it
+    touches CUDA or NCCL (no rank ever blocks in the communicator set-up on a bad call)."""
+    h = ctypes.c_void_p()
+    nid = b"\0" * 128
+    for p, rank, nranks in ((pd.make_problem(config("c4")), 0, 2),                 # CH: replicas only
+                            (pd.make_problem(config("c3")), 3, 2),                 # rank outside the world
+                            (pd.make_problem(config("c3")), 0, 9),                 # more than 8 ranks
+                            (pd.make_problem(config("c3"), m=8), 0, 4)):           # < 3 rows per rank
+        rc = lib.paradiag_init(ctypes.byref(p), 0, None, nid, rank, nranks, ctypes.byref(h))
+        assert rc == pd.PD_EINVAL and not h.value
+
+
+def test_workspace_bytes_per_rank(lib):
+    one = pd.paradiag_workspace_bytes(pd.make_problem(config("c5")))
+    eight = pd.paradiag_workspace_bytes(pd.make_problem(config("c5")), 8)
+    assert eight < one
