@@ -84,7 +84,8 @@ def test_virtual_ranks_iterate_reports_global_norms(cuda_lib, P):
             a = cuda_lib.paradiag_iterate_virtual(hs, u0s, Us, a)
             b = s.iterate(u0, V, b)
             assert a.iters == b.iters == k + 1
-            assert abs(a.delta_max - b.delta_max) <= 1e-11 * b.delta_max
+            # (relative to ‖U‖∞: by iteration 3 the increment of c3 is at rounding level, 1e-15)
+            assert abs(a.delta_max - b.delta_max) <= 1e-11 * max(b.delta_max, 1e-3 * b.u_max)
             assert abs(a.u_max - b.u_max) <= 1e-12 * b.u_max
         assert rel_err(to_host(torch.cat(Us, dim=1)), to_host(V)) <= 5e-11
     finally:
