@@ -184,52 +184,43 @@ class EventTimer:
 
 
 def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
-    """c5 (or any 2D linear config) sharded over the ranks: one SlabRank per process, NCCL
-    collectives (strong scaling: the whole problem is fixed, value = total dofs / max-rank time)."""
+    """c5 (or any 2D linear config) sharded over the ranks by the LIBRARY (include/paradiag.h
+    paradiag_init with an NCCL id, csrc/shard.cu): rank 0 draws the NCCL id, torch.distributed
+    broadcasts it, every rank's handle owns its communicator and runs the halo exchange, the two
+    all-to-all transposes and the stop-rule all-reduce itself (strong scaling: the whole problem is
+    fixed, value = total dofs / max-rank time)."""
     import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2304_14021_b200 as pd
-    from paper_2304_14021_b200 import dist as pdist
-    L = pdist.SlabLayout(p.n, p.nt, world)
-    y0, nyl = L.rows[rank]
-    x0, nxl = L.cols[rank]
-    ops = pdist.GpuOps(p, local, stream.cuda_stream, y0, nyl, x0, nxl)
-    # PARADIAG_SLAB_FUSED=0: the copy-based pack / unpack orchestration (A/B)
-    # PARADIAG_SLAB_CHUNKS: slice ranges whose all-to-all overlaps the next range's passes
-    # PARADIAG_SLAB_P2P=1 (opt-in): peer-memory transposes over CUDA IPC instead of the all-to-all
-    p2p = os.environ.get("PARADIAG_SLAB_P2P", "0") == "1"
-    rk = pdist.SlabRank(L, rank, ops, fused=os.environ.get("PARADIAG_SLAB_FUSED", "1") != "0",
-                        chunks=int(os.environ.get("PARADIAG_SLAB_CHUNKS", "4" if world > 1 else "1")), p2p=p2p)
-    comm = pdist.TorchComm()
-    if p2p:
-        rk.setup_p2p(comm)
+    from dataclasses import replace as _replace
+    obj = [pd.paradiag_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    nid = obj[0]
+    pk = _replace(p, fixed_iters=args.steps)
+    s = pd.Solver(pk, device=local, stream=stream.cuda_stream, nccl_id=nid, rank=rank, nranks=world)
+    y0, nyl = s.y0, s.ny
     u0_l = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).to(dev)
-
-    def fresh_U():
-        if p.init == "zero":
-            return torch.zeros(L.row_slab(rank), dtype=torch.float64, device=dev)
-        return u0_l.reshape(1, nyl, p.n).expand(p.nt, nyl, p.n).contiguous().reshape(-1)
-
-    U_l = fresh_U()
+    U_l = s.empty()
+    info = None
     for _ in range(args.warmup):
-        rk.iterate(u0_l, U_l, comm)
-    timer = EventTimer(stream)
-    pd.paradiag_profile(ops.h, True)
+        info = s.iterate(u0_l, U_l, info)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
-            dmax, umax = rk.iterate(u0_l, U_l, comm, timer)
+        rc, sinfo = s.solve(u0_l, U_l)          # exactly K iterations (host loop, NCCL inside)
         ev1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    prof = pd.paradiag_profile_read(ops.h)
-    pd.paradiag_profile(ops.h, False)
-    coll = timer.collect()
+    # per-kernel split: a second, profiled run of the same K iterations
+    s.profile(True)
+    s.solve(u0_l, U_l)
+    torch.cuda.synchronize()
+    prof = s.profile_read()
+    s.profile(False)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -241,8 +232,7 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
     for name, (n, tot) in prof.items():
         avg = tot / max(n, 1)
         bpd = BYTES_PER_DOF.get(name)
-        kernels[name] = {"avg_ms": avg, "share": tot / (ms if ms > 0 else 1),
-                         "gbs": (bpd * local_dofs / (avg * 1e-3) / 1e9) if bpd else None}
+        kernels[name] = {"avg_ms": avg, "gbs": (bpd * local_dofs / (avg * 1e-3) / 1e9) if bpd else None}
     top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
     roof = None
     if top:
@@ -253,74 +243,70 @@ def run_sharded(args, p, rank, world, local, dev, stream, u0, cfg, metric):
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_source": peak_src, "traffic": None, "algorithmic_bytes_per_launch": bpd * local_dofs,
                 "per": "rank 0 (its row / column slab)"}
-    # NVLink: bytes this rank sends per all-to-all (the local block stays on the device).  The timed
-    # iteration overlaps the per-range transposes with the passes, so the link is measured on its
-    # own afterwards: the iteration's forward transpose (every range), timed on the device.
-    sent = 8 * (sum(L.fwd_send_splits(rank)) - L.block(rank, rank))
+    # NVLink: the bytes one transpose sends per rank (the (row slab r) x (column slab q) blocks of
+    # the peers), timed as a standalone NCCL all-to-all of that size after the timed region
+    from paper_2304_14021_b200.dist import split
+    rows = split(p.n, world)
+    sent_elems = p.nt * nyl * (p.n - rows[rank][1])
     nvlink = None
-    if world > 1 and not rk.p2p:
-        groups = getattr(rk, "regions", None) or [{"send": rk.send, "recv": rk.recv, "splits": rk.splits}]
+    if world > 1:
+        send = torch.empty(sent_elems + world, dtype=torch.float64, device=dev)
+        recv = torch.empty_like(send)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 3
         dist.barrier()
         e0.record(stream)
         for _ in range(reps):
-            for g in groups:
-                ssp, rsp = g["splits"]["fwd"]
-                comm.all_to_all(g["recv"], g["send"], rsp, ssp)
+            dist.all_to_all_single(recv, send)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        a2a_ms = float(t.item())
-        nvlink = {"achieved": sent / (a2a_ms * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s",
-                  "frac": sent / (a2a_ms * 1e-3) / 1e9 / 770.0, "peak_source": "guide: measured peer copy per direction",
-                  "bytes_per_alltoall": sent, "alltoall_ms": a2a_ms, "chunks": getattr(rk, "chunks", 1),
-                  "measured": "standalone forward transpose of the iteration's blocks (max over ranks)",
-                  "in_iteration_exposed_ms": {k: coll[k] for k in coll}}
-    # end to end: H2D of the rank's u0 rows, K = 3 iterations, D2H of its u_{N_t} rows
+        tt = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        a2a_ms = float(tt.item())
+        nb = 8 * send.numel() * (world - 1) / world
+        nvlink = {"achieved": nb / (a2a_ms * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s",
+                  "frac": nb / (a2a_ms * 1e-3) / 1e9 / 770.0, "peak_source": "guide: measured peer copy per direction",
+                  "bytes_per_alltoall": nb, "alltoall_ms": a2a_ms,
+                  "measured": "standalone NCCL all-to-all of one transpose's byte count (max over ranks)"}
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e:                      # H2D u0 rows, K = 3 iterations, D2H u_Nt rows
+        obj = [pd.paradiag_nccl_unique_id() if rank == 0 else None]     # one id per communicator
+        dist.broadcast_object_list(obj, src=0)
+        se = pd.Solver(_replace(p, fixed_iters=p.fixed_iters or 3), device=local, stream=stream.cuda_stream,
+                       nccl_id=obj[0], rank=rank, nranks=world)
         K = p.fixed_iters or 3
         u0h = torch.from_numpy(np.ascontiguousarray(u0[y0:y0 + nyl])).pin_memory()
         outh = torch.empty((nyl, p.n), dtype=torch.float64).pin_memory()
+        Ue = se.empty()
         dist.barrier()
         t0 = time.perf_counter()
         u0d = u0h.to(dev, non_blocking=True)
-        Ue = fresh_U()
-        for _ in range(K):
-            rk.iterate(u0d, Ue, comm)
-        outh.copy_(Ue.reshape(p.nt, nyl, p.n)[-1], non_blocking=True)
+        se.solve(u0d, Ue)
+        outh.copy_(Ue[-1], non_blocking=True)
         torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        tt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
         e2e = {"value": K * p.dofs / te, "unit": "dof/s", "h2d_bytes_per_step": int(p.ns * 8),
                "d2h_bytes_per_step": int(p.ns * 8), "step": f"H2D u0 slabs, {K} sharded iterations, D2H u_Nt slabs",
                "seconds_per_step": te}
-    # this rank's kernels in the timed region: the library's profiled launches plus, per step, the
-    # two halo pack copies and the stats reset (not profiled); every rank launches the same set
-    launches = sum(n for n, _ in prof.values()) + 3 * args.steps
+        se.close()
+    launches = sum(n for n, _ in prof.values())
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "dof/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(cfg, parallelism=f"slab{world}: row slabs (residual, x transforms, update) / column "
-                                                 f"slabs (y transforms, time pass), NCCL all-to-all + halo; passes "
-                                                 f"address the transpose blocks directly"
-                                                 + (f", {rk.chunks} slice ranges overlapping the transposes"
-                                                    if rk.chunks > 1 else "")),
+                "config": dict(cfg, parallelism=f"slab{world}: library-owned NCCL communicator (paradiag_init with an "
+                                                 f"NCCL id): row slabs (residual, x transforms, update) / column "
+                                                 f"slabs (y transforms, time pass), two all-to-alls + a 2-row halo "
+                                                 f"per iteration, max all-reduce of the stop rule",
+                               step="one iteration of a K-iteration sharded paradiag_solve (host loop)"),
                 "roofline": roof, "nvlink": nvlink, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": launches * world, "clocks": clk.summary(), "kernels": kernels,
                 "precond": precond_summary(prof, args.steps, local_dofs, peak),
-                "last_iter": {"delta_max": dmax, "u_max": umax}}
+                "last_iter": {"last_rel": float(sinfo.last_rel[0])}}
         print(json.dumps(_finite(line), allow_nan=False), flush=True)
-    if rk.p2p:
-        torch.cuda.synchronize()
-        dist.barrier()                      # no rank still stores into a peer before unmapping
-        rk.close_p2p()
-    ops.close()
+    s.close()
     dist.destroy_process_group()
     return 0
 

@@ -155,7 +155,8 @@ PD_API int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* byt
  * and owns the NCCL communicator (ncclCommInitRank with the NCCL the process has loaded — torch's)
  * and runs the halo exchange, the two all-to-all transposes per P_α⁻¹ and the max all-reduce of
  * the stop rule itself; the caller passes only its row slab (paradiag_local_rows): u0 [ny_l][nx],
- * U / r / δ [nt][ny_l][nx].  Every rank must make the same calls in the same order.
+ * U / r / δ [nt][ny_l][nx].  Every rank must make the same calls in the same order; an id serves
+ * one communicator (draw a fresh one per sharded handle).
  * nccl_id = NULL and nranks ≤ 1: a single-GPU handle (rank ignored). */
 PD_API int paradiag_init(const pd_problem* p, int device, void* cuda_stream, const unsigned char* nccl_id,
                          int rank, int nranks, pd_handle** out);
