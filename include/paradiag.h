@@ -179,6 +179,14 @@ PD_API int paradiag_iterate_virtual(pd_handle* const* hs, int nranks, const doub
 PD_API int paradiag_solve_virtual(pd_handle* const* hs, int nranks, const double* const* u0_l,
                                   double* const* U_l, pd_solve_info* info);
 
+/* The slab layout the sharded engine uses for rank `rank` of `nranks` on an n × n grid with nt
+ * slices (host only, no CUDA): out = {y0, ny_l, x0, nx_l, nsr, so, fs[P], fr[P], cfs[P], cfr[P],
+ * then the four transpose-block maps x_out, y_in, y_out, x_in, each {P, (e0, cnt, off) × P}};
+ * fs / fr = forward send / receive element counts per peer (0 for the rank itself), cfs / cfr their
+ * offsets in the send [0, nsr) / receive [nsr, 2 nsr) regions, so = the kept block.  cap = capacity
+ * of out (≥ 6 + 4P + 4(1 + 3P)).  Lets the CPU tests check the engine's maps. */
+PD_API int paradiag_shard_layout(int64_t n, int64_t nt, int nranks, int rank, int64_t* out, int64_t cap);
+
 /* Residual r = b - K(U) of the all-at-once system (P:127-149 linear; -G(U) of P:460-463 for CH,
  * mixed form v = U³ - U - ε²Δ_h U, r = Δ_h v - (U_n - U_{n-1})/Δt), with U_0 := u0, stencils in
  * nested form (R#15).  For CH also reduces J̄ = mean(3U² - 1) into the handle (device-resident),

@@ -64,7 +64,7 @@ EXPORTS = ["paradiag_profile", "paradiag_profile_read", "paradiag_abi_version", 
            "paradiag_slab_update", "paradiag_copy3d", "paradiag_stats_reset",
            "paradiag_stats_read", "paradiag_tslab_pitch", "paradiag_tslab_residual", "paradiag_tslab_time",
            "paradiag_tslab_update", "paradiag_nccl_unique_id", "paradiag_local_rows", "paradiag_init_virtual",
-           "paradiag_iterate_virtual", "paradiag_solve_virtual"]
+           "paradiag_iterate_virtual", "paradiag_solve_virtual", "paradiag_shard_layout"]
 ABI_VERSION = 5
 GROWTH_LIMIT = 3          # PD_GROWTH_LIMIT
 
@@ -89,6 +89,8 @@ def load(path: str = LIB_PATH):
     lib.paradiag_init_virtual.argtypes = [P(pd_problem), ctypes.c_int, vp, ctypes.c_int, P(vp)]
     lib.paradiag_iterate_virtual.argtypes = [P(vp), ctypes.c_int, P(vp), P(vp), P(pd_iter_info)]
     lib.paradiag_solve_virtual.argtypes = [P(vp), ctypes.c_int, P(vp), P(vp), P(pd_solve_info)]
+    lib.paradiag_shard_layout.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, P(ctypes.c_int64),
+                                          ctypes.c_int64]
     lib.paradiag_residual.argtypes = [vp, vp, vp, vp, P(ctypes.c_double)]
     lib.paradiag_apply_precond.argtypes = [vp, vp, vp, ctypes.c_double]
     lib.paradiag_apply_precond_jt.argtypes = [vp, vp, vp, vp]
@@ -225,6 +227,25 @@ def paradiag_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load().paradiag_nccl_unique_id(buf), "paradiag_nccl_unique_id")
     return buf.raw
+
+
+def paradiag_shard_layout(n: int, nt: int, nranks: int, rank: int) -> dict:
+    """The sharded engine's layout of one rank (host only): slabs, splits and transpose-block maps."""
+    P = nranks
+    cap = 6 + 4 * P + 4 * (1 + 3 * P)
+    buf = (ctypes.c_int64 * cap)()
+    _check(load().paradiag_shard_layout(int(n), int(nt), int(nranks), int(rank), buf, cap), "paradiag_shard_layout")
+    v = list(buf)
+    out = dict(zip(("y0", "nyl", "x0", "nxl", "nsr", "so"), v[:6]))
+    k = 6
+    for name in ("fs", "fr", "cfs", "cfr"):
+        out[name] = v[k:k + P]
+        k += P
+    for name in ("xm_out", "ym_in", "ym_out", "xm_in"):
+        blk = v[k + 1:k + 1 + 3 * P]
+        out[name] = [tuple(blk[3 * i:3 * i + 3]) for i in range(P)]
+        k += 1 + 3 * P
+    return out
 
 
 def paradiag_local_rows(h):

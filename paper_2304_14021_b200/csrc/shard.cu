@@ -575,3 +575,22 @@ int paradiag_solve_virtual(pd_handle* const* hs, int nranks, const double* const
   if (!u0_l || !U_l || !info) return pd_set_error(PD_EINVAL, "NULL argument");
   return group_solve(g, u0_l, U_l, info);
 }
+
+// ---------------------------------------------------------------- public: the layout (host only)
+int paradiag_shard_layout(int64_t n, int64_t nt, int nranks, int rank, int64_t* out, int64_t cap) {
+  if (!out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks || n / nranks < 3 || nt < 1)
+    return pd_set_error(PD_EINVAL, "shard layout: bad arguments");
+  const int64_t P = nranks, need = 6 + 4 * P + 4 * (1 + 3 * P);
+  if (cap < need) return pd_set_error(PD_EINVAL, "shard layout: output too small");
+  pd_shard s;
+  s.n = n;
+  s.nt = nt;
+  layout(&s, nranks, rank);
+  int64_t k = 0;
+  for (int64_t v : {s.y0, s.nyl, s.x0, s.nxl, s.nsr, s.so}) out[k++] = v;
+  for (const auto* v : {&s.fs, &s.fr, &s.cfs, &s.cfr})
+    for (int64_t x : *v) out[k++] = x;
+  for (const auto* v : {&s.xm_out, &s.ym_in, &s.ym_out, &s.xm_in})
+    for (int64_t x : *v) out[k++] = x;
+  return PD_OK;
+}

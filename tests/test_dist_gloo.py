@@ -272,3 +272,28 @@ def test_block_maps_match_the_pack_descriptors():
             for y0, cnt, off in L.ymap(r):
                 t, yy, cc = np.meshgrid(np.arange(nt), np.arange(cnt), np.arange(nxl), indexing="ij")
                 assert (srcof[t, y0 + yy, cc] == off + (t * cnt + yy) * nxl + cc).all()
+
+
+@pytest.mark.parametrize("n,nt,P", [(33, 8, 2), (31, 8, 3), (129, 32, 8), (65, 4, 5), (2049, 512, 8)])
+def test_library_shard_layout_equals_the_gloo_tested_layout(n, nt, P):
+    """The C++ engine's slab layout (paradiag_shard_layout, csrc/shard.cu) is the one this file
+    runs with real gloo collectives (dist.SlabRank, fused single-range form): same slabs, splits,
+    send / receive regions and transpose-block maps for every rank — so the world-size-2 data
+    movement checked against the oracle above is the library's."""
+    import paper_2304_14021_b200 as pd
+    from paper_2304_14021_b200 import dist
+
+    class _Ops:
+        def empty(self, count):
+            return torch.zeros(1, dtype=torch.float64)
+
+    L = dist.SlabLayout(n, nt, P)
+    for r in range(P):
+        got = pd.paradiag_shard_layout(n, nt, P, r)
+        rk = dist.SlabRank(L, r, _Ops(), fused=True, chunks=1)
+        g = rk.regions[0]
+        assert (got["y0"], got["nyl"]) == L.rows[r] and (got["x0"], got["nxl"]) == L.cols[r]
+        fs, fr = g["splits"]["fwd"]
+        assert got["fs"] == fs and got["fr"] == fr and got["nsr"] == g["ns"]
+        assert got["xm_out"] == rk.xm_out and got["ym_in"] == rk.ym_in
+        assert got["ym_out"] == rk.ym_out and got["xm_in"] == rk.xm_in
