@@ -61,6 +61,19 @@ def precond_summary(prof, steps, dofs, peak):
             "kernels": [k for k in prof if k in PRECOND_KERNELS]}
 
 
+def ncu_counters(name):
+    """DRAM bytes per launch and FP64-pipe utilisation of kernel `name` from the committed ncu
+    --set full capture of the c5 bench (profiles/ncu_counters.json, tools/ncu_counters.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as f:
+            d = json.load(f)
+        k = d["kernels"].get(name) or {}
+        return {"traffic": k.get("traffic"), "fp64_pipe_pct": k.get("fp64_pipe_pct"),
+                "source": "profiles/ncu_counters.json <- " + d.get("source", "?")}
+    except Exception:
+        return {}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -461,12 +474,22 @@ def main():
     from workloads import config, make_u0
     p = config(args.config)
     metric = "space-time dof/s per ParaDiag iteration (fp64)"
-    cfg = {"workload": f"BASELINE.json configs[4] ({args.config}): 2D linearised Cahn-Hilliard, Neumann, "
-                       f"{p.ny}x{p.nx} nodes, N_t={p.nt}, T={p.t_window}, alpha={p.alpha}, beta={p.beta}, "
-                       f"eps={p.eps}, U0=0" if args.config == "c5" else
-                       f"{args.config} (SURVEY §8(f) NEXT-3, P:692-699): 1D biharmonic, u = u_xx = 0, h = 1/{p.m} "
-                       f"({p.nx} unknowns), N_t={p.nt} (2^20 stand-in for 10^6), T={p.t_window}, alpha={p.alpha}"
-                       if args.config == "c6" else args.config,
+    desc = {
+        "c1": f"BASELINE.json configs[0] (c1): 1D biharmonic, u = u_xx = 0, {p.nx} interior points, N_t={p.nt}, "
+              f"T={p.t_window}, alpha={p.alpha}, u0 = sin(pi x)",
+        "c2": f"BASELINE.json configs[1] (c2): 1D linearised Cahn-Hilliard, Neumann, {p.nx} nodes, N_t={p.nt}, "
+              f"T={p.t_window}, alpha={p.alpha}, beta={p.beta}, eps={p.eps}",
+        "c3": f"BASELINE.json configs[2] (c3): 2D biharmonic, u = Lap u = 0, {p.ny}x{p.nx} interior (512x512 grid), "
+              f"N_t={p.nt}, T={p.t_window}, alpha={p.alpha}",
+        "c4": f"BASELINE.json configs[3] (c4): 2D Cahn-Hilliard PinT-I, Neumann, {p.ny}x{p.nx} nodes, N_t={p.nt} per "
+              f"window, dt={p.t_window / p.nt}, alpha={p.alpha}, eps={p.eps}; timed on window 1 (damped "
+              f"averaged-Jacobian iteration)",
+        "c5": f"BASELINE.json configs[4] (c5): 2D linearised Cahn-Hilliard, Neumann, {p.ny}x{p.nx} nodes, N_t={p.nt}, "
+              f"T={p.t_window}, alpha={p.alpha}, beta={p.beta}, eps={p.eps}, U0=0",
+        "c6": f"c6 (SURVEY §8(f) NEXT-3, P:692-699): 1D biharmonic, u = u_xx = 0, h = 1/{p.m} ({p.nx} unknowns), "
+              f"N_t={p.nt} (2^20 stand-in for 10^6), T={p.t_window}, alpha={p.alpha}",
+    }
+    cfg = {"workload": desc.get(args.config, args.config),
            "dofs_per_iteration": p.dofs,
            "l2": (f"inputs {p.dofs * 8 / 1e9:.3g} GB/array >> 126 MB L2 (no flush needed)" if p.dofs * 8 > 4 * 126e6
                   else "arrays fit in L2: warm-L2 numbers")}
@@ -521,9 +544,9 @@ def main():
     # pipelined engine: each iteration's update rides in the next residual); mode
     # "iterate": K calls of paradiag_iterate (residual, P_α⁻¹, separate update)
     from dataclasses import replace as _replace
-    if args.mode == "solve":
+    if args.mode == "solve":                # exactly K iterations of one window (windows are sequential)
         s.close()
-        s = pd.Solver(_replace(p, fixed_iters=args.steps), device=local, stream=stream.cuda_stream)
+        s = pd.Solver(_replace(p, fixed_iters=args.steps, n_windows=1), device=local, stream=stream.cuda_stream)
     for _ in range(args.warmup):            # W untimed iterations on the timed handle
         info = s.iterate(u0_d, U, info)
     if args.mode == "solve":
@@ -590,15 +613,13 @@ def main():
         avg = tot / n
         bpd = BYTES_PER_DOF.get(name, 16.0)
         ach = bpd * p.dofs / (avg * 1e-3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get(name)
-        except Exception:
-            pass
+        nc = ncu_counters(name) if args.config == "c5" else {}
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "peak_source": peak_src, "traffic": traffic,
-                "algorithmic_bytes_per_launch": bpd * p.dofs}
+                "frac": ach / peak, "peak_source": peak_src, "traffic": nc.get("traffic"),
+                "algorithmic_bytes_per_launch": bpd * p.dofs,
+                # the secondary bound: FP64-pipe utilisation of the same kernel
+                "fp64_pipe_pct": nc.get("fp64_pipe_pct"),
+                "counters_source": nc.get("source")}
     # whole-iteration HBM efficiency at the design byte count: the algorithmic bytes
     # of the kernels that ran, per step
     design_bytes = sum(BYTES_PER_DOF.get(k, 0.0) * n for k, (n, _) in prof.items()) / args.steps * p.dofs
@@ -623,9 +644,9 @@ def main():
             t = torch.tensor([te], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": world * pe.fixed_iters * pe.dofs / te, "unit": "dof/s",
+        e2e = {"value": world * pe.fixed_iters * pe.n_windows * pe.dofs / te, "unit": "dof/s",
                "h2d_bytes_per_step": int(u0h.nbytes), "d2h_bytes_per_step": int(uT.nbytes + 32 * pe.fixed_iters),
-               "step": f"paradiag_solve_host: H2D u0, {pe.fixed_iters} iterations, D2H u_Nt",
+               "step": f"paradiag_solve_host: H2D u0, {pe.n_windows} window(s) x {pe.fixed_iters} iterations, D2H u_Nt",
                "seconds_per_step": te}
         se.close()
 

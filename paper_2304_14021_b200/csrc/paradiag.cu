@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cmath>
@@ -214,7 +215,10 @@ struct pd_handle {
 
 namespace {
 
+// Every pass is an NVTX range (header-only NVTX3: a no-op unless a tool such as ncu
+// or nsys is attached) and, with paradiag_profile on, a pair of CUDA events.
 void prof_begin(pd_handle* h, int id) {
+  nvtxRangePushA(kKernelNames[id]);
   if (!h->prof) return;
   if (!h->ev[id][0]) {
     cudaEventCreate(&h->ev[id][0]);
@@ -223,6 +227,7 @@ void prof_begin(pd_handle* h, int id) {
   cudaEventRecord(h->ev[id][0], h->stream);
 }
 void prof_end(pd_handle* h, int id) {
+  nvtxRangePop();
   if (!h->prof) return;
   cudaEventRecord(h->ev[id][1], h->stream);
   h->ev_used[id] = true;

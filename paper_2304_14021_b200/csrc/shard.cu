@@ -20,6 +20,7 @@
 // B200_PROFILING.md requires when ranks share a GPU) — the test of the layout and the block
 // addressing without a multi-GPU box.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstring>
@@ -222,8 +223,14 @@ int check_problem(const pd_problem* p, int nranks) {
 // ---------------------------------------------------------------- collectives (group-wide)
 pd_shard* S(pd_handle* h) { return pd_handle_shard(h); }
 
+struct NvtxRange {                    // NVTX range of a collective (C1-C3)
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 int comm_halo(Group* g) {
   if (g->P == 1) return PD_OK;
+  NvtxRange nv("halo_exchange");
   if (g->virt) {                     // rank r's first rows -> r-1's upper halo, last rows -> r+1's lower halo
     for (int r = 0; r < g->P; ++r) {
       pd_shard* s = S(g->hs[r]);
@@ -254,6 +261,7 @@ int comm_halo(Group* g) {
 // dir 0: forward (rows -> columns), 1: backward.  Sends from [0, nsr), receives into [nsr, 2 nsr).
 int comm_a2a(Group* g, int dir) {
   if (g->P == 1) return PD_OK;
+  NvtxRange nv(dir == 0 ? "alltoall_fwd" : "alltoall_bwd");
   if (g->virt) {
     for (int r = 0; r < g->P; ++r) {
       pd_shard* s = S(g->hs[r]);
@@ -287,6 +295,7 @@ int comm_a2a(Group* g, int dir) {
 
 // global (‖δ‖∞, ‖U‖∞): max over the ranks of the handles' statistics (bit-pattern maxima)
 int comm_stats(Group* g, double* dmax, double* umax) {
+  NvtxRange nv("allreduce_stats");
   if (!g->virt && g->comm)          // (a one-rank world runs it too: the NCCL path is exercised)
     PD_NCCL(nccl()->allReduce(pd_handle_stats_dev(g->hs[0]), pd_handle_stats_dev(g->hs[0]), 2, ncclUint64, ncclMax,
                               g->comm, pd_handle_stream(g->hs[0])));
