@@ -48,6 +48,14 @@ struct TlongParams {
   const double* glo;
   const double* gihi;
   const double* gilo;
+  // mixed-radix factors (k_tmix.cuh; N1, N2 products of 2, 4, 5, 8): radix plans, root tables
+  // mt1[j] = W_{N1}^j, mt2[j] = W_{N2}^j, mtN[b] = W_N^b (b < N2)
+  int mixed;
+  int nst1, nst2;
+  int8_t plan1[12], plan2[12];
+  const double2* mt1;
+  const double2* mt2;
+  const double2* mtN;
 };
 
 #ifdef PD_TLONG_KERNELS     // defined only in tlong.cu (the engine sees TlongParams alone)
@@ -184,7 +192,7 @@ k_tl_divide(double2* __restrict__ X, TlongParams Q) {
   const double jbar = Q.T.kind >= 2 ? Q.T.st->jbar : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i / Q.P, p = i - k * Q.P;
-    const int64_t km = (Q.N - k) & (Q.N - 1);
+    const int64_t km = k == 0 ? 0 : Q.N - k;          // the Hermitian mirror bin (any N)
     const double2 Zl = X[k * Q.P + p], Zm = X[km * Q.P + p];
     const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
     const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));

@@ -173,6 +173,11 @@ struct pd_handle {
   // DST-I/DCT-I eigenbasis like 2D (x passes + per-mode divide) instead of the pentadiagonal LU.
   bool tlong = false;
   int log2n1 = 0, log2n2 = 0;
+  int n1 = 0, n2 = 0;                 // N_t = n1·n2 (four-step factors)
+  bool mixed = false;                 // N_t = 2^a 5^b, not a power of two: k_tmix.cuh passes
+  int nst1 = 0, nst2 = 0;
+  int8_t plan1[12] = {}, plan2[12] = {};
+  double2* mtab = nullptr;            // mixed roots: W_{n1}^j (n1), W_{n2}^j (n2), W_N^b (b < n2)
   // 1D long windows with N_x ≤ 64: x transforms as DMMA products with T (k_x1d.cuh), fused with
   // the residual (forward) and the update (inverse); x1T = Tᵀ zero padded to 64×64
   bool x1 = false;
@@ -267,9 +272,16 @@ int validate(const pd_problem* p) {
   if (p->dim != 1 && p->dim != 2) return fail(PD_EINVAL, "dim must be 1 or 2");
   if (is_ch(p->kind) && (p->dim != 2 || p->bc != PD_BC_NEUMANN))
     return fail(PD_EINVAL, "Cahn-Hilliard is supported in 2D with Neumann BCs (P:59)");
-  if (!is_pow2(p->nt) || p->nt < 2 || p->nt > kMaxNt) return fail(PD_EINVAL, "nt must be a power of two in [2, 2^20]");
-  if (p->nt > kMaxNtShort && p->dim == 1 && (!is_pow2(p->m) || p->m > 4096))
-    return fail(PD_EINVAL, "1D with nt > 4096 (spectral long-window path): m must be a power of two <= 4096");
+  {
+    int n1, n2, ns1, ns2;
+    int8_t pl1[12], pl2[12];
+    const bool mixed = !is_pow2(p->nt) && mixed_split(p->nt, &n1, &n2, pl1, &ns1, pl2, &ns2);
+    if (!((is_pow2(p->nt) && p->nt >= 2 && p->nt <= kMaxNt) || mixed))
+      return fail(PD_EINVAL, "nt must be a power of two in [2, 2^20], or 2^a 5^b (>= 64) split as N1 N2 <= 1024^2 "
+                             "(mixed-radix long-window path, e.g. 10^6 = 1000 x 1000, P:692)");
+    if ((p->nt > kMaxNtShort || mixed) && p->dim == 1 && (!is_pow2(p->m) || p->m > 4096))
+      return fail(PD_EINVAL, "1D long windows (nt > 4096 or mixed radix): m must be a power of two <= 4096");
+  }
   if (p->dim == 2 && (!is_pow2(p->m) || p->m < 4 || p->m > 4096))
     return fail(PD_EINVAL, "2D: m (intervals per axis) must be a power of two in [4, 4096]");
   if (p->dim == 1 && (p->m < 4 || p->m > (1 << 20))) return fail(PD_EINVAL, "1D: m must be in [4, 2^20]");
@@ -541,7 +553,11 @@ TimeParams time_params(pd_handle* h, unsigned long long* amax) {
 int tlong_time(pd_handle* h, const double* in, double* out, int64_t c0 = 0, int64_t bc = 0) {
   TlongParams Q;
   Q.N = h->P.nt; Q.log2N = h->log2nt;
-  Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = 1 << h->log2n1; Q.N2 = 1 << h->log2n2;
+  Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = h->n1; Q.N2 = h->n2;
+  Q.mixed = h->mixed ? 1 : 0;
+  Q.nst1 = h->nst1; Q.nst2 = h->nst2;
+  for (int i = 0; i < 12; ++i) { Q.plan1[i] = h->plan1[i]; Q.plan2[i] = h->plan2[i]; }
+  Q.mt1 = h->mtab; Q.mt2 = h->mtab ? h->mtab + h->n1 : nullptr; Q.mtN = h->mtab ? h->mtab + h->n1 + h->n2 : nullptr;
   Q.ns = h->ns; Q.P = (h->ns + 1) / 2; Q.nch = (Q.P + kTlPairs - 1) / kTlPairs;
   Q.ld = h->x1 ? (int64_t)x1_pitch(h) : h->ns;
   Q.ghi = h->tlg; Q.glo = h->tlg + Q.N1; Q.gihi = h->tlg + Q.N1 + Q.N2; Q.gilo = h->tlg + 2 * Q.N1 + Q.N2;
@@ -1137,7 +1153,7 @@ int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes) {
   geometry(p, &nx, &ny);
   const size_t ns = (size_t)nx * ny, total = ns * p->nt, nb = p->nt / 2 + 1;
   size_t b = total * sizeof(double) + ns * sizeof(double);
-  const bool tl = p->nt > kMaxNtShort;
+  const bool tl = p->nt > kMaxNtShort || !is_pow2(p->nt);
   if (tl) b += 2 * (size_t)p->nt * ((ns + 1) / 2) * sizeof(double2);       // Y, X of k_tlong.cuh
   else if (p->dim == 1) b += 7 * (size_t)nx * nb * sizeof(double2) + 5 * (size_t)nx * sizeof(double);
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
@@ -1207,15 +1223,24 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   {
     const char* f = std::getenv("PARADIAG_TLONG");
     const bool force = f && std::atoi(f) != 0;
-    h->tlong = p->nt > kMaxNtShort || (force && p->nt >= 1024 && (p->dim == 2 || (is_pow2(M) && M <= 4096)));
-    tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
+    h->mixed = !is_pow2(p->nt);          // 2^a 5^b (validate): the mixed-radix four-step passes
+    h->tlong = p->nt > kMaxNtShort || h->mixed ||
+               (force && p->nt >= 1024 && (p->dim == 2 || (is_pow2(M) && M <= 4096)));
+    if (h->mixed) {
+      mixed_split(p->nt, &h->n1, &h->n2, h->plan1, &h->nst1, h->plan2, &h->nst2);
+      h->log2n1 = h->log2n2 = 0;
+    } else {
+      tlong_split(h->log2nt, &h->log2n1, &h->log2n2);
+      h->n1 = 1 << h->log2n1;
+      h->n2 = 1 << h->log2n2;
+    }
     h->x1 = h->tlong && p->dim == 1 && h->nx <= 2 * kX1H;
     if (const char* f3 = std::getenv("PARADIAG_TLFUSE")) h->tlfuse = std::atoi(f3) != 0;
     if (const char* f4 = std::getenv("PARADIAG_GRAPH")) h->use_graph = std::atoi(f4) != 0;
     if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
   }
   h->log2h = (p->dim == 2 || h->tlong) ? ilog2(M) - 1 : 0;
-  h->twlog = std::max(h->log2nt, h->log2h);
+  h->twlog = h->mixed ? std::max(h->log2h, 1) : std::max(h->log2nt, h->log2h);   // mixed: own root tables
 
   auto cleanup = [&](int code) {
     paradiag_destroy(h);
@@ -1350,7 +1375,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
   if (h->tlong) {
     // γ_n = α^{n/N_t} (R#2) split at n = N2·n1 + n2; the inverse side carries 1/N_t and the spatial
     // normalisation like ginv
-    const int N1 = 1 << h->log2n1, N2 = 1 << h->log2n2;
+    const int N1 = h->n1, N2 = h->n2;
     std::vector<double> g(2 * (size_t)(N1 + N2));
     for (int i = 0; i < N1; ++i) {
       g[i] = std::exp((double)N2 * i * lna / nt);
@@ -1362,6 +1387,18 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     }
     PD_TRY(dalloc(h, &h->tlg, g.size()));
     if (up(h->tlg, g.data(), g.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "tlong table upload"));
+    if (h->mixed) {        // roots of the factor lengths and W_N^b, b < N2 (k_tmix.cuh): exact angles
+      std::vector<double2> mt((size_t)N1 + 2 * (size_t)N2);
+      auto root = [](int64_t j, int64_t L) {
+        const double a = 2.0 * M_PI * (double)j / (double)L;
+        return make_double2(std::cos(a), -std::sin(a));
+      };
+      for (int j = 0; j < N1; ++j) mt[j] = root(j, N1);
+      for (int j = 0; j < N2; ++j) mt[(size_t)N1 + j] = root(j, N2);
+      for (int j = 0; j < N2; ++j) mt[(size_t)N1 + N2 + j] = root(j, nt);
+      PD_TRY(dalloc(h, &h->mtab, mt.size()));
+      if (up(h->mtab, mt.data(), mt.size() * sizeof(double2))) return cleanup(fail(PD_ECUDA, "mixed table upload"));
+    }
     const size_t nc = (size_t)nt * (size_t)((h->ns + 1) / 2);
     PD_TRY(dalloc(h, &h->spec, nc));
     PD_TRY(dalloc(h, &h->w1, nc));

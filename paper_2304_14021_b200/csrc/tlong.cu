@@ -2,6 +2,7 @@
 // transform length 32·E of each four-step factor.  paradiag.cu sees only tlong.h.
 #define PD_TLONG_KERNELS
 #include "tlong.h"
+#include "k_tmix.cuh"
 
 #include <algorithm>
 
@@ -49,7 +50,30 @@ void tlong_split(int log2N, int* log2N1, int* log2N2) {
   *log2N1 = log2N - *log2N2;
 }
 
-bool tlong_fusable(const TlongParams& Q) { return Q.N2 == 1024 && Q.N1 >= 32; }
+bool tlong_fusable(const TlongParams& Q) { return !Q.mixed && Q.N2 == 1024 && Q.N1 >= 32; }
+
+bool mixed_split(int N, int* N1, int* N2, int8_t* plan1, int* ns1, int8_t* plan2, int* ns2) {
+  auto smooth = [](int v) {
+    while (v % 2 == 0) v /= 2;
+    while (v % 5 == 0) v /= 5;
+    return v == 1;
+  };
+  if (N < 64 || !smooth(N)) return false;
+  int best = 0;
+  for (int a = 8; a <= kMixMaxL && (int64_t)a * a <= N; ++a)          // largest N1 ≤ √N with both factors ≤ kMixMaxL
+    if (N % a == 0 && smooth(a) && N / a <= kMixMaxL) best = a;
+  if (!best) return false;
+  *N1 = best;
+  *N2 = N / best;
+  auto plan = [](int L, int8_t* p, int* n) {
+    *n = 0;
+    for (int r : {8, 4, 2}) while (L % r == 0) { p[(*n)++] = (int8_t)r; L /= r; }
+    while (L % 5 == 0) { p[(*n)++] = 5; L /= 5; }
+  };
+  plan(*N1, plan1, ns1);
+  plan(*N2, plan2, ns2);
+  return true;
+}
 
 cudaError_t tlong_attrs() {
   cudaError_t e;
@@ -58,6 +82,10 @@ cudaError_t tlong_attrs() {
     return e;
   if ((e = cudaFuncSetAttribute(k_tl_b_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem)))
     return e;
+  if ((e = cudaFuncSetAttribute(k_mx_a_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mx_a_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mx_b_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mx_b_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
   return cudaFuncSetAttribute(k_tl_b_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
 }
 
@@ -68,6 +96,17 @@ bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cu
     const unsigned grid = (unsigned)(nch4 * (Q.N1 / 2));
     if (!Q.T.el && !Q.T.l3) k_tl_b_fused<true><<<grid, kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
     else k_tl_b_fused<false><<<grid, kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
+    return true;
+  }
+  if (Q.mixed && stage != 2) {                          // mixed radix (k_tmix.cuh): one transform per CTA
+    const unsigned grid = (unsigned)(Q.nch * ((stage == 0 || stage == 4) ? Q.N2 : Q.N1));
+    switch (stage) {
+      case 0: k_mx_a_fwd<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double*>(in), static_cast<double2*>(out), Q); break;
+      case 1: k_mx_b_fwd<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
+      case 3: k_mx_b_inv<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
+      case 4: k_mx_a_inv<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double*>(out), Q); break;
+      default: return false;
+    }
     return true;
   }
   if (stage == 2) {

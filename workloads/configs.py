@@ -84,6 +84,11 @@ CONFIGS = {
     # random start is read as noise on top of the c1 sine.
     "c6": Problem("c6", "biharmonic", "hinged", 1, m=64, nt=1 << 20, t_window=1.0, alpha=1e-3,
                   u0_kind="sine_plus_noise", u0_range=(-0.01, 0.01), seed=6),
+    # NEXT-3 as the paper states it (Fig. 3 neighbourhood): 1D biharmonic with
+    # the paper's Neumann Δ_h, h = 1/64 (65 nodes), Δt = 10⁻⁶, N_t = 10⁶ = 2⁶·5⁶
+    # (the mixed-radix four-step time pass, k_tmix.cuh: 1000 × 1000), T = 1, α = 10⁻³
+    "c6n": Problem("c6n", "biharmonic", "neumann", 1, m=64, nt=10 ** 6, t_window=1.0, alpha=1e-3,
+                   u0_kind="sine_plus_noise", u0_range=(-0.01, 0.01), seed=6),
     # NEXT-4: c4's PinT-I with the paper's time-only averaged Jacobian
     # J̃ = I_t ⊗ (1/N_t) Σ_n J_s(u_n) — spatially varying, Step-(2) solved by an inner Krylov
     # iteration preconditioned by the scalar-J̄ spectral solve
