@@ -47,7 +47,7 @@ def test_workspace_bytes_all_configs(lib, name):
     assert b >= p.dofs * 8
 
 
-@pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=100), dict(nt=1), dict(nt=1 << 21),
+@pytest.mark.parametrize("bad", [dict(alpha=0.0), dict(alpha=1.0), dict(nt=96), dict(nt=3000), dict(nt=1), dict(nt=1 << 21),
                                  dict(theta=0.4), dict(theta=1.1), dict(m=100), dict(eps=-1.0), dict(t_window=0.0),
                                  dict(kind="cahn_hilliard"), dict(n_windows=0), dict(tol=0.0)])
 def test_invalid_problems_rejected(lib, bad):
@@ -122,3 +122,11 @@ def test_workspace_bytes_per_rank(lib):
     one = pd.paradiag_workspace_bytes(pd.make_problem(config("c5")))
     eight = pd.paradiag_workspace_bytes(pd.make_problem(config("c5")), 8)
     assert eight < one
+
+
+@pytest.mark.parametrize("nt", [100, 625, 1000, 10 ** 4, 40000, 10 ** 6])
+def test_mixed_radix_windows_accepted(lib, nt):
+    """N_t = 2^a 5^b (the paper's 10^4; 40000; 10^6) takes the mixed-radix
+    long-window path."""
+    from dataclasses import replace
+    assert pd.paradiag_workspace_bytes(pd.make_problem(replace(config("c6n"), nt=nt))) > 0
