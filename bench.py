@@ -487,7 +487,10 @@ def main():
         "c5": f"BASELINE.json configs[4] (c5): 2D linearised Cahn-Hilliard, Neumann, {p.ny}x{p.nx} nodes, N_t={p.nt}, "
               f"T={p.t_window}, alpha={p.alpha}, beta={p.beta}, eps={p.eps}, U0=0",
         "c6": f"c6 (SURVEY §8(f) NEXT-3, P:692-699): 1D biharmonic, u = u_xx = 0, h = 1/{p.m} ({p.nx} unknowns), "
-              f"N_t={p.nt} (2^20 stand-in for 10^6), T={p.t_window}, alpha={p.alpha}",
+              f"N_t={p.nt} (2^20 power-of-two form), T={p.t_window}, alpha={p.alpha}",
+        "c6n": f"c6n (SURVEY §8(f) NEXT-3 as the paper states it, P:692-699): 1D biharmonic, Neumann (P:84-87), "
+               f"h = 1/{p.m} ({p.nx} nodes), N_t={p.nt} = 2^6 5^6 (dt = 1e-6, mixed-radix time pass), T={p.t_window}, "
+               f"alpha={p.alpha}",
     }
     cfg = {"workload": desc.get(args.config, args.config),
            "dofs_per_iteration": p.dofs,

@@ -31,6 +31,7 @@ PRECOND = {
     "c6n_nt1280": _c6n(1280),                                   # 32 x 40: (8,4) / (8,5)
     "c6n_nt625": _c6n(625),                                     # odd N: 25 x 25, no Nyquist bin
     "c6n_nt2000_theta": _c6n(2000, theta=0.5),                  # 40 x 50, trapezoid e_l
+    "c6n_nt10000": _c6n(10 ** 4),                               # P:717's N_t = 10^4: 100 x 100, (4,5,5)
     "c6h_nt2000": replace(config("c6"), nt=2000, t_window=2000 * DT),   # hinged 63 unknowns: DMMA x path
     "c2_nt1000": twin("c2", m=64, nt=1000, t_window=1.0),       # linear CH, Neumann growing modes
     "c5_m32_nt1000": twin("c5", m=32, nt=1000, t_window=0.5),   # 2D Neumann, mixed time pass
