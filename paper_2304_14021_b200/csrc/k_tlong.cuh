@@ -56,6 +56,11 @@ struct TlongParams {
   const double2* mt1;
   const double2* mt2;
   const double2* mtN;
+  // digit reversal of the DIF plans: rev[pos] = frequency at DIF output position, irev its inverse
+  const int* rev1;
+  const int* rev2;
+  const int* irev1;
+  const int* irev2;
 };
 
 #ifdef PD_TLONG_KERNELS     // defined only in tlong.cu (the engine sees TlongParams alone)

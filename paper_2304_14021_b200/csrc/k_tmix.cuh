@@ -18,30 +18,8 @@
 
 namespace pd {
 
-// digit-reversed position of frequency k for a DIF plan r[0..ns) of length L:
-// k = q0 + r0·q1 + r0·r1·q2 + …  sits at  pos = q0·(L/r0) + q1·(L/(r0 r1)) + …
-PD_DEV int mix_pos(int k, const int8_t* r, int ns, int L) {
-  int pos = 0, span = L;
-  for (int s = 0; s < ns; ++s) {
-    const int q = k % r[s];
-    k /= r[s];
-    span /= r[s];
-    pos += q * span;
-  }
-  return pos;
-}
-// frequency k stored at digit-reversed position pos (inverse of mix_pos)
-PD_DEV int mix_freq(int pos, const int8_t* r, int ns, int L) {
-  int k = 0, mul = 1, span = L;
-  for (int s = 0; s < ns; ++s) {
-    span /= r[s];
-    const int q = pos / span;
-    pos -= q * span;
-    k += q * mul;
-    mul *= r[s];
-  }
-  return k;
-}
+// Digit reversal (tables built on the host, TlongParams.rev* / irev*): for a DIF plan r0, r1, … of
+// length L, frequency k = q0 + r0·q1 + r0·r1·q2 + … sits at position pos = q0·(L/r0) + q1·(L/(r0 r1)) + ….
 
 // small DFTs y_q = Σ_t a_t W_R^{SIGN·t·q}, W_R = e^{-2πi/R} (SIGN = -1 forward, +1 inverse), in place
 template <int SIGN>
@@ -109,10 +87,10 @@ PD_DEV void dft_r(double2* a) {
   else dft8<SIGN>(a);
 }
 
-// W_L^{SIGN·e}, e taken mod L, from tab[j] = e^{-2πi j/L}
+// W_L^{SIGN·e} from tab[j] = e^{-2πi j/L}, 0 <= e < L (a stage's j·q·(L/len) < L since j < len/R, q < R)
 template <int SIGN>
-PD_DEV double2 mix_root(const double2* __restrict__ tab, int64_t e, int L) {
-  double2 w = __ldg(tab + (int)(e % L));
+PD_DEV double2 mix_root(const double2* __restrict__ tab, int e) {
+  double2 w = __ldg(tab + e);
   if (SIGN > 0) w.y = -w.y;
   return w;
 }
@@ -131,12 +109,12 @@ PD_DEV void mix_stage(double2* x, int pitch, int L, int len, const double2* __re
     for (int t = 0; t < R; ++t) a[t] = x[(b + j + t * m) * pitch];
     if (SIGN > 0) {                                  // DIT: undo the twiddles first
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<+1>(tab, (int64_t)j * q * stride, L));
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<+1>(tab, j * q * stride));
     }
     dft_r<R, SIGN>(a);
     if (SIGN < 0) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<-1>(tab, (int64_t)j * q * stride, L));
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<-1>(tab, j * q * stride));
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) x[(b + j + t * m) * pitch] = a[t];
@@ -173,9 +151,9 @@ PD_DEV void mix_fft_inv(double2* x, int pitch, int L, const int8_t* r, int ns, c
 
 // four-step twiddle W_N^{SIGN·n2·k1} = W_{N1}^{a}·W_N^{b}, n2·k1 mod N = a·N2 + b
 template <int SIGN>
-PD_DEV double2 mix_tw4(const TlongParams& Q, int64_t n2, int64_t k1) {
-  const int64_t e = (n2 * k1) % Q.N, a = e / Q.N2, b = e - a * Q.N2;
-  return cmul(mix_root<SIGN>(Q.mt1, a, Q.N1), mix_root<SIGN>(Q.mtN, b, Q.N2));     // mtN[b] = W_N^b, b < N2
+PD_DEV double2 mix_tw4(const TlongParams& Q, int n2, int k1) {
+  const int e = (n2 * k1) % Q.N, a = e / Q.N2, b = e - a * Q.N2;       // n2·k1 < N ≤ 2^20: 32-bit
+  return cmul(mix_root<SIGN>(Q.mt1, a), mix_root<SIGN>(Q.mtN, b));      // mtN[b] = W_N^b, b < N2
 }
 
 constexpr int kMxRowC = kTlPairs + 1;                 // staged row pitch (complex): 8 pairs + 1 pad
@@ -191,11 +169,19 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_a_fwd(const double* __rest
   const int n2 = (int)(blockIdx.x / Q.nch);
   const int64_t c0 = chunk * (2 * kTlPairs);
   const int L = Q.N1;
-  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {
+  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {      // rows of 16 doubles (128 B)
     const int c = idx & 15, n1 = idx >> 4;
     const int64_t n = (int64_t)Q.N2 * n1 + n2;
-    sd[n1 * 2 * kMxRowC + c] = c0 + c < Q.ns ? __ldg(in + n * Q.ld + c0 + c) * __ldg(Q.ghi + n1) * __ldg(Q.glo + n2)
-                                              : 0.0;
+    double* d = sd + n1 * 2 * kMxRowC + c;
+    if (c0 + c < Q.ns) cp_async8(d, in + n * Q.ld + c0 + c);
+    else *d = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  const double g2 = __ldg(Q.glo + n2);
+  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {      // γ_n = ghi[n1]·glo[n2], own elements
+    const int c = idx & 15, n1 = idx >> 4;
+    sd[n1 * 2 * kMxRowC + c] *= __ldg(Q.ghi + n1) * g2;
   }
   __syncthreads();
   mix_fft_fwd(sm + warp, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, lane);
@@ -203,7 +189,7 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_a_fwd(const double* __rest
   for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
     const int w = idx & 7, pos = idx >> 3;
     const int64_t p = chunk * kTlPairs + w;
-    const int k1 = mix_freq(pos, Q.plan1, Q.nst1, L);
+    const int k1 = __ldg(Q.rev1 + pos);
     if (p < Q.P) Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] = cmul(sm[pos * kMxRowC + w], mix_tw4<-1>(Q, n2, k1));
   }
 }
@@ -219,15 +205,18 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_fwd(const double2* __res
   for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
     const int w = idx & 7, n2 = idx >> 3;
     const int64_t p = chunk * kTlPairs + w;
-    sm[n2 * kMxRowC + w] = p < Q.P ? Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] : make_double2(0.0, 0.0);
+    if (p < Q.P) cp_async16(sm + n2 * kMxRowC + w, Y + ((int64_t)k1 * Q.N2 + n2) * Q.P + p);
+    else sm[n2 * kMxRowC + w] = make_double2(0.0, 0.0);
   }
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
   mix_fft_fwd(sm + warp, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, lane);
   __syncthreads();
   for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
     const int w = idx & 7, pos = idx >> 3;
     const int64_t p = chunk * kTlPairs + w;
-    const int k2 = mix_freq(pos, Q.plan2, Q.nst2, L);
+    const int k2 = __ldg(Q.rev2 + pos);
     if (p < Q.P) X[((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p] = sm[pos * kMxRowC + w];
   }
 }
@@ -244,9 +233,12 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_inv(const double2* __res
   for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
     const int w = idx & 7, k2 = idx >> 3;
     const int64_t p = chunk * kTlPairs + w;
-    sm[mix_pos(k2, Q.plan2, Q.nst2, L) * kMxRowC + w] =
-        p < Q.P ? X[((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p] : make_double2(0.0, 0.0);
+    double2* d = sm + __ldg(Q.irev2 + k2) * kMxRowC + w;
+    if (p < Q.P) cp_async16(d, X + ((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
   }
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
   mix_fft_inv(sm + warp, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, lane);
   __syncthreads();
@@ -271,8 +263,16 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_a_inv(const double2* __res
   for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
     const int w = idx & 7, k1 = idx >> 3;
     const int64_t p = chunk * kTlPairs + w;
-    sm[mix_pos(k1, Q.plan1, Q.nst1, L) * kMxRowC + w] =
-        p < Q.P ? cmul(Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p], mix_tw4<+1>(Q, n2, k1)) : make_double2(0.0, 0.0);
+    double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
+    if (p < Q.P) cp_async16(d, Y + ((int64_t)k1 * Q.N2 + n2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {   // × W_N^{-n2 k1}, own elements
+    const int w = idx & 7, k1 = idx >> 3;
+    double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
+    *d = cmul(*d, mix_tw4<+1>(Q, n2, k1));
   }
   __syncthreads();
   mix_fft_inv(sm + warp, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, lane);

@@ -178,6 +178,7 @@ struct pd_handle {
   int nst1 = 0, nst2 = 0;
   int8_t plan1[12] = {}, plan2[12] = {};
   double2* mtab = nullptr;            // mixed roots: W_{n1}^j (n1), W_{n2}^j (n2), W_N^b (b < n2)
+  int* mrev = nullptr;                // digit reversals: rev1 [n1], irev1 [n1], rev2 [n2], irev2 [n2]
   // 1D long windows with N_x ≤ 64: x transforms as DMMA products with T (k_x1d.cuh), fused with
   // the residual (forward) and the update (inverse); x1T = Tᵀ zero padded to 64×64
   bool x1 = false;
@@ -558,6 +559,8 @@ int tlong_time(pd_handle* h, const double* in, double* out, int64_t c0 = 0, int6
   Q.nst1 = h->nst1; Q.nst2 = h->nst2;
   for (int i = 0; i < 12; ++i) { Q.plan1[i] = h->plan1[i]; Q.plan2[i] = h->plan2[i]; }
   Q.mt1 = h->mtab; Q.mt2 = h->mtab ? h->mtab + h->n1 : nullptr; Q.mtN = h->mtab ? h->mtab + h->n1 + h->n2 : nullptr;
+  Q.rev1 = h->mrev; Q.irev1 = h->mrev ? h->mrev + h->n1 : nullptr;
+  Q.rev2 = h->mrev ? h->mrev + 2 * h->n1 : nullptr; Q.irev2 = h->mrev ? h->mrev + 2 * h->n1 + h->n2 : nullptr;
   Q.ns = h->ns; Q.P = (h->ns + 1) / 2; Q.nch = (Q.P + kTlPairs - 1) / kTlPairs;
   Q.ld = h->x1 ? (int64_t)x1_pitch(h) : h->ns;
   Q.ghi = h->tlg; Q.glo = h->tlg + Q.N1; Q.gihi = h->tlg + Q.N1 + Q.N2; Q.gilo = h->tlg + 2 * Q.N1 + Q.N2;
@@ -1398,6 +1401,27 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       for (int j = 0; j < N2; ++j) mt[(size_t)N1 + N2 + j] = root(j, nt);
       PD_TRY(dalloc(h, &h->mtab, mt.size()));
       if (up(h->mtab, mt.data(), mt.size() * sizeof(double2))) return cleanup(fail(PD_ECUDA, "mixed table upload"));
+      // digit reversal of the DIF plans (k_tmix.cuh): frequency k = q0 + r0 q1 + … sits at position
+      // pos = q0 (L/r0) + q1 (L/(r0 r1)) + …
+      std::vector<int> rv(2 * (size_t)(N1 + N2));
+      auto rev = [](int L, const int8_t* r, int ns, int* fwd, int* inv) {
+        for (int k = 0; k < L; ++k) {
+          int kk = k, pos = 0, span = L;
+          for (int q = 0; q < ns; ++q) {
+            span /= r[q];
+            pos += (kk % r[q]) * span;
+            kk /= r[q];
+          }
+          fwd[pos] = k;
+          inv[k] = pos;
+        }
+      };
+      rev(N1, h->plan1, h->nst1, rv.data(), rv.data() + N1);
+      rev(N2, h->plan2, h->nst2, rv.data() + 2 * N1, rv.data() + 2 * N1 + N2);
+      int* drv = nullptr;
+      PD_TRY(dalloc(h, &drv, rv.size()));
+      if (up(drv, rv.data(), rv.size() * sizeof(int))) return cleanup(fail(PD_ECUDA, "mixed table upload"));
+      h->mrev = drv;
     }
     const size_t nc = (size_t)nt * (size_t)((h->ns + 1) / 2);
     PD_TRY(dalloc(h, &h->spec, nc));
