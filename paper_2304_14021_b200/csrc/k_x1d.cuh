@@ -26,11 +26,12 @@ namespace pd {
 
 constexpr int kX1Warps = 8;               // warps per CTA (2 CTAs per SM)
 constexpr int kX1Threads = kX1Warps * 32;
-constexpr int kX1H = 32;                  // half transform size (N_x ≤ 64)
-constexpr int kX1BP = 40;                 // B tile pitch (doubles)
-constexpr int kX1RP = 68;                 // staged row pitch: 2 ghosts | 64 | 2 ghosts
+constexpr int kX1H = 32;                  // half transform size (N_x ≤ 64, or 65 Neumann nodes)
+constexpr int kX1K = 36;                  // B rows (K): j < 32, plus the centre j = 32 of N_x = 65
+constexpr int kX1BP = 40;                 // B tile pitch (doubles): modes i < 32, plus i = 32 (mode 64)
+constexpr int kX1RP = 70;                 // staged row pitch: 2 ghosts | up to 65 | 2 ghosts
 constexpr int kX1In = 9 * kX1RP;          // one input buffer: 9 rows (MODE 0: rows n0-1 .. n0+7)
-constexpr size_t kX1Smem = (size_t)(2 * kX1H * kX1BP + kX1Warps * 2 * kX1In) * sizeof(double);
+constexpr size_t kX1Smem = (size_t)(2 * kX1K * kX1BP + kX1Warps * 2 * kX1In) * sizeof(double);
 
 struct X1Params {
   int nx, nt;
@@ -41,7 +42,7 @@ struct X1Params {
   int bc;
   int64_t bstride;
   ResidualParams R;          // stencil coefficients (MODE 0)
-  const double* B;           // [2][32][32]: B[0][j][i] = T[2i][j], B[1][j][i] = T[2i+1][j], zero padded
+  const double* B;           // [2][kX1K][kX1BP]: B[0][j][i] = T[2i][j], B[1][j][i] = T[2i+1][j], zero padded
   DevStats* st;
 };
 
@@ -69,11 +70,14 @@ __global__ void __launch_bounds__(kX1Threads, 2)
 k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __restrict__ out, X1Params Q) {
   extern __shared__ double xs[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* Bs = xs;                                                  // [2][32][kX1BP]
-  double* const ibuf = xs + 2 * kX1H * kX1BP + warp * 2 * kX1In;   // two buffers of kX1In
-  for (int i = tid; i < 2 * kX1H * kX1H; i += kX1Threads) Bs[(i >> 5) * kX1BP + (i & 31)] = __ldg(Q.B + i);
+  double* Bs = xs;                                                  // [2][kX1K][kX1BP]
+  double* const ibuf = xs + 2 * kX1K * kX1BP + warp * 2 * kX1In;   // two buffers of kX1In
+  for (int i = tid; i < 2 * kX1K * kX1BP; i += kX1Threads) Bs[i] = __ldg(Q.B + i);
   __syncthreads();
   const int nx = Q.nx, nh = nx >> 1;
+  // N_x = 65 (Neumann m = 64, c6n): the centre column j = 32 is a ninth K step of the even product
+  // and mode 64 a fifth N tile (DCT-I: T[2i][32] = 2(-1)^i, T[64][j] = c_j (-1)^j)
+  const bool ext = nx > 2 * kX1H;
   const int nunits = (Q.nt + 7) >> 3;
   // block offsets of this lane's two columns (time-slab input layout)
   const int64_t boff0 = Q.bc ? (int64_t)(lane / Q.bc) * Q.bstride + lane % Q.bc : 0;
@@ -109,10 +113,10 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
     cp_async_commit();
     const int n0 = u * 8, rows = min(8, Q.nt - n0);
     // MODE 3: this lane's U values (row g, columns 2c .. 2c+3 of each n-tile), in flight during the math
-    double uv[4][4];
+    double uv[5][4];
     if (MODE == 3) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < 5; ++t)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int x = 2 * (8 * t + 2 * q) + e;
@@ -135,9 +139,9 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
       __syncwarp();
     }
     // A fragments: row g, columns 4kk + q of s | d, s_j = v_j + v_{n-1-j}, d_j = v_j - v_{n-1-j}
-    double as[8], ad[8];
+    double as[9], ad[9];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
+    for (int kk = 0; kk < 9; ++kk) {
       const int j = 4 * kk + q, jm = nx - 1 - j;
       const bool pair = j < nh, mid = (j == nh) && (nx & 1);
       double a = 0.0, b = 0.0;
@@ -164,27 +168,35 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
     }
     __syncwarp();                                   // the buffer is refilled two units from now
     // even modes 2i from s (B[0]), odd modes 2i+1 from d (B[1])
-    double ae[4][2], ao[4][2];
+    double ae[5][2], ao[4][2];
 #pragma unroll
     for (int t = 0; t < 4; ++t) ae[t][0] = ae[t][1] = ao[t][0] = ao[t][1] = 0.0;
+    ae[4][0] = ae[4][1] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const double* be = Bs + (4 * kk + q) * kX1BP + g;
-      const double* bo = be + kX1H * kX1BP;
+      const double* bo = be + kX1K * kX1BP;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         dmma_f64(ae[t], as[kk], be[8 * t]);
         dmma_f64(ao[t], ad[kk], bo[8 * t]);
       }
+      if (ext) dmma_f64(ae[4], as[kk], be[32]);
+    }
+    if (ext) {                                      // the centre column (K step 9) of the even product
+      const double* be = Bs + (32 + q) * kX1BP + g;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) dmma_f64(ae[t], as[8], be[8 * t]);
     }
     // lane (g, q) holds out[g][2c], out[g][2c+1], out[g][2c+2], out[g][2c+3] for c = 8t + 2q:
     // (ae[t][0], ao[t][0], ae[t][1], ao[t][1])
     if (g < rows) {
       double* dst = out + (size_t)(n0 + g) * Q.ld_out;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < 5; ++t) {
+        if (t == 4 && !ext) break;
         const int x = 2 * (8 * t + 2 * q);
-        const double v[4] = {ae[t][0], ao[t][0], ae[t][1], ao[t][1]};
+        const double v[4] = {ae[t][0], t < 4 ? ao[t][0] : 0.0, ae[t][1], t < 4 ? ao[t][1] : 0.0};
         if (MODE <= 1 && Q.bc) {                    // time-slab blocks (bc even: pairs stay in one block)
           double* bo = out + (size_t)(n0 + g) * Q.bc;
           if (x < Q.ld_out)

@@ -342,7 +342,8 @@ int setup_fast_attrs(pd_handle* h) {
 }
 
 // k_x1d workspace row pitch: 2⌈N_x/2⌉ doubles (the time pass reads 16-byte pencil pairs)
-size_t x1_pitch(const pd_handle* h) { return (size_t)((h->nx + 1) / 2) * 2; }
+// (N_x = 65: 80, so time slabs of 2, 4, 5 or 8 ranks get even column blocks; the pads stay zero)
+size_t x1_pitch(const pd_handle* h) { return h->nx > 64 ? 80 : (size_t)((h->nx + 1) / 2) * 2; }
 
 ResidualParams residual_params(pd_handle* h) {
   ResidualParams R;
@@ -1237,7 +1238,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       h->n1 = 1 << h->log2n1;
       h->n2 = 1 << h->log2n2;
     }
-    h->x1 = h->tlong && p->dim == 1 && h->nx <= 2 * kX1H;
+    h->x1 = h->tlong && p->dim == 1 && (h->nx <= 2 * kX1H || (h->neumann && h->nx == 2 * kX1H + 1));
     if (const char* f3 = std::getenv("PARADIAG_TLFUSE")) h->tlfuse = std::atoi(f3) != 0;
     if (const char* f4 = std::getenv("PARADIAG_GRAPH")) h->use_graph = std::atoi(f4) != 0;
     if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
@@ -1441,11 +1442,11 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       const long a = ((long)(k + 1) * (j + 1)) % (2L * M);
       return 2.0 * std::sin(M_PI * (double)a / M);
     };
-    std::vector<double> B((size_t)2 * kX1H * kX1H, 0.0);
+    std::vector<double> B((size_t)2 * kX1K * kX1BP, 0.0);              // [2][kX1K][kX1BP]
     for (int j = 0; j < hc; ++j)
       for (int i = 0; 2 * i < n; ++i) {
-        B[(size_t)j * kX1H + i] = Tkj(2 * i, j);
-        if (j < nh && 2 * i + 1 < n) B[(size_t)(kX1H + j) * kX1H + i] = Tkj(2 * i + 1, j);
+        B[(size_t)j * kX1BP + i] = Tkj(2 * i, j);
+        if (j < nh && 2 * i + 1 < n) B[(size_t)(kX1K + j) * kX1BP + i] = Tkj(2 * i + 1, j);
       }
     PD_TRY(dalloc(h, &h->x1T, B.size()));
     if (up(h->x1T, B.data(), B.size() * sizeof(double))) return cleanup(fail(PD_ECUDA, "T upload"));
