@@ -518,7 +518,8 @@ def main():
     # exactly what the library's sharded entry points accept (paradiag_init_slab / tslab_check)
     slab_ok = p.dim == 2 and p.kind in ("biharmonic", "linear_ch") and p.theta == 1.0 and \
         64 <= p.m <= 2048 and 32 <= p.nt <= 1024
-    tslab_ok = p.dim == 1 and p.kind in ("biharmonic", "linear_ch") and p.nt > 4096 and p.nx <= 64
+    tslab_ok = p.dim == 1 and p.kind in ("biharmonic", "linear_ch") and p.nt > 4096 and \
+        (p.nx <= 64 or (p.bc == "neumann" and p.nx == 65))
     if args.parallelism == "slab" and not slab_ok:
         raise SystemExit(f"--parallelism slab: {args.config} is not shardable in slabs "
                          "(2D linear kinds, theta = 1, 64 <= m <= 2048, 32 <= N_t <= 1024)")

@@ -82,6 +82,7 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
   // block offsets of this lane's two columns (time-slab input layout)
   const int64_t boff0 = Q.bc ? (int64_t)(lane / Q.bc) * Q.bstride + lane % Q.bc : 0;
   const int64_t boff1 = Q.bc ? (int64_t)((lane + 32) / Q.bc) * Q.bstride + (lane + 32) % Q.bc : 0;
+  const int64_t boff2 = Q.bc ? (int64_t)((lane + 64) / Q.bc) * Q.bstride + (lane + 64) % Q.bc : 0;   // N_x = 65
   const int gw = blockIdx.x * kX1Warps + warp, nw = gridDim.x * kX1Warps;
   constexpr int NR = MODE == 0 ? 9 : 8;                             // staged rows per unit
   // cp.async copies of unit `u` (its rows; MODE 0 also row n0-1, = u0 for the first unit) into `b`
@@ -96,6 +97,7 @@ k_x1d(const double* __restrict__ u0, const double* __restrict__ in, double* __re
         const double* src = in + (size_t)n * Q.bc;
         if (lane < nx) cp_async8(dst + lane, src + boff0);
         if (lane + 32 < nx) cp_async8(dst + lane + 32, src + boff1);
+        if (lane + 64 < nx) cp_async8(dst + lane + 64, src + boff2);
       } else {
         const double* src = (MODE == 0 && n < 0) ? u0 : in + (size_t)n * Q.ld_in;
         for (int x = lane; x < nx; x += 32) cp_async8(dst + x, src + x);

@@ -31,7 +31,10 @@ UNFORCED = {
     "c6_nt8192": _c6(8192),                    # five-stage time pass (N2 = 64)
     "c6_nt32768": _c6(32768),                  # fused pass B (N2 = 1024)
 }
-CASES = {**FORCED, **UNFORCED}
+# c6n physics (Neumann, 65 nodes: DMMA x path with the x-mode pitch 80, so 2, 4, 8 ranks get even
+# column blocks) with a mixed-radix window (2000 = 40 x 50, k_tmix.cuh)
+MIXED = {"c6n_nt2000": twin("c6n", nt=2000, t_window=2000e-6)}
+CASES = {**FORCED, **UNFORCED, **MIXED}
 
 
 def _run(cuda_lib, monkeypatch, name, P, K=3):
@@ -71,7 +74,7 @@ def test_virtual_time_slabs_match_single_gpu(cuda_lib, monkeypatch, name, P):
         assert st == st_ref
 
 
-@pytest.mark.parametrize("name", sorted(FORCED))
+@pytest.mark.parametrize("name", sorted(FORCED) + sorted(MIXED))
 def test_virtual_time_slabs_match_oracle(cuda_lib, monkeypatch, name):
     p, u0, U0, out = _run(cuda_lib, monkeypatch, name, 4, K=2)
     U_o = U0
