@@ -51,6 +51,7 @@ struct TlongParams {
   // mixed-radix factors (k_tmix.cuh; N1, N2 products of 2, 4, 5, 8): radix plans, root tables
   // mt1[j] = W_{N1}^j, mt2[j] = W_{N2}^j, mtN[b] = W_N^b (b < N2)
   int mixed;
+  int mxp;                 // pencil pairs per CTA of the mixed passes (8 or 4; fused pass B: mxp/2 per group)
   int nst1, nst2;
   int8_t plan1[12], plan2[12];
   const double2* mt1;

@@ -95,15 +95,27 @@ PD_DEV double2 mix_root(const double2* __restrict__ tab, int e) {
   return w;
 }
 
-// One stage of radix R on the pencil x[i·pitch] (i < L) of the calling warp.  Forward (DIF): span
-// len → m = len/R: gather a_t = x[b + j + t m], y = DFT_R(a), y_q ·= W_len^{j q}, store at b + j + q m.
-// Inverse (DIT, SIGN = +1): span m → len = m R: a_q = x[b + j + q m]·W_len^{-j q}, y = DFT_R^{+}(a),
-// store y_t at b + j + t m.  tab = roots of L (W_len^{jq} = W_L^{jq·L/len}).
+// One stage of radix R on the pencil x[i·pitch] (i < L) of the calling warp group (WPP warps per
+// pencil pair, `sub` = the warp's index in its group, group barrier `gbar` between stages).
+// Forward (DIF): span len → m = len/R: gather a_t = x[b + j + t m], y = DFT_R(a), y_q ·= W_len^{j q},
+// store at b + j + q m.  Inverse (DIT, SIGN = +1): span m → len = m R: a_q = x[b + j + q m]·W_len^{-j q},
+// y = DFT_R^{+}(a), store y_t at b + j + t m.  tab = roots of L (W_len^{jq} = W_L^{jq·L/len}).
+// idx / m by a 2^20-scaled reciprocal: exact for idx < L/R ≤ 512 and m < 1024 (the error
+// idx·(⌈2^20/m⌉ − 2^20/m)/2^20 < 2^-11 stays below the 1/m gap to the next integer).
+constexpr int kMxWpp = 2;                                   // warps per pencil pair
+
+PD_DEV void mx_group_sync(int gid) {                        // the kMxWpp warps of pencil group gid
+  if (kMxWpp == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(kMxWpp * 32) : "memory");
+}
+
 template <int R, int SIGN>
-PD_DEV void mix_stage(double2* x, int pitch, int L, int len, const double2* __restrict__ tab, int lane) {
+PD_DEV void mix_stage(double2* x, int pitch, int L, int len, const double2* __restrict__ tab, int t0) {
   const int m = len / R, nb = L / len, stride = L / len;
-  for (int idx = lane; idx < nb * m; idx += 32) {
-    const int b = (idx / m) * len, j = idx - (idx / m) * m;
+  const unsigned inv_m = ((1u << 20) + (unsigned)m - 1u) / (unsigned)m;
+  for (int idx = t0; idx < nb * m; idx += 32 * kMxWpp) {
+    const int bq = (int)(((unsigned)idx * inv_m) >> 20);
+    const int b = bq * len, j = idx - bq * m;
     double2 a[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) a[t] = x[(b + j + t * m) * pitch];
@@ -119,103 +131,186 @@ PD_DEV void mix_stage(double2* x, int pitch, int L, int len, const double2* __re
 #pragma unroll
     for (int t = 0; t < R; ++t) x[(b + j + t * m) * pitch] = a[t];
   }
-  __syncwarp();
 }
 
 template <int SIGN>
-PD_DEV void mix_stage_rt(int R, double2* x, int pitch, int L, int len, const double2* tab, int lane) {
+PD_DEV void mix_stage_rt(int R, double2* x, int pitch, int L, int len, const double2* tab, int t0, int gid) {
   switch (R) {
-    case 2: mix_stage<2, SIGN>(x, pitch, L, len, tab, lane); break;
-    case 4: mix_stage<4, SIGN>(x, pitch, L, len, tab, lane); break;
-    case 5: mix_stage<5, SIGN>(x, pitch, L, len, tab, lane); break;
-    default: mix_stage<8, SIGN>(x, pitch, L, len, tab, lane); break;
+    case 2: mix_stage<2, SIGN>(x, pitch, L, len, tab, t0); break;
+    case 4: mix_stage<4, SIGN>(x, pitch, L, len, tab, t0); break;
+    case 5: mix_stage<5, SIGN>(x, pitch, L, len, tab, t0); break;
+    default: mix_stage<8, SIGN>(x, pitch, L, len, tab, t0); break;
   }
+  mx_group_sync(gid);
 }
 
-// Forward (DIF) transform of length L of the warp's pencil: natural in, digit-reversed out
-PD_DEV void mix_fft_fwd(double2* x, int pitch, int L, const int8_t* r, int ns, const double2* tab, int lane) {
+// Compile-time plans (the production lengths: N_t = 10⁶ → L = 1000 = 8·5·5·5, N_t = 10⁴ → L = 100
+// = 4·5·5): the same stages with L, the span and the radix as constants, so the index arithmetic
+// folds (ncu c6n: integer multiply-adds were the largest instruction class of the runtime-plan
+// stages, and their three runtime divisions per stage showed up as I2F stalls) and the butterfly
+// loop unrolls.  Identical arithmetic to mix_stage.
+template <int R, int L, int LEN, int SIGN, int NTP>
+PD_DEV void mix_stage_ct(double2* x, int pitch, const double2* __restrict__ tab, int t0) {
+  constexpr int m = LEN / R, nb = L / LEN, stride = L / LEN, cnt = nb * m, IT = (cnt + NTP - 1) / NTP;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int idx = t0 + it * NTP;
+    if (idx < cnt) {
+      const int bq = idx / m;
+      const int b = bq * LEN, j = idx - bq * m;
+      double2 a[R];
+#pragma unroll
+      for (int t = 0; t < R; ++t) a[t] = x[(b + j + t * m) * pitch];
+      if (SIGN > 0) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<+1>(tab, j * q * stride));
+      }
+      dft_r<R, SIGN>(a);
+      if (SIGN < 0) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<-1>(tab, j * q * stride));
+      }
+#pragma unroll
+      for (int t = 0; t < R; ++t) x[(b + j + t * m) * pitch] = a[t];
+    }
+  }
+}
+template <int L, int LEN, int NTP, int R, int... Rest>
+PD_DEV void mix_fwd_ct(double2* x, int pitch, const double2* tab, int t0, int gid) {
+  mix_stage_ct<R, L, LEN, -1, NTP>(x, pitch, tab, t0);
+  mx_group_sync(gid);
+  if constexpr (sizeof...(Rest) > 0) mix_fwd_ct<L, LEN / R, NTP, Rest...>(x, pitch, tab, t0, gid);
+}
+template <int L, int LEN, int NTP, int R, int... Rest>
+PD_DEV void mix_inv_ct(double2* x, int pitch, const double2* tab, int t0, int gid) {
+  if constexpr (sizeof...(Rest) > 0) mix_inv_ct<L, LEN / R, NTP, Rest...>(x, pitch, tab, t0, gid);
+  mix_stage_ct<R, L, LEN, +1, NTP>(x, pitch, tab, t0);
+  mx_group_sync(gid);
+}
+PD_DEV bool plan_is(const int8_t* r, int ns, int n, int a, int b, int c, int d) {
+  return ns == n && r[0] == a && r[1] == b && (n < 3 || r[2] == c) && (n < 4 || r[3] == d);
+}
+
+// Forward (DIF) transform of length L of the group's pencil: natural in, digit-reversed out.
+// t0 = sub·32 + lane; gid = pencil group (every warp of the group calls, so the barriers match).
+PD_DEV void mix_fft_fwd(double2* x, int pitch, int L, const int8_t* r, int ns, const double2* tab, int t0, int gid) {
+  constexpr int NTP = kMxWpp * 32;
+  if (L == 1000 && plan_is(r, ns, 4, 8, 5, 5, 5)) return mix_fwd_ct<1000, 1000, NTP, 8, 5, 5, 5>(x, pitch, tab, t0, gid);
+  if (L == 100 && plan_is(r, ns, 3, 4, 5, 5, 0)) return mix_fwd_ct<100, 100, NTP, 4, 5, 5>(x, pitch, tab, t0, gid);
   int len = L;
   for (int s = 0; s < ns; ++s) {
-    mix_stage_rt<-1>(r[s], x, pitch, L, len, tab, lane);
+    mix_stage_rt<-1>(r[s], x, pitch, L, len, tab, t0, gid);
     len /= r[s];
   }
 }
 // Inverse (DIT, conjugate roots, unnormalised): digit-reversed in, natural out
-PD_DEV void mix_fft_inv(double2* x, int pitch, int L, const int8_t* r, int ns, const double2* tab, int lane) {
+PD_DEV void mix_fft_inv(double2* x, int pitch, int L, const int8_t* r, int ns, const double2* tab, int t0, int gid) {
+  constexpr int NTP = kMxWpp * 32;
+  if (L == 1000 && plan_is(r, ns, 4, 8, 5, 5, 5)) return mix_inv_ct<1000, 1000, NTP, 8, 5, 5, 5>(x, pitch, tab, t0, gid);
+  if (L == 100 && plan_is(r, ns, 3, 4, 5, 5, 0)) return mix_inv_ct<100, 100, NTP, 4, 5, 5>(x, pitch, tab, t0, gid);
   int len = 1;
   for (int s = ns - 1; s >= 0; --s) {
     len *= r[s];
-    mix_stage_rt<+1>(r[s], x, pitch, L, len, tab, lane);
+    mix_stage_rt<+1>(r[s], x, pitch, L, len, tab, t0, gid);
   }
 }
 
-// four-step twiddle W_N^{SIGN·n2·k1} = W_{N1}^{a}·W_N^{b}, n2·k1 mod N = a·N2 + b
+// four-step twiddle W_N^{SIGN·n2·k1} = W_{N1}^{a}·W_N^{b}, n2·k1 = a·N2 + b (n2 < N2, k1 < N1, so
+// n2·k1 < N: no reduction mod N); a = ⌊e/N2⌋ by the reciprocal inv_n2 = ⌈2^32/N2⌉, exact for
+// e < 2^32/N2 (e < N ≤ 2^20, N2 ≤ 1024)
 template <int SIGN>
-PD_DEV double2 mix_tw4(const TlongParams& Q, int n2, int k1) {
-  const int e = (n2 * k1) % Q.N, a = e / Q.N2, b = e - a * Q.N2;       // n2·k1 < N ≤ 2^20: 32-bit
-  return cmul(mix_root<SIGN>(Q.mt1, a), mix_root<SIGN>(Q.mtN, b));      // mtN[b] = W_N^b, b < N2
+PD_DEV double2 mix_tw4(const TlongParams& Q, int n2, int k1, unsigned inv_n2) {
+  const unsigned e = (unsigned)(n2 * k1), a = __umulhi(e, inv_n2), b = e - a * (unsigned)Q.N2;
+  return cmul(mix_root<SIGN>(Q.mt1, (int)a), mix_root<SIGN>(Q.mtN, (int)b));      // mtN[b] = W_N^b, b < N2
 }
+PD_DEV unsigned mx_inv_n2(int N2) { return (unsigned)((0x100000000ull + (unsigned)N2 - 1) / (unsigned)N2); }
 
-constexpr int kMxRowC = kTlPairs + 1;                 // staged row pitch (complex): 8 pairs + 1 pad
+// Pass kernels: NP pencil pairs per CTA (8: 128-byte row segments, one CTA per SM; 4: 64-byte
+// segments, two CTAs per SM so that one CTA's loads and stores overlap the other's transform).
 
 // Pass A forward: rows n = N2·n1 + n2, 16 real columns (8 pairs) of chunk; z = γ_n (r[2p] + i r[2p+1]);
 // length-N1 DFT over n1 (DIF); × W_N^{n2 k1}; store Y[k1][n2][p] (k1 un-reversed).
-__global__ void __launch_bounds__(kTlThreads, 1) k_mx_a_fwd(const double* __restrict__ in, double2* __restrict__ Y,
+// 16 warps: two per pencil pair (stages split between them, group barriers); pencil pairs past P
+// (the padded last chunk) skip the transform.  Rows are staged with 16-byte copies when the row
+// pitch is even.
+template <int NP>
+__global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(const double* __restrict__ in, double2* __restrict__ Y,
                                                               TlongParams Q) {
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   double* sd = reinterpret_cast<double*>(sm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = blockIdx.x % Q.nch;
-  const int n2 = (int)(blockIdx.x / Q.nch);
-  const int64_t c0 = chunk * (2 * kTlPairs);
+  const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
+  const int64_t chunk = blockIdx.x % nch;
+  const int n2 = (int)(blockIdx.x / nch);
+  const int64_t c0 = chunk * (2 * NP);
   const int L = Q.N1;
-  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {      // rows of 16 doubles (128 B)
-    const int c = idx & 15, n1 = idx >> 4;
+  const bool v16 = (Q.ld & 1) == 0;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {      // column pairs of 16-double rows
+    const int c = 2 * (idx % NP), n1 = idx / NP;
     const int64_t n = (int64_t)Q.N2 * n1 + n2;
     double* d = sd + n1 * 2 * kMxRowC + c;
-    if (c0 + c < Q.ns) cp_async8(d, in + n * Q.ld + c0 + c);
-    else *d = 0.0;
+    const double* g = in + n * Q.ld + c0 + c;
+    if (c0 + c + 1 < Q.ns) {
+      if (v16) cp_async16(d, g);
+      else { cp_async8(d, g); cp_async8(d + 1, g + 1); }
+    } else if (c0 + c < Q.ns) {
+      cp_async8(d, g);
+      d[1] = 0.0;
+    } else {
+      d[0] = 0.0;
+      d[1] = 0.0;
+    }
   }
   cp_async_commit();
   cp_async_wait_all();
   const double g2 = __ldg(Q.glo + n2);
-  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {      // γ_n = ghi[n1]·glo[n2], own elements
-    const int c = idx & 15, n1 = idx >> 4;
-    sd[n1 * 2 * kMxRowC + c] *= __ldg(Q.ghi + n1) * g2;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {    // γ_n = ghi[n1]·glo[n2], own elements
+    const int c = 2 * (idx % NP), n1 = idx / NP;
+    const double gm = __ldg(Q.ghi + n1) * g2;
+    double* d = sd + n1 * 2 * kMxRowC + c;
+    d[0] *= gm;
+    d[1] *= gm;
   }
   __syncthreads();
-  mix_fft_fwd(sm + warp, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, lane);
+  if (chunk * NP + pen < Q.P) mix_fft_fwd(sm + pen, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, t0, pen);
   __syncthreads();
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, pos = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  const unsigned inv_n2 = mx_inv_n2(Q.N2);
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, pos = idx / NP;
+    const int64_t p = chunk * NP + w;
     const int k1 = __ldg(Q.rev1 + pos);
-    if (p < Q.P) Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] = cmul(sm[pos * kMxRowC + w], mix_tw4<-1>(Q, n2, k1));
+    if (p < Q.P) Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] = cmul(sm[pos * kMxRowC + w], mix_tw4<-1>(Q, n2, k1, inv_n2));
   }
 }
 
 // Pass B forward: Y rows k1·N2 + n2 (n2 < N2); length-N2 DFT over n2 (DIF); X[k1 + N1·k2][p].
-__global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_fwd(const double2* __restrict__ Y, double2* __restrict__ X,
+template <int NP>
+__global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_fwd(const double2* __restrict__ Y, double2* __restrict__ X,
                                                               TlongParams Q) {
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = blockIdx.x % Q.nch;
-  const int k1 = (int)(blockIdx.x / Q.nch);
+  const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
+  const int64_t chunk = blockIdx.x % nch;
+  const int k1 = (int)(blockIdx.x / nch);
   const int L = Q.N2;
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, n2 = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, n2 = idx / NP;
+    const int64_t p = chunk * NP + w;
     if (p < Q.P) cp_async16(sm + n2 * kMxRowC + w, Y + ((int64_t)k1 * Q.N2 + n2) * Q.P + p);
     else sm[n2 * kMxRowC + w] = make_double2(0.0, 0.0);
   }
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  mix_fft_fwd(sm + warp, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, lane);
+  if (chunk * NP + pen < Q.P) mix_fft_fwd(sm + pen, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, t0, pen);
   __syncthreads();
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, pos = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, pos = idx / NP;
+    const int64_t p = chunk * NP + w;
     const int k2 = __ldg(Q.rev2 + pos);
     if (p < Q.P) X[((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p] = sm[pos * kMxRowC + w];
   }
@@ -223,16 +318,20 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_fwd(const double2* __res
 
 // Pass B inverse: X[k1 + N1·k2] placed at the digit-reversed position of k2, inverse DIT over k2
 // → natural n2; Y[k1][n2].
-__global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_inv(const double2* __restrict__ X, double2* __restrict__ Y,
+template <int NP>
+__global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_inv(const double2* __restrict__ X, double2* __restrict__ Y,
                                                               TlongParams Q) {
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = blockIdx.x % Q.nch;
-  const int k1 = (int)(blockIdx.x / Q.nch);
+  const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
+  const int64_t chunk = blockIdx.x % nch;
+  const int k1 = (int)(blockIdx.x / nch);
   const int L = Q.N2;
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, k2 = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, k2 = idx / NP;
+    const int64_t p = chunk * NP + w;
     double2* d = sm + __ldg(Q.irev2 + k2) * kMxRowC + w;
     if (p < Q.P) cp_async16(d, X + ((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p);
     else *d = make_double2(0.0, 0.0);
@@ -240,48 +339,166 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_mx_b_inv(const double2* __res
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  mix_fft_inv(sm + warp, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, lane);
+  if (chunk * NP + pen < Q.P) mix_fft_inv(sm + pen, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, t0, pen);
   __syncthreads();
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, n2 = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, n2 = idx / NP;
+    const int64_t p = chunk * NP + w;
     if (p < Q.P) Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] = sm[n2 * kMxRowC + w];
   }
 }
 
 // Pass A inverse: Y[k1][n2] × W_N^{-n2 k1} at the digit-reversed position of k1, inverse DIT over
 // k1 → natural n1; out rows n = N2·n1 + n2 with Γ_α⁻¹·(1/N_t)·(spatial normalisation).
-__global__ void __launch_bounds__(kTlThreads, 1) k_mx_a_inv(const double2* __restrict__ Y, double* __restrict__ out,
+template <int NP>
+__global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_inv(const double2* __restrict__ Y, double* __restrict__ out,
                                                               TlongParams Q) {
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   double* sd = reinterpret_cast<double*>(sm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = blockIdx.x % Q.nch;
-  const int n2 = (int)(blockIdx.x / Q.nch);
-  const int64_t c0 = chunk * (2 * kTlPairs);
+  const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
+  const int64_t chunk = blockIdx.x % nch;
+  const int n2 = (int)(blockIdx.x / nch);
+  const int64_t c0 = chunk * (2 * NP);
   const int L = Q.N1;
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {
-    const int w = idx & 7, k1 = idx >> 3;
-    const int64_t p = chunk * kTlPairs + w;
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int w = idx % NP, k1 = idx / NP;
+    const int64_t p = chunk * NP + w;
     double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
     if (p < Q.P) cp_async16(d, Y + ((int64_t)k1 * Q.N2 + n2) * Q.P + p);
     else *d = make_double2(0.0, 0.0);
   }
   cp_async_commit();
   cp_async_wait_all();
-  for (int idx = threadIdx.x; idx < L * kTlPairs; idx += kTlThreads) {   // × W_N^{-n2 k1}, own elements
-    const int w = idx & 7, k1 = idx >> 3;
+  const unsigned inv_n2 = mx_inv_n2(Q.N2);
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {   // × W_N^{-n2 k1}, own elements
+    const int w = idx % NP, k1 = idx / NP;
     double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
-    *d = cmul(*d, mix_tw4<+1>(Q, n2, k1));
+    *d = cmul(*d, mix_tw4<+1>(Q, n2, k1, inv_n2));
   }
   __syncthreads();
-  mix_fft_inv(sm + warp, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, lane);
+  if (chunk * NP + pen < Q.P) mix_fft_inv(sm + pen, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, t0, pen);
   __syncthreads();
-  for (int idx = threadIdx.x; idx < L * 16; idx += kTlThreads) {
-    const int c = idx & 15, n1 = idx >> 4;
+  const bool v16 = (Q.ld & 1) == 0;
+  const double g2 = __ldg(Q.gilo + n2);
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
+    const int c = 2 * (idx % NP), n1 = idx / NP;
     const int64_t n = (int64_t)Q.N2 * n1 + n2;
-    if (c0 + c < Q.ns)
-      out[n * Q.ld + c0 + c] = sd[n1 * 2 * kMxRowC + c] * (__ldg(Q.gihi + n1) * __ldg(Q.gilo + n2));
+    const double gm = __ldg(Q.gihi + n1) * g2;
+    const double* d = sd + n1 * 2 * kMxRowC + c;
+    double* o = out + n * Q.ld + c0 + c;
+    if (c0 + c + 1 < Q.ns) {
+      if (v16) *reinterpret_cast<double2*>(o) = make_double2(d[0] * gm, d[1] * gm);
+      else { o[0] = d[0] * gm; o[1] = d[1] * gm; }
+    } else if (c0 + c < Q.ns) {
+      o[0] = d[0] * gm;
+    }
+  }
+}
+
+// Pass B forward + Step (2) + pass B inverse in one kernel for the mixed-radix split (the
+// counterpart of k_tl_b_fused): a CTA holds the k1 = j and k1 = N1 − j groups (j = 0 pairs with
+// N1/2 when N1 is even) of 4 pencil pairs, so every bin k = k1 + N1·k2 finds its Hermitian mirror
+// N − k in shared memory: k1 = 0 → (0, (N2 − k2) mod N2); k1 = N1/2 → (N1/2, N2 − 1 − k2);
+// otherwise (N1 − k1, N2 − 1 − k2).  The forward DIF leaves bin k2 at its digit-reversed position,
+// the divide works position by position (reads of both mirrors, CTA barrier, writes), and the
+// inverse DIT takes exactly that order back to natural n2: Y is read and written once, in place,
+// instead of three round trips through X.
+// MP pencil pairs per group (4: 160 KB, one CTA per SM; 2: 80 KB, two per SM)
+template <int MP>
+constexpr size_t mx_fused_smem() { return (size_t)2 * 1024 * (MP + 1) * sizeof(double2); }
+
+template <bool PLAIN, int MP>      // PLAIN: θ = 1 and no λ₃ term, divisor d_k + μ
+__global__ void __launch_bounds__(2 * MP * kMxWpp * 32, MP <= 2 ? 2 : 1) k_mx_b_fused(double2* __restrict__ Y, TlongParams Q) {
+  constexpr int kMfPairs = MP, kMfRowC = MP + 1, NT = 2 * MP * kMxWpp * 32;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / (kMfPairs * kMxWpp), pen = (warp / kMxWpp) % kMfPairs;
+  const int t0 = (warp % kMxWpp) * 32 + lane, gid = grp * kMfPairs + pen;
+  const int64_t nch4 = (Q.P + kMfPairs - 1) / kMfPairs;
+  const int64_t chunk = blockIdx.x % nch4;
+  const int j = (int)(blockIdx.x / nch4);
+  const int L = Q.N2;
+  const bool two = j != 0 || (Q.N1 & 1) == 0;          // does the second group exist
+  const int k1b = j == 0 ? Q.N1 / 2 : Q.N1 - j;
+  const int ng = two ? 2 : 1;
+  for (int idx = threadIdx.x; idx < ng * L * kMfPairs; idx += NT) {
+    const int w = idx & (kMfPairs - 1), row = idx / kMfPairs;
+    const int g = row >= L ? 1 : 0, n2 = row - g * L;
+    const int64_t p = chunk * kMfPairs + w;
+    double2* d = sm + (g * L + n2) * kMfRowC + w;
+    if (p < Q.P) cp_async16(d, Y + ((int64_t)(g ? k1b : j) * Q.N2 + n2) * Q.P + p);
+    else *d = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  const bool real_pen = chunk * kMfPairs + pen < Q.P && (grp == 0 || two);
+  if (real_pen) mix_fft_fwd(sm + grp * L * kMfRowC + pen, kMfRowC, L, Q.plan2, Q.nst2, Q.mt2, t0, gid);
+  __syncthreads();
+  // Step (2) at every staged position: reads of the element and its mirror into registers first
+  constexpr int kPer = (2 * 1024 * kMfPairs + NT - 1) / NT;   // 16
+  double2 nv[kPer];
+  const double jbar = Q.T.kind >= 2 ? Q.T.st->jbar : 0.0;
+  // the pair column w = idx mod MP is the same for all of a thread's elements (NT is a multiple
+  // of MP): its two modes' eigenvalues once per thread
+  const int64_t p_t = chunk * kMfPairs + (threadIdx.x & (kMfPairs - 1));
+  const int64_t sa_t = 2 * p_t, sb_t = sa_t + 1;
+  const bool hb_t = sb_t < Q.ns, real_t = p_t < Q.P;
+  const double mua = real_t ? mode_mu(sa_t, Q.T, jbar) : 0.0;
+  const double mub = real_t && hb_t ? mode_mu(sb_t, Q.T, jbar) : mua;
+  const double lama = real_t && Q.T.l3 ? mode_lam(sa_t, Q.T) : 0.0;
+  const double lamb = real_t && Q.T.l3 && hb_t ? mode_lam(sb_t, Q.T) : 0.0;
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int idx = threadIdx.x + r * NT;
+    nv[r] = make_double2(0.0, 0.0);
+    if (idx >= ng * L * kMfPairs) continue;
+    const int w = idx & (kMfPairs - 1), row = idx / kMfPairs;
+    const int g = row >= L ? 1 : 0, pos = row - g * L;
+    const int64_t p = chunk * kMfPairs + w;
+    if (p >= Q.P) continue;
+    const int k1 = g ? k1b : j;
+    const int k2 = __ldg(Q.rev2 + pos);
+    int mg, k2m;
+    if (k1 == 0) { mg = g; k2m = k2 == 0 ? 0 : L - k2; }
+    else if (2 * k1 == Q.N1) { mg = g; k2m = L - 1 - k2; }
+    else { mg = 1 - g; k2m = L - 1 - k2; }
+    const double2 Zl = sm[(g * L + pos) * kMfRowC + w];
+    const double2 Zm = sm[(mg * L + __ldg(Q.irev2 + k2m)) * kMfRowC + w];
+    const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
+    const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
+    const int k = k1 + Q.N1 * k2;
+    const double2 d = __ldg(Q.T.dl + k);
+    double2 Af, Bf;
+    if (PLAIN) {
+      Af = cmul(A, cinv_fast(make_double2(d.x + mua, d.y)));
+      Bf = cmul(B, cinv_fast(make_double2(d.x + mub, d.y)));
+    } else {
+      Af = cmul(A, cinv_fast(shifted(d, Q.T.el, k, mua, Q.T.l3, lama)));
+      Bf = cmul(B, cinv_fast(shifted(d, Q.T.el, k, mub, Q.T.l3, lamb)));
+    }
+    nv[r] = make_double2(Af.x - Bf.y, Af.y + Bf.x);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int idx = threadIdx.x + r * NT;
+    if (idx >= ng * L * kMfPairs) continue;
+    const int w = idx & (kMfPairs - 1), row = idx / kMfPairs;
+    const int g = row >= L ? 1 : 0, pos = row - g * L;
+    sm[(g * L + pos) * kMfRowC + w] = nv[r];
+  }
+  __syncthreads();
+  if (real_pen) mix_fft_inv(sm + grp * L * kMfRowC + pen, kMfRowC, L, Q.plan2, Q.nst2, Q.mt2, t0, gid);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < ng * L * kMfPairs; idx += NT) {
+    const int w = idx & (kMfPairs - 1), row = idx / kMfPairs;
+    const int g = row >= L ? 1 : 0, n2 = row - g * L;
+    const int64_t p = chunk * kMfPairs + w;
+    if (p < Q.P) Y[((int64_t)(g ? k1b : j) * Q.N2 + n2) * Q.P + p] = sm[(g * L + n2) * kMfRowC + w];
   }
 }
 

@@ -182,6 +182,7 @@ struct pd_handle {
   // 1D long windows with N_x ≤ 64: x transforms as DMMA products with T (k_x1d.cuh), fused with
   // the residual (forward) and the update (inverse); x1T = Tᵀ zero padded to 64×64
   bool x1 = false;
+  int mxp = 4;                        // PARADIAG_MXPAIRS: pencil pairs per CTA of the mixed-radix passes (4: two CTAs per SM, measured 3.49 vs 3.59 ms on c6n; or 8)
   bool tlfuse = true;                 // PARADIAG_TLFUSE=0: unfused pass B / divide / pass B⁻¹ (A/B, tests)
   double* x1T = nullptr;
   double* tlg = nullptr;              // k_tlong.cuh split Γ_α tables: ghi[N1] glo[N2] gihi[N1] gilo[N2]
@@ -557,6 +558,7 @@ int tlong_time(pd_handle* h, const double* in, double* out, int64_t c0 = 0, int6
   Q.N = h->P.nt; Q.log2N = h->log2nt;
   Q.log2N1 = h->log2n1; Q.log2N2 = h->log2n2; Q.N1 = h->n1; Q.N2 = h->n2;
   Q.mixed = h->mixed ? 1 : 0;
+  Q.mxp = h->mxp;
   Q.nst1 = h->nst1; Q.nst2 = h->nst2;
   for (int i = 0; i < 12; ++i) { Q.plan1[i] = h->plan1[i]; Q.plan2[i] = h->plan2[i]; }
   Q.mt1 = h->mtab; Q.mt2 = h->mtab ? h->mtab + h->n1 : nullptr; Q.mtN = h->mtab ? h->mtab + h->n1 + h->n2 : nullptr;
@@ -1240,6 +1242,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     }
     h->x1 = h->tlong && p->dim == 1 && (h->nx <= 2 * kX1H || (h->neumann && h->nx == 2 * kX1H + 1));
     if (const char* f3 = std::getenv("PARADIAG_TLFUSE")) h->tlfuse = std::atoi(f3) != 0;
+    if (const char* f4 = std::getenv("PARADIAG_MXPAIRS")) h->mxp = std::atoi(f4) == 8 ? 8 : 4;
     if (const char* f4 = std::getenv("PARADIAG_GRAPH")) h->use_graph = std::atoi(f4) != 0;
     if (const char* f2 = std::getenv("PARADIAG_X1")) h->x1 = h->x1 && std::atoi(f2) != 0;
   }
@@ -1740,7 +1743,7 @@ int paradiag_solve_host(pd_handle* h, const double* u0_host, double* uT_host, pd
 int paradiag_launches_per_iteration(const pd_handle* h) {
   if (!h) return 0;
   if (h->P.jacobian == PD_JACOBIAN_TIME_AVG) return -1;   // data dependent (inner GMRES steps)
-  const int ntime = h->tlong ? (h->tlfuse && h->log2n2 == 10 && h->log2n1 >= 5 ? 3 : 5) : 1;
+  const int ntime = h->tlong ? (h->tlfuse && (h->mixed || (h->log2n2 == 10 && h->log2n1 >= 5)) ? 3 : 5) : 1;
   if (h->x1) return 1 /*reset*/ + 1 /*residual + x*/ + ntime + 1 /*x⁻¹ + update*/;
   int n = 1 /*reset*/ + 1 /*residual*/ + (can_fuse_update(h) ? 0 : 1) /*update*/;
   n += h->P.dim == 2 ? 4 + ntime : (h->tlong ? 2 + ntime : 3);

@@ -50,7 +50,8 @@ void tlong_split(int log2N, int* log2N1, int* log2N2) {
   *log2N1 = log2N - *log2N2;
 }
 
-bool tlong_fusable(const TlongParams& Q) { return !Q.mixed && Q.N2 == 1024 && Q.N1 >= 32; }
+// power of two: k_tl_b_fused (N2 = 1024); mixed radix: k_mx_b_fused (any split, N2 ≤ kMixMaxL)
+bool tlong_fusable(const TlongParams& Q) { return Q.mixed ? Q.N1 >= 2 : (Q.N2 == 1024 && Q.N1 >= 32); }
 
 bool mixed_split(int N, int* N1, int* N2, int8_t* plan1, int* ns1, int8_t* plan2, int* ns2) {
   auto smooth = [](int v) {
@@ -82,16 +83,36 @@ cudaError_t tlong_attrs() {
     return e;
   if ((e = cudaFuncSetAttribute(k_tl_b_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem)))
     return e;
-  if ((e = cudaFuncSetAttribute(k_mx_a_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mx_a_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mx_b_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mx_b_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem))) return e;
+#define PD_MXA(K, B)                                                                              \
+  if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(B)))) return e;
+  PD_MXA(k_mx_a_fwd<8>, 1024 * 9 * 16) PD_MXA(k_mx_a_inv<8>, 1024 * 9 * 16)
+  PD_MXA(k_mx_b_fwd<8>, 1024 * 9 * 16) PD_MXA(k_mx_b_inv<8>, 1024 * 9 * 16)
+  PD_MXA(k_mx_a_fwd<4>, 1024 * 5 * 16) PD_MXA(k_mx_a_inv<4>, 1024 * 5 * 16)
+  PD_MXA(k_mx_b_fwd<4>, 1024 * 5 * 16) PD_MXA(k_mx_b_inv<4>, 1024 * 5 * 16)
+  PD_MXA((k_mx_b_fused<true, 4>), mx_fused_smem<4>()) PD_MXA((k_mx_b_fused<false, 4>), mx_fused_smem<4>())
+  PD_MXA((k_mx_b_fused<true, 2>), mx_fused_smem<2>()) PD_MXA((k_mx_b_fused<false, 2>), mx_fused_smem<2>())
+#undef PD_MXA
   return cudaFuncSetAttribute(k_tl_b_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
 }
 
 bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cudaStream_t s) {
   if (stage == 5) {                                     // fused B: Y in place (`out`)
     if (!tlong_fusable(Q)) return false;
+    if (Q.mixed) {
+      const int mp = Q.mxp / 2;                          // pairs per group
+      const int64_t nch4 = (Q.P + mp - 1) / mp;
+      const unsigned grid = (unsigned)(nch4 * ((Q.N1 - 1) / 2 + 1));
+      double2* y = static_cast<double2*>(out);
+      const bool plain = !Q.T.el && !Q.T.l3;
+      if (mp == 2) {
+        if (plain) k_mx_b_fused<true, 2><<<grid, 256, mx_fused_smem<2>(), s>>>(y, Q);
+        else k_mx_b_fused<false, 2><<<grid, 256, mx_fused_smem<2>(), s>>>(y, Q);
+      } else {
+        if (plain) k_mx_b_fused<true, 4><<<grid, 512, mx_fused_smem<4>(), s>>>(y, Q);
+        else k_mx_b_fused<false, 4><<<grid, 512, mx_fused_smem<4>(), s>>>(y, Q);
+      }
+      return true;
+    }
     const int64_t nch4 = (Q.P + kFbPairs - 1) / kFbPairs;
     const unsigned grid = (unsigned)(nch4 * (Q.N1 / 2));
     if (!Q.T.el && !Q.T.l3) k_tl_b_fused<true><<<grid, kFbThreads, kFbSmem, s>>>(static_cast<double2*>(out), Q);
@@ -99,14 +120,20 @@ bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cu
     return true;
   }
   if (Q.mixed && stage != 2) {                          // mixed radix (k_tmix.cuh): one transform per CTA
-    const unsigned grid = (unsigned)(Q.nch * ((stage == 0 || stage == 4) ? Q.N2 : Q.N1));
-    switch (stage) {
-      case 0: k_mx_a_fwd<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double*>(in), static_cast<double2*>(out), Q); break;
-      case 1: k_mx_b_fwd<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
-      case 3: k_mx_b_inv<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break;
-      case 4: k_mx_a_inv<<<grid, kTlThreads, kTlSmem, s>>>(static_cast<const double2*>(in), static_cast<double*>(out), Q); break;
-      default: return false;
+    const int np = Q.mxp;                               // pencil pairs per CTA: 8 or 4
+    const unsigned grid = (unsigned)(((Q.P + np - 1) / np) * ((stage == 0 || stage == 4) ? Q.N2 : Q.N1));
+    const size_t sm = (size_t)1024 * (np + 1) * sizeof(double2);
+    const unsigned nt = (unsigned)(np * kMxWpp * 32);
+#define PD_MX(NP)                                                                                          \
+    switch (stage) {                                                                                       \
+      case 0: k_mx_a_fwd<NP><<<grid, nt, sm, s>>>(static_cast<const double*>(in), static_cast<double2*>(out), Q); break; \
+      case 1: k_mx_b_fwd<NP><<<grid, nt, sm, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break; \
+      case 3: k_mx_b_inv<NP><<<grid, nt, sm, s>>>(static_cast<const double2*>(in), static_cast<double2*>(out), Q); break; \
+      case 4: k_mx_a_inv<NP><<<grid, nt, sm, s>>>(static_cast<const double2*>(in), static_cast<double*>(out), Q); break; \
+      default: return false;                                                                               \
     }
+    if (np == 4) { PD_MX(4) } else { PD_MX(8) }
+#undef PD_MX
     return true;
   }
   if (stage == 2) {

@@ -91,3 +91,22 @@ def test_c6n_full_window_1e6(cuda_lib):
     g, c0 = modespace.mode_iterates(p, u0, K)
     ref = modespace.sample(p, g, c0, pts)
     assert np.abs(got - ref).max() <= 1e-10 * float(U.abs().max())
+
+
+@pytest.mark.parametrize("name", ["c6n_nt1000", "c6n_nt625", "c6n_nt2000_theta", "c5_m32_nt1000"])
+def test_mixed_fused_pass_b_matches_unfused(cuda_lib, monkeypatch, name):
+    """The fused mixed-radix pass B (k_mx_b_fused: forward DIF, the Hermitian-pair divide at the
+    digit-reversed positions, inverse DIT, Y read and written once) against the three-kernel
+    sequence (pass B, k_tl_divide, pass B⁻¹), each pinned to the oracle above: the same operations,
+    so they agree to rounding (odd N1 = 25 exercises the self-mirrored k1 = 0 group alone)."""
+    p = PRECOND[name]
+    r = np.random.default_rng(29).uniform(-1, 1, gshape(p))
+    out = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("PARADIAG_TLFUSE", fuse)
+        s = cuda_lib.Solver(p)
+        d = s.empty()
+        s.apply_precond(to_dev(r, p), d, 0.0)
+        out.append(to_host(d, p))
+        s.close()
+    assert rel_err(out[0], out[1]) <= 1e-12
