@@ -227,10 +227,20 @@ PD_DEV unsigned mx_inv_n2(int N2) { return (unsigned)((0x100000000ull + (unsigne
 
 // Pass kernels: NP pencil pairs per CTA (8: 128-byte row segments, one CTA per SM; 4: 64-byte
 // segments, two CTAs per SM so that one CTA's loads and stores overlap the other's transform).
+// Dynamic shared memory: the staged tile [L][NP + 1] complex (sized for L = 1024), then the
+// per-CTA tables of the pass: the digit-reversal map of its length (int [1024]) and, for pass A,
+// the four-step twiddles of its n2 (complex [1024]).  ncu c6n: the per-element global lookups of
+// those tables inside the load / store loops (each behind the previous cp.async or store) were
+// the largest long-scoreboard stall; the tables are now built once per CTA, while the tile loads
+// are in flight where possible.
+template <int NP>
+__host__ __device__ constexpr size_t mx_tile_bytes() { return (size_t)1024 * (NP + 1) * sizeof(double2); }
+template <int NP>
+__host__ __device__ constexpr size_t mx_pass_smem() { return mx_tile_bytes<NP>() + 1024 * sizeof(int) + 1024 * sizeof(double2); }
 
-// Pass A forward: rows n = N2·n1 + n2, 16 real columns (8 pairs) of chunk; z = γ_n (r[2p] + i r[2p+1]);
+// Pass A forward: rows n = N2·n1 + n2, 2·NP real columns (NP pairs) of chunk; z = γ_n (r[2p] + i r[2p+1]);
 // length-N1 DFT over n1 (DIF); × W_N^{n2 k1}; store Y[k1][n2][p] (k1 un-reversed).
-// 16 warps: two per pencil pair (stages split between them, group barriers); pencil pairs past P
+// Two warps per pencil pair (stages split between them, group barriers); pencil pairs past P
 // (the padded last chunk) skip the transform.  Rows are staged with 16-byte copies when the row
 // pitch is even.
 template <int NP>
@@ -240,6 +250,8 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(
   const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   double* sd = reinterpret_cast<double*>(sm);
+  int* k1s = reinterpret_cast<int*>(reinterpret_cast<char*>(sm) + mx_tile_bytes<NP>());
+  double2* tws = reinterpret_cast<double2*>(k1s + 1024);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
   const int64_t chunk = blockIdx.x % nch;
@@ -247,7 +259,7 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(
   const int64_t c0 = chunk * (2 * NP);
   const int L = Q.N1;
   const bool v16 = (Q.ld & 1) == 0;
-  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {      // column pairs of 16-double rows
+  for (int idx = threadIdx.x; idx < L * NP; idx += NT) {      // column pairs of the staged rows
     const int c = 2 * (idx % NP), n1 = idx / NP;
     const int64_t n = (int64_t)Q.N2 * n1 + n2;
     double* d = sd + n1 * 2 * kMxRowC + c;
@@ -264,6 +276,15 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(
     }
   }
   cp_async_commit();
+  {                                                     // tables while the tile loads are in flight
+    const unsigned inv_n2 = mx_inv_n2(Q.N2);
+#pragma unroll 4
+    for (int pos = threadIdx.x; pos < L; pos += NT) {
+      const int k1 = __ldg(Q.rev1 + pos);
+      k1s[pos] = k1;
+      tws[pos] = mix_tw4<-1>(Q, n2, k1, inv_n2);
+    }
+  }
   cp_async_wait_all();
   const double g2 = __ldg(Q.glo + n2);
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {    // γ_n = ghi[n1]·glo[n2], own elements
@@ -276,12 +297,10 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(
   __syncthreads();
   if (chunk * NP + pen < Q.P) mix_fft_fwd(sm + pen, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, t0, pen);
   __syncthreads();
-  const unsigned inv_n2 = mx_inv_n2(Q.N2);
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
     const int w = idx % NP, pos = idx / NP;
     const int64_t p = chunk * NP + w;
-    const int k1 = __ldg(Q.rev1 + pos);
-    if (p < Q.P) Y[((int64_t)k1 * Q.N2 + n2) * Q.P + p] = cmul(sm[pos * kMxRowC + w], mix_tw4<-1>(Q, n2, k1, inv_n2));
+    if (p < Q.P) Y[((int64_t)k1s[pos] * Q.N2 + n2) * Q.P + p] = cmul(sm[pos * kMxRowC + w], tws[pos]);
   }
 }
 
@@ -289,9 +308,10 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_fwd(
 template <int NP>
 __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_fwd(const double2* __restrict__ Y, double2* __restrict__ X,
                                                               TlongParams Q) {
-  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;
   const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
+  int* k2s = reinterpret_cast<int*>(reinterpret_cast<char*>(sm) + mx_tile_bytes<NP>());
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
   const int64_t chunk = blockIdx.x % nch;
@@ -304,6 +324,8 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_fwd(
     else sm[n2 * kMxRowC + w] = make_double2(0.0, 0.0);
   }
   cp_async_commit();
+#pragma unroll 4
+  for (int pos = threadIdx.x; pos < L; pos += NT) k2s[pos] = __ldg(Q.rev2 + pos);
   cp_async_wait_all();
   __syncthreads();
   if (chunk * NP + pen < Q.P) mix_fft_fwd(sm + pen, kMxRowC, L, Q.plan2, Q.nst2, Q.mt2, t0, pen);
@@ -311,8 +333,7 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_fwd(
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
     const int w = idx % NP, pos = idx / NP;
     const int64_t p = chunk * NP + w;
-    const int k2 = __ldg(Q.rev2 + pos);
-    if (p < Q.P) X[((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p] = sm[pos * kMxRowC + w];
+    if (p < Q.P) X[((int64_t)k1 + (int64_t)Q.N1 * k2s[pos]) * Q.P + p] = sm[pos * kMxRowC + w];
   }
 }
 
@@ -321,18 +342,22 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_fwd(
 template <int NP>
 __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_inv(const double2* __restrict__ X, double2* __restrict__ Y,
                                                               TlongParams Q) {
-  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;
   const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
+  int* ps = reinterpret_cast<int*>(reinterpret_cast<char*>(sm) + mx_tile_bytes<NP>());
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
   const int64_t chunk = blockIdx.x % nch;
   const int k1 = (int)(blockIdx.x / nch);
   const int L = Q.N2;
+#pragma unroll 4
+  for (int k2 = threadIdx.x; k2 < L; k2 += NT) ps[k2] = __ldg(Q.irev2 + k2);
+  __syncthreads();
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
     const int w = idx % NP, k2 = idx / NP;
     const int64_t p = chunk * NP + w;
-    double2* d = sm + __ldg(Q.irev2 + k2) * kMxRowC + w;
+    double2* d = sm + ps[k2] * kMxRowC + w;
     if (p < Q.P) cp_async16(d, X + ((int64_t)k1 + (int64_t)Q.N1 * k2) * Q.P + p);
     else *d = make_double2(0.0, 0.0);
   }
@@ -353,30 +378,40 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_b_inv(
 template <int NP>
 __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_inv(const double2* __restrict__ Y, double* __restrict__ out,
                                                               TlongParams Q) {
-  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;   // staged row pitch (complex), threads
+  constexpr int kMxRowC = NP + 1, NT = NP * kMxWpp * 32;
   const int64_t nch = (Q.P + NP - 1) / NP;
   extern __shared__ double2 sm[];
   double* sd = reinterpret_cast<double*>(sm);
+  int* ps = reinterpret_cast<int*>(reinterpret_cast<char*>(sm) + mx_tile_bytes<NP>());
+  double2* tws = reinterpret_cast<double2*>(ps + 1024);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pen = warp / kMxWpp, t0 = (warp % kMxWpp) * 32 + lane;
   const int64_t chunk = blockIdx.x % nch;
   const int n2 = (int)(blockIdx.x / nch);
   const int64_t c0 = chunk * (2 * NP);
   const int L = Q.N1;
+  {
+    const unsigned inv_n2 = mx_inv_n2(Q.N2);
+#pragma unroll 4
+    for (int k1 = threadIdx.x; k1 < L; k1 += NT) {
+      ps[k1] = __ldg(Q.irev1 + k1);
+      tws[k1] = mix_tw4<+1>(Q, n2, k1, inv_n2);
+    }
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {
     const int w = idx % NP, k1 = idx / NP;
     const int64_t p = chunk * NP + w;
-    double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
+    double2* d = sm + ps[k1] * kMxRowC + w;
     if (p < Q.P) cp_async16(d, Y + ((int64_t)k1 * Q.N2 + n2) * Q.P + p);
     else *d = make_double2(0.0, 0.0);
   }
   cp_async_commit();
   cp_async_wait_all();
-  const unsigned inv_n2 = mx_inv_n2(Q.N2);
   for (int idx = threadIdx.x; idx < L * NP; idx += NT) {   // × W_N^{-n2 k1}, own elements
     const int w = idx % NP, k1 = idx / NP;
-    double2* d = sm + __ldg(Q.irev1 + k1) * kMxRowC + w;
-    *d = cmul(*d, mix_tw4<+1>(Q, n2, k1, inv_n2));
+    double2* d = sm + ps[k1] * kMxRowC + w;
+    *d = cmul(*d, tws[k1]);
   }
   __syncthreads();
   if (chunk * NP + pen < Q.P) mix_fft_inv(sm + pen, kMxRowC, L, Q.plan1, Q.nst1, Q.mt1, t0, pen);
@@ -408,7 +443,9 @@ __global__ void __launch_bounds__(NP * kMxWpp * 32, NP <= 4 ? 2 : 1) k_mx_a_inv(
 // instead of three round trips through X.
 // MP pencil pairs per group (4: 160 KB, one CTA per SM; 2: 80 KB, two per SM)
 template <int MP>
-constexpr size_t mx_fused_smem() { return (size_t)2 * 1024 * (MP + 1) * sizeof(double2); }
+__host__ __device__ constexpr size_t mx_fused_tile() { return (size_t)2 * 1024 * (MP + 1) * sizeof(double2); }
+template <int MP>
+__host__ __device__ constexpr size_t mx_fused_smem() { return mx_fused_tile<MP>() + 2 * 1024 * sizeof(int); }   // + rev2, irev2
 
 template <bool PLAIN, int MP>      // PLAIN: θ = 1 and no λ₃ term, divisor d_k + μ
 __global__ void __launch_bounds__(2 * MP * kMxWpp * 32, MP <= 2 ? 2 : 1) k_mx_b_fused(double2* __restrict__ Y, TlongParams Q) {
@@ -433,6 +470,13 @@ __global__ void __launch_bounds__(2 * MP * kMxWpp * 32, MP <= 2 ? 2 : 1) k_mx_b_
     else *d = make_double2(0.0, 0.0);
   }
   cp_async_commit();
+  int* rs = reinterpret_cast<int*>(reinterpret_cast<char*>(sm) + mx_fused_tile<MP>());
+  int* irs = rs + 1024;
+#pragma unroll 4
+  for (int q = threadIdx.x; q < L; q += NT) {
+    rs[q] = __ldg(Q.rev2 + q);
+    irs[q] = __ldg(Q.irev2 + q);
+  }
   cp_async_wait_all();
   __syncthreads();
   const bool real_pen = chunk * kMfPairs + pen < Q.P && (grp == 0 || two);
@@ -461,13 +505,13 @@ __global__ void __launch_bounds__(2 * MP * kMxWpp * 32, MP <= 2 ? 2 : 1) k_mx_b_
     const int64_t p = chunk * kMfPairs + w;
     if (p >= Q.P) continue;
     const int k1 = g ? k1b : j;
-    const int k2 = __ldg(Q.rev2 + pos);
+    const int k2 = rs[pos];
     int mg, k2m;
     if (k1 == 0) { mg = g; k2m = k2 == 0 ? 0 : L - k2; }
     else if (2 * k1 == Q.N1) { mg = g; k2m = L - 1 - k2; }
     else { mg = 1 - g; k2m = L - 1 - k2; }
     const double2 Zl = sm[(g * L + pos) * kMfRowC + w];
-    const double2 Zm = sm[(mg * L + __ldg(Q.irev2 + k2m)) * kMfRowC + w];
+    const double2 Zm = sm[(mg * L + irs[k2m]) * kMfRowC + w];
     const double2 A = make_double2(0.5 * (Zl.x + Zm.x), 0.5 * (Zl.y - Zm.y));
     const double2 B = make_double2(0.5 * (Zl.y + Zm.y), -0.5 * (Zl.x - Zm.x));
     const int k = k1 + Q.N1 * k2;

@@ -85,10 +85,10 @@ cudaError_t tlong_attrs() {
     return e;
 #define PD_MXA(K, B)                                                                              \
   if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(B)))) return e;
-  PD_MXA(k_mx_a_fwd<8>, 1024 * 9 * 16) PD_MXA(k_mx_a_inv<8>, 1024 * 9 * 16)
-  PD_MXA(k_mx_b_fwd<8>, 1024 * 9 * 16) PD_MXA(k_mx_b_inv<8>, 1024 * 9 * 16)
-  PD_MXA(k_mx_a_fwd<4>, 1024 * 5 * 16) PD_MXA(k_mx_a_inv<4>, 1024 * 5 * 16)
-  PD_MXA(k_mx_b_fwd<4>, 1024 * 5 * 16) PD_MXA(k_mx_b_inv<4>, 1024 * 5 * 16)
+  PD_MXA(k_mx_a_fwd<8>, mx_pass_smem<8>()) PD_MXA(k_mx_a_inv<8>, mx_pass_smem<8>())
+  PD_MXA(k_mx_b_fwd<8>, mx_pass_smem<8>()) PD_MXA(k_mx_b_inv<8>, mx_pass_smem<8>())
+  PD_MXA(k_mx_a_fwd<4>, mx_pass_smem<4>()) PD_MXA(k_mx_a_inv<4>, mx_pass_smem<4>())
+  PD_MXA(k_mx_b_fwd<4>, mx_pass_smem<4>()) PD_MXA(k_mx_b_inv<4>, mx_pass_smem<4>())
   PD_MXA((k_mx_b_fused<true, 4>), mx_fused_smem<4>()) PD_MXA((k_mx_b_fused<false, 4>), mx_fused_smem<4>())
   PD_MXA((k_mx_b_fused<true, 2>), mx_fused_smem<2>()) PD_MXA((k_mx_b_fused<false, 2>), mx_fused_smem<2>())
 #undef PD_MXA
@@ -122,7 +122,7 @@ bool tlong_launch(int stage, const void* in, void* out, const TlongParams& Q, cu
   if (Q.mixed && stage != 2) {                          // mixed radix (k_tmix.cuh): one transform per CTA
     const int np = Q.mxp;                               // pencil pairs per CTA: 8 or 4
     const unsigned grid = (unsigned)(((Q.P + np - 1) / np) * ((stage == 0 || stage == 4) ? Q.N2 : Q.N1));
-    const size_t sm = (size_t)1024 * (np + 1) * sizeof(double2);
+    const size_t sm = np == 4 ? mx_pass_smem<4>() : mx_pass_smem<8>();
     const unsigned nt = (unsigned)(np * kMxWpp * 32);
 #define PD_MX(NP)                                                                                          \
     switch (stage) {                                                                                       \
