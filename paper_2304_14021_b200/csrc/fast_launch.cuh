@@ -38,6 +38,11 @@ void fast_cols_cm(int neumann, int dir, const double* in, double* out, const Lin
                   int64_t lp);
 template <int E>
 void fast_time(const double* in, double* out, const TimeParams& T, const FastLaunch& F);
+// y⁻¹ pass with TMA box stores into the padded workspace that tmo describes (k_cols_tma_inv;
+// M = 2048 only).  Returns false when this E has none.
+template <int E>
+bool fast_cols_tma_inv(int neumann, const double* in, const LineParams& L, const FastLaunch& F, int64_t lp,
+                       const CUtensorMap* tmo);
 // TMA-staged three-stage time pass (k_time2d_v4), in place on the buffer tmap describes: [N_t][ps]
 // with ps = N_s rounded up to even, box {16, min(N_t, 256)}.  Returns false when this E has none.
 template <int E>
@@ -101,6 +106,10 @@ cudaError_t fast_attrs() {
     PD_ATTR((k_rows4<0, kPairsPerRowCta>), dttp_rows_smem());
     PD_ATTR((k_cols4<1>), dttp_cols_smem());
     PD_ATTR((k_cols4<0>), dttp_cols_smem());
+  }
+  if constexpr (E == 32) {
+    PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
+    PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
   }
   PD_ATTR((k_cols3<1, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
   PD_ATTR((k_cols3<0, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
@@ -216,9 +225,27 @@ void fast_cols_cm(int neumann, int dir, const double* in, double* out, const Lin
   }
 }
 
+template <int E>
+bool fast_cols_tma_inv(int neumann, const double* in, const LineParams& L, const FastLaunch& F, int64_t lp,
+                       const CUtensorMap* tmo) {
+  if constexpr (E != 32) {
+    return false;
+  } else {
+    constexpr int NW = fast_col_warps(32);
+    constexpr int C = NW * (32 / E);
+    const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
+    const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
+    const size_t sm = dtt3_cols_smem<32>() + 1024 + kYsRing;
+    if (neumann) k_cols_tma_inv<1, NW><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
+    else k_cols_tma_inv<0, NW><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
+    return true;
+  }
+}
+
 #define PD_FAST_INSTANTIATE(E)                                                                       \
   template void fast_cols_cm<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&, int64_t); \
   template bool fast_time_tma<E>(double*, const TimeParams&, const FastLaunch&, const CUtensorMap*); \
+  template bool fast_cols_tma_inv<E>(int, const double*, const LineParams&, const FastLaunch&, int64_t, const CUtensorMap*); \
   template cudaError_t fast_attrs<E>();                                                             \
   template void fast_line<E>(int, int, const double*, double*, const LineParams&, const FastLaunch&); \
   template void fast_time<E>(const double*, double*, const TimeParams&, const FastLaunch&);

@@ -227,7 +227,8 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
   unsigned long long ubits = 0ull;
   const int64_t ngroups = (L.nlines + D::P - 1) / D::P;
   const int64_t gstride = (int64_t)gridDim.x * NW;
-  const double* in_end = in + L.nlines * L.nx;
+  const int64_t ldi = GEN ? L.nx : L.ldi, ldo = GEN ? L.nx : L.ldo;   // row pitches (block maps: nx)
+  const double* in_end = in + L.nlines * ldi;
   if (!NEUMANN) {
     for (int p = lane; p < D::P; p += 32) {
       xb[p * D::LDX] = 0.0;
@@ -238,9 +239,9 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     const int64_t L0 = g * D::P;
     const int64_t rem = L.nlines - L0;
     const int nl = rem < D::P ? (int)rem : D::P;
-    const double* src = in + L0 * L.nx;
+    const double* src = in + L0 * ldi;
     if ((L.tune & 1) && lane == 0 && g + gstride < ngroups)
-      bulk_prefetch_l2(in + (g + gstride) * D::P * L.nx, (size_t)D::P * L.nx * sizeof(double), in_end);
+      bulk_prefetch_l2(in + (g + gstride) * D::P * ldi, (size_t)D::P * L.nx * sizeof(double), in_end);
     // fused update: bring this group's U rows towards L2 now, they are read after the transform
     if (UPD && L.upd && lane == 0)
       bulk_prefetch_l2(L.upd + L0 * L.nx, (size_t)nl * L.nx * sizeof(double), L.upd + L.nlines * L.nx);
@@ -255,7 +256,8 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
             for (int e = e0 + lane; e < e1; e += 32) cp_async8(x + e, s + e);
           }
         } else if (!(L.tune & 16384)) {           // (A/B) tune 16384: no loads
-          const double* s = src + p * L.nx;
+          const double* s = src + p * ldi;
+          // (16-byte pair copies from the 16-byte aligned wp rows measured slower: x⁻¹ 9.3 -> 10.3 ms)
           for (int e = lane; e < L.nel; e += 32) cp_async8(x + e, s + e);
         }
       }
@@ -271,15 +273,15 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
       __syncwarp();
     }
     D::transform(xb, L, trig2, lane);
-    double* dst = out + L0 * L.nx;
+    double* dst = out + L0 * ldo;
 #pragma unroll
     for (int p = 0; p < D::P; ++p) {
       if (p < nl) {
         if (UPD && L.upd) update_line<(D::M + 32) / 32>(xb + p * D::LDO, L.upd + (L0 + p) * L.nx, L.nel, lane, lmax, ubits);
         else if (GEN && L.sout.n && L.amax) store_line_seg<true>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
         else if (GEN && L.sout.n) store_line_seg<false>(xb + p * D::LDO, out, L.sout, L0 + p, lane, lmax);
-        else if (V == 1 || (GEN && L.amax)) store_line<true>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
-        else if (!(L.tune & 32768)) store_line<false>(xb + p * D::LDO, dst + p * L.nx, L.nel, lane, lmax);
+        else if (V == 1 || (GEN && L.amax)) store_line<true>(xb + p * D::LDO, dst + p * ldo, L.nel, lane, lmax);
+        else if (!(L.tune & 32768)) store_line<false>(xb + p * D::LDO, dst + p * ldo, L.nel, lane, lmax);
       }
     }
     __syncwarp();
@@ -599,9 +601,9 @@ k_cols_cm(const double* in, double* out, LineParams L, const double2* __restrict
     if (DIR == 0) {                                               // natural columns -> line buffers
       if (c_t < wcols) {
         double* lb = base + (size_t)w_t * D::BUF + p_t * D::LDX + (NEUMANN ? 0 : 1) + e_t;
-        const double* s = in + n * L.ps_in + x0 + (int64_t)e_t * L.nx + c_t;
-        const int64_t rstride = (int64_t)RSTEP * L.nx;
-        for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.nx) {
+        const double* s = in + n * L.ps_in + x0 + (int64_t)e_t * L.ldn + c_t;
+        const int64_t rstride = (int64_t)RSTEP * L.ldn;
+        for (int e0 = e_t; e0 < kNel; e0 += 64, lb += 64, s += 64 * L.ldn) {
 #pragma unroll
           for (int j = 0; j < PER; ++j)
             if (e0 + j * RSTEP < kNel) cp_async8(lb + j * RSTEP, s + j * rstride);
@@ -688,11 +690,11 @@ k_cols_cm(const double* in, double* out, LineParams L, const double2* __restrict
           ov[k * PER + j] = (c_t < wcols && e_t + 64 * k + j * RSTEP < kNel) ? ob[65 * k + j * RSTEP] : 0.0;
       __syncthreads();
       if (G + gridDim.x < ngroups) issue(G + gridDim.x);
-      if (c_t < wcols) {
+      if (c_t < wcols && !(L.tune & (1 << 19))) {      // (A/B) tune 2^19: no natural-side stores
         // running pointer (rows e_t, e_t + RSTEP, ...): one add per store instead of a 64-bit
         // multiply by the runtime row length (ncu r02t: 12% of the stall samples on those IMADs)
-        double* d = out + n * L.ps_out + x0 + (int64_t)e_t * L.nx + c_t;
-        const int64_t rstride = (int64_t)RSTEP * L.nx;
+        double* d = out + n * L.ps_out + x0 + (int64_t)e_t * L.ldn + c_t;
+        const int64_t rstride = (int64_t)RSTEP * L.ldn;
 #pragma unroll
         for (int k = 0; k < KB; ++k)
 #pragma unroll
@@ -702,6 +704,143 @@ k_cols_cm(const double* in, double* out, LineParams L, const double2* __restrict
     }
   }
   cp_async_wait_all();
+}
+
+// ---------------------------------------------------------------- y⁻¹ with TMA stores (M = 2048)
+// The inverse y pass of k_cols_cm (column-major wt lines in, one bulk copy per Neumann line) with
+// the natural-side output leaving through TMA instead of one 8-byte store per element and thread:
+// measured on c5 (tune 2^19, r02y), the scattered natural-side stores cost 4.4 of the pass's
+// 13.5 ms.  The output goes to the library's padded workspace wp (row pitch L.ldn, a multiple of 8
+// doubles, so every 8-column box row is a 64-byte aligned segment and the tensor map's strides are
+// legal), through a ring of kYsSlots staging chunks of kYsRows rows × 8 columns: each thread
+// writes its outputs of a chunk (a warp covers 4 rows × 64 B: conflict-free), the CTA fences the
+// writes to the async proxy and syncs, one thread issues the chunk's box store; before the barrier
+// of chunk c that thread waits until the store of chunk c + 1 − kYsSlots has read its slot, so one
+// barrier per chunk suffices.  Rows ≥ N_y and columns ≥ N_x of the last boxes are clipped by TMA.
+constexpr int kYsRows = 256;
+constexpr int kYsSlots = 4;
+constexpr size_t kYsRing = (size_t)kYsSlots * kYsRows * 8 * sizeof(double);   // 64 KB
+
+template <int NEUMANN, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2, int64_t lp,
+               const __grid_constant__ CUtensorMap tmo) {
+  constexpr int E = 32;
+  using D = Dtt3<NEUMANN, E>;
+  constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;
+  constexpr int C = NW * D::P;
+  static_assert(C == 8, "8-column tiles: 64-byte box rows");
+  constexpr int NTH = NW * 32;
+  constexpr int RSTEP = NTH / C;
+  constexpr int PER = 64 / RSTEP;
+  constexpr int KB = (kNel + 63) / 64;
+  constexpr int NCH = (kNel + kYsRows - 1) / kYsRows;
+  static_assert(kYsRows % 64 == 0, "a chunk holds whole 64-row blocks");
+  constexpr int KPC = kYsRows / 64;                             // 64-row blocks per chunk
+  extern __shared__ double2 smem2[];
+  double* base = reinterpret_cast<double*>(smem2);
+  double* ring = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(base + (size_t)NW * D::BUF) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xb = base + (size_t)warp * D::BUF;
+  const int64_t gx = (L.nx + C - 1) / C;
+  const int64_t nsl = L.nlines / L.nx;
+  const int64_t ngroups = nsl * gx;
+  const int c_t = threadIdx.x % C, e_t = threadIdx.x / C;
+  const int w_t = c_t / D::P, p_t = c_t - w_t * D::P;
+  const int64_t cps = (int64_t)L.nx * lp;
+  constexpr bool BULK = NEUMANN;
+  __shared__ uint64_t bar;
+  unsigned phase = 0;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmo);
+    if (BULK) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int64_t G) {
+    const int64_t n = G / gx;
+    const int x0 = (int)((G - n * gx) * C);
+    if (BULK) {
+      if (threadIdx.x == 0) {
+        const int nl = min(C, (int)(L.nx - x0));
+        fence_proxy_async();
+        mbar_expect_tx(&bar, (unsigned)(nl * lp * 8));
+        for (int c = 0; c < nl; ++c) {
+          const int w = c / D::P, p = c - w * D::P;
+          const double* src = in + n * cps + (int64_t)(x0 + c) * lp;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(base + (size_t)w * D::BUF + p * D::LDX)), "l"(src), "r"((unsigned)(lp * 8)),
+                         "r"(smem_u32(&bar)) : "memory");
+        }
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < D::P; ++p) {
+        const int x = x0 + warp * D::P + p;
+        if (x < L.nx) {
+          double* lb = xb + p * D::LDX + 1;
+          const double* s = in + n * cps + (int64_t)x * lp;
+          for (int e = lane; e < kNel; e += 32) cp_async8(lb + e, s + e);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  int64_t chunk = 0;                                            // box stores issued by this CTA
+  if (blockIdx.x < ngroups) issue(blockIdx.x);
+  for (int64_t G = blockIdx.x; G < ngroups; G += gridDim.x) {
+    const int64_t n = G / gx;
+    const int x0 = (int)((G - n * gx) * C);
+    const int wcols = min(C, (int)(L.nx - x0));
+    if (!NEUMANN) {
+      for (int p = lane; p < D::P; p += 32) {
+        xb[p * D::LDX] = 0.0;
+        xb[p * D::LDX + D::M] = 0.0;
+      }
+    }
+    if (BULK) {
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    D::transform(xb, L, trig2, lane, L.oscale ? __ldg(L.oscale + n) : 1.0);
+    __syncthreads();
+    double ov[KB * PER];
+    const double* ob = base + (size_t)w_t * D::BUF + p_t * D::LDO + e_t;   // opos(e0 + r) = 65·(e0/64) + r
+#pragma unroll
+    for (int k = 0; k < KB; ++k)
+#pragma unroll
+      for (int j = 0; j < PER; ++j)
+        ov[k * PER + j] = (c_t < wcols && e_t + 64 * k + j * RSTEP < kNel) ? ob[65 * k + j * RSTEP] : 0.0;
+    __syncthreads();                                            // line buffers free: next tile's loads
+    if (G + gridDim.x < ngroups) issue(G + gridDim.x);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch, ++chunk) {
+      double* slot = ring + (size_t)(chunk % kYsSlots) * (kYsRows * 8);
+#pragma unroll
+      for (int kk = 0; kk < KPC; ++kk) {
+        const int k = ch * KPC + kk;
+        if (k < KB) {
+#pragma unroll
+          for (int j = 0; j < PER; ++j) slot[(kk * 64 + e_t + j * RSTEP) * 8 + c_t] = ov[k * PER + j];
+        }
+      }
+      fence_proxy_async();
+      if (threadIdx.x == 0) tma_wait_read_le<kYsSlots - 2>();   // slot of chunk + 1 free for the next write
+      __syncthreads();
+      if (threadIdx.x == 0 && !(L.tune & (1 << 19))) {
+        tma_store_3d(&tmo, x0, ch * kYsRows, (int)n, slot);
+        tma_commit();
+      }
+    }
+  }
+  cp_async_wait_all();
+  if (threadIdx.x == 0) tma_wait_all();
 }
 
 }  // namespace pd

@@ -57,6 +57,8 @@ struct LineParams {
   int stagger_ns;        // k_cols3: start delay of the second CTA of each SM (phase offset)
   SegMap sin, sout;      // k_rows3 / k_cols3: transpose-block input / output (n = 0: plain)
   int64_t ps_in, ps_out; // k_cols3: slice pitch of in / out (ns, or the even pitch of the TMA workspace)
+  int64_t ldi, ldo;      // k_rows3 (plain variants): row pitch of in / out (nx, or the padded pitch of wp)
+  int64_t ldn;           // k_cols_cm: row pitch of the natural-layout side (nx, or the padded pitch of wp)
 };
 
 // buffer index of stored element e: Neumann x_e = node e; hinged x_{e+1} = interior node e+1

@@ -105,6 +105,24 @@ bool make_map_2d(CUtensorMap* m, const double* base, int64_t inner, int64_t oute
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// 3D tensor map of an [nt][ny][pitch] fp64 array (inner extent nx <= pitch, pitch even), boxes
+// {box_w, box_h, 1}, no swizzle (the y⁻¹ staging chunks are plain [rows][8] tiles)
+bool make_map_3d(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t nt, int64_t pitch, unsigned box_w,
+                 unsigned box_h) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !enc)
+    return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (pitch & 1) || box_h > 256) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nt};
+  const cuuint64_t strides[2] = {(cuuint64_t)(pitch * 8), (cuuint64_t)(pitch * ny * 8)};
+  const cuuint32_t box[3] = {box_w, box_h, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 int ilog2(int64_t v) {
   int l = 0;
   while ((int64_t(1) << l) < v) ++l;
@@ -129,6 +147,12 @@ struct pd_handle {
   // runs in place on it, the inverse y pass reads it
   double* wt = nullptr;
   int64_t ps = 0, lp = 0;             // wt slice pitch (nx·lp) and column-major line pitch
+  // padded natural-layout workspace wp [nt][ny][lpx] between the x and y passes (M = 2048): row
+  // pitch lpx = N_x rounded up to 8 doubles (64-byte aligned rows), so the inverse y pass stores
+  // its tiles with TMA (k_cols_tma_inv, tensor map wp_map); PARADIAG_WP=0 turns it off (A/B)
+  double* wp = nullptr;
+  int64_t lpx = 0;
+  CUtensorMap wp_map;
   double inv_dt = 0, inv_h2 = 0, b2 = 0, e2 = 0;
   // device buffers
   double* work = nullptr;             // 2D: δ/r workspace [nt][ns]; 1D: r [nt][nx]
@@ -447,6 +471,7 @@ LineParams line_params(pd_handle* h, int axis, unsigned long long* amax, double*
   L.sin.n = 0;
   L.sout.n = 0;
   L.ps_in = L.ps_out = h->ns;
+  L.ldi = L.ldo = L.ldn = h->nx;
   return L;
 }
 
@@ -472,11 +497,14 @@ bool fast_line_any(pd_handle* h, const double* in, double* out, int axis, const 
 }
 
 int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned long long* amax, int kid,
-                 double* upd = nullptr, const double* oscale = nullptr, int64_t ps_in = 0, int64_t ps_out = 0) {
+                 double* upd = nullptr, const double* oscale = nullptr, int64_t ps_in = 0, int64_t ps_out = 0,
+                 int64_t ldi = 0, int64_t ldo = 0) {
   LineParams L = line_params(h, axis, amax, upd);
   L.oscale = oscale;
   if (ps_in) L.ps_in = ps_in;
   if (ps_out) L.ps_out = ps_out;
+  if (ldi) L.ldi = ldi;                 // row passes: padded row pitch of in / out (wp)
+  if (ldo) L.ldo = ldo;
   prof_begin(h, kid);
   const bool fast = h->fast && fast_line_any(h, in, out, axis, L);
   if (!fast) {
@@ -505,9 +533,14 @@ int launch_lines(pd_handle* h, const double* in, double* out, int axis, unsigned
 }
 
 // y pass between the natural layout and the column-major wt (k_cols_cm): dir 0 forward, 1 inverse
-int launch_cols_cm(pd_handle* h, int dir, const double* in, double* out, int kid, const double* oscale) {
+int launch_cols_cm(pd_handle* h, int dir, const double* in, double* out, int kid, const double* oscale,
+                   int64_t ldn = 0) {
   LineParams L = line_params(h, 1, nullptr);
   L.oscale = oscale;
+  if (ldn) {                            // natural side in the padded workspace wp
+    L.ldn = ldn;
+    (dir == 0 ? L.ps_in : L.ps_out) = (int64_t)h->ny * ldn;
+  }
   const FastLaunch F = fast_launch(h);
   const int nm = h->neumann ? 1 : 0;
   prof_begin(h, kid);
@@ -521,6 +554,21 @@ int launch_cols_cm(pd_handle* h, int dir, const double* in, double* out, int kid
     default: return fail(PD_EINVAL, "column-major y pass: unsupported line length");
   }
   prof_end(h, kid);
+  PD_LAUNCHED();
+  return PD_OK;
+}
+
+// y⁻¹ from the column-major wt into the padded workspace wp through TMA box stores (M = 2048)
+int launch_cols_tma_inv(pd_handle* h, const double* in, int kid, const double* oscale) {
+  LineParams L = line_params(h, 1, nullptr);
+  L.oscale = oscale;
+  L.ldn = h->lpx;
+  L.ps_out = (int64_t)h->ny * h->lpx;
+  const FastLaunch F = fast_launch(h);
+  prof_begin(h, kid);
+  const bool ok = fast_cols_tma_inv<32>(h->neumann ? 1 : 0, in, L, F, h->lp, &h->wp_map);
+  prof_end(h, kid);
+  if (!ok) return fail(PD_EINVAL, "TMA y-inverse pass: M = 2048 only");
   PD_LAUNCHED();
   return PD_OK;
 }
@@ -622,9 +670,13 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     const bool fold = !h->tlong && h->fast && h->dtt_ver >= 3 && h->P.m >= 64 && h->P.m <= 2048 && h->P.nt >= 32 &&
                       h->P.nt <= 1024;
     const bool use_wt = h->wt && h->dtt_ver == 3 && !(h->tune & 65536);   // tune 65536 (A/B): the in-place v2 time pass
-    if ((rc = launch_lines(h, r, delta, 0, nullptr, K_XFWD))) return rc;
+    const bool use_wp = use_wt && h->wp;          // x, y passes exchange data through wp
+    double* xo = use_wp ? h->wp : delta;           // x-pass output / x⁻¹-pass input
+    if ((rc = launch_lines(h, r, xo, 0, nullptr, K_XFWD, nullptr, nullptr, 0, 0, 0, use_wp ? h->lpx : 0))) return rc;
+    // (a TMA-load variant of the forward y pass through a 4-chunk staging ring measured slower,
+    // 12.5 -> 13.9 ms: the ring holds half a tile, so half the loads still wait after the transform)
     if (use_wt) {
-      if ((rc = launch_cols_cm(h, 0, delta, h->wt, K_YFWD, fold ? h->gam : nullptr))) return rc;
+      if ((rc = launch_cols_cm(h, 0, xo, h->wt, K_YFWD, fold ? h->gam : nullptr, use_wp ? h->lpx : 0))) return rc;
     } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) {
       return rc;
     }
@@ -671,13 +723,16 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     prof_end(h, K_TIME);
     PD_LAUNCHED();
     }
-    if (use_wt) {
+    if (use_wp) {
+      if ((rc = launch_cols_tma_inv(h, h->wt, K_YINV, fold ? h->ginv : nullptr))) return rc;
+    } else if (use_wt) {
       if ((rc = launch_cols_cm(h, 1, h->wt, delta, K_YINV, fold ? h->ginv : nullptr))) return rc;
     } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YINV, nullptr, fold ? h->ginv : nullptr))) {
       return rc;
     }
-    if (U_fused) return launch_lines(h, delta, delta, 0, dmax, K_XINVUPD, U_fused);
-    if ((rc = launch_lines(h, delta, delta, 0, want_dmax ? dmax : nullptr, K_XINV))) return rc;
+    const int64_t li = use_wp ? h->lpx : 0;
+    if (U_fused) return launch_lines(h, xo, delta, 0, dmax, K_XINVUPD, U_fused, nullptr, 0, 0, li, 0);
+    if ((rc = launch_lines(h, xo, delta, 0, want_dmax ? dmax : nullptr, K_XINV, nullptr, nullptr, 0, 0, li, 0))) return rc;
     return PD_OK;
   }
   if (h->tlong) {     // 1D long window: DST-I/DCT-I along x, four-step time pass with divide, inverse
@@ -1165,7 +1220,11 @@ int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes) {
   b += (size_t)p->nt * (2 * sizeof(double) + sizeof(double2)) + (size_t)(p->m + 2) * (sizeof(double) + sizeof(double2));
   b += (size_t)(1 << std::max(ilog2(p->nt), ilog2(p->m))) * sizeof(double2);
   // TMA time pass workspace (2D, 32 <= nt <= 512, 64 <= m <= 2048): one more iterate-sized array
-  if (p->dim == 2 && !tl && p->nt >= 32 && p->nt <= 512 && p->m >= 64 && p->m <= 2048) b += p->nt * (ns + 1) * sizeof(double);
+  if (p->dim == 2 && !tl && p->nt >= 32 && p->nt <= 512 && p->m >= 64 && p->m <= 2048) {
+    b += p->nt * (ns + 1) * sizeof(double);
+    // M = 2048: the padded x/y exchange workspace wp (rows rounded up to 8 doubles)
+    if (p->m == 2048) b += (size_t)p->nt * ny * ((nx + 7) & ~7) * sizeof(double);
+  }
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
   if (p->jacobian == PD_JACOBIAN_TIME_AVG) b += (size_t)(kKryM + 2) * total * sizeof(double) + 2 * ns * sizeof(double);
   *bytes = b;
@@ -1552,6 +1611,13 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       // the pad column shares a complex pencil with point ns-1 in the time pass: keep it finite
       if (cudaMemsetAsync(h->wt, 0, (size_t)nt * h->ps * sizeof(double), h->stream) != cudaSuccess)
         return cleanup(fail(PD_ECUDA, "wt memset"));
+      const char* fw = std::getenv("PARADIAG_WP");
+      if (p->m == 2048 && h->dtt_ver == 3 && !(fw && std::atoi(fw) == 0)) {
+        h->lpx = (h->nx + 7) & ~(int64_t)7;
+        PD_TRY(dalloc(h, &h->wp, (size_t)nt * h->ny * h->lpx));
+        if (!make_map_3d(&h->wp_map, h->wp, h->nx, h->ny, nt, h->lpx, 8, kYsRows))
+          return cleanup(fail(PD_ECUDA, "wp tensor map encode failed"));
+      }
     }
   }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return cleanup(fail(PD_ECUDA, "init synchronize"));

@@ -48,6 +48,14 @@ PD_DEV void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(src))
                : "memory");
 }
+PD_DEV void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+// at most N of this thread's bulk groups still reading their shared-memory source
+template <int N>
+PD_DEV void tma_wait_read_le() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 PD_DEV void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 PD_DEV void tma_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 PD_DEV void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
