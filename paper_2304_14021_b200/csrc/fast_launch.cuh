@@ -110,6 +110,10 @@ cudaError_t fast_attrs() {
   if constexpr (E == 32) {
     PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
     PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
+    PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32), 2>), dtt3_cols_smem<32>() + 1024 + kYsRing / 2);
+    PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32), 2>), dtt3_cols_smem<32>() + 1024 + kYsRing / 2);
+    PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32), 3>), dtt3_cols_smem<32>() + 1024 + kYsRing * 3 / 4);
+    PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32), 3>), dtt3_cols_smem<32>() + 1024 + kYsRing * 3 / 4);
   }
   PD_ATTR((k_cols3<1, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
   PD_ATTR((k_cols3<0, E, 4>), ((size_t)4 * Dtt3<1, E>::BUF * sizeof(double)));
@@ -235,9 +239,15 @@ bool fast_cols_tma_inv(int neumann, const double* in, const LineParams& L, const
     constexpr int C = NW * (32 / E);
     const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
     const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
-    const size_t sm = dtt3_cols_smem<32>() + 1024 + kYsRing;
-    if (neumann) k_cols_tma_inv<1, NW><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
-    else k_cols_tma_inv<0, NW><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
+    // ring slots: 4 (default), 2 or 3 (A/B: tune 2^21 / 2^22; a smaller ring leaves more L1 to the
+    // transform's tables)
+    const int ns = (L.tune & (1 << 21)) ? 2 : (L.tune & (1 << 22)) ? 3 : kYsSlots;
+    const size_t sm = dtt3_cols_smem<32>() + 1024 + kYsRing / kYsSlots * ns;
+#define PD_TI(NS)                                                                                \
+    if (neumann) k_cols_tma_inv<1, NW, NS><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo); \
+    else k_cols_tma_inv<0, NW, NS><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
+    if (ns == 2) { PD_TI(2) } else if (ns == 3) { PD_TI(3) } else { PD_TI(kYsSlots) }
+#undef PD_TI
     return true;
   }
 }

@@ -721,7 +721,7 @@ constexpr int kYsRows = 256;
 constexpr int kYsSlots = 4;
 constexpr size_t kYsRing = (size_t)kYsSlots * kYsRows * 8 * sizeof(double);   // 64 KB
 
-template <int NEUMANN, int NW>
+template <int NEUMANN, int NW, int NS = kYsSlots>
 __global__ void __launch_bounds__(NW * 32, 1)
 k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2, int64_t lp,
                const __grid_constant__ CUtensorMap tmo) {
@@ -821,7 +821,7 @@ k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2
     if (G + gridDim.x < ngroups) issue(G + gridDim.x);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch, ++chunk) {
-      double* slot = ring + (size_t)(chunk % kYsSlots) * (kYsRows * 8);
+      double* slot = ring + (size_t)(chunk % NS) * (kYsRows * 8);
 #pragma unroll
       for (int kk = 0; kk < KPC; ++kk) {
         const int k = ch * KPC + kk;
@@ -831,7 +831,7 @@ k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2
         }
       }
       fence_proxy_async();
-      if (threadIdx.x == 0) tma_wait_read_le<kYsSlots - 2>();   // slot of chunk + 1 free for the next write
+      if (threadIdx.x == 0) tma_wait_read_le<NS - 2>();         // slot of chunk + 1 free for the next write
       __syncthreads();
       if (threadIdx.x == 0 && !(L.tune & (1 << 19))) {
         tma_store_3d(&tmo, x0, ch * kYsRows, (int)n, slot);

@@ -673,8 +673,9 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     const bool use_wp = use_wt && h->wp;          // x, y passes exchange data through wp
     double* xo = use_wp ? h->wp : delta;           // x-pass output / x⁻¹-pass input
     if ((rc = launch_lines(h, r, xo, 0, nullptr, K_XFWD, nullptr, nullptr, 0, 0, 0, use_wp ? h->lpx : 0))) return rc;
-    // (a TMA-load variant of the forward y pass through a 4-chunk staging ring measured slower,
-    // 12.5 -> 13.9 ms: the ring holds half a tile, so half the loads still wait after the transform)
+    // (measured and not kept: TMA loads of the natural side through a 4-chunk staging ring, whole
+    // tile 13.9 ms or half of it prefetched during the transform 14.4 ms, against 12.3 ms for the
+    // per-element cp.async — the 64 KB ring takes the L1 the transform's tables live in)
     if (use_wt) {
       if ((rc = launch_cols_cm(h, 0, xo, h->wt, K_YFWD, fold ? h->gam : nullptr, use_wp ? h->lpx : 0))) return rc;
     } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) {
