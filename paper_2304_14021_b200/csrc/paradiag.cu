@@ -674,8 +674,10 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     double* xo = use_wp ? h->wp : delta;           // x-pass output / x⁻¹-pass input
     if ((rc = launch_lines(h, r, xo, 0, nullptr, K_XFWD, nullptr, nullptr, 0, 0, 0, use_wp ? h->lpx : 0))) return rc;
     // (measured and not kept: TMA loads of the natural side through a 4-chunk staging ring, whole
-    // tile 13.9 ms or half of it prefetched during the transform 14.4 ms, against 12.3 ms for the
-    // per-element cp.async — the 64 KB ring takes the L1 the transform's tables live in)
+    // tile 13.9 ms or half of it prefetched during the transform 14.4 ms, and TMA box stores of the
+    // wt lines through the same ring 16.1 ms, against 12.3 ms for per-element cp.async + coalesced
+    // register stores — the 64 KB ring takes the L1 that the transform's tables and the 8-byte
+    // cp.async.ca column tile share; the inverse pass loads its wt lines by bulk copy, bypassing L1)
     if (use_wt) {
       if ((rc = launch_cols_cm(h, 0, xo, h->wt, K_YFWD, fold ? h->gam : nullptr, use_wp ? h->lpx : 0))) return rc;
     } else if ((rc = launch_lines(h, delta, delta, 1, nullptr, K_YFWD, nullptr, fold ? h->gam : nullptr))) {
