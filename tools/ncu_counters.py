@@ -12,6 +12,7 @@ import sys
 
 # ncu kernel name (prefix) -> library kernel name; k_rows3 runs twice per iteration (forward, inverse)
 MAP = [("k_residual_tile", "residual"), ("k_cols_cm<1, 32, 8, 0>", "dtt_y_fwd"), ("k_cols_cm<1, 32, 8, 1>", "dtt_y_inv"),
+       ("k_cols_tma_inv", "dtt_y_inv"),
        ("k_time2d_v4", "time_solve_2d"), ("k_update", "update"), ("k_rows3", ("dtt_x_fwd", "dtt_x_inv")),
        ("k_cols3", ("dtt_y_fwd", "dtt_y_inv")), ("k_time2d_v2", "time_solve_2d")]
 KEYS = {"dram__bytes_read.sum": "read", "dram__bytes_write.sum": "write", "gpu__time_duration.sum": "duration",
