@@ -51,3 +51,24 @@ def test_timeavg_solve_parity(cuda_lib, name):
     assert list(info.iters[:p.n_windows]) == iters_o
     assert rel_err(to_host(U, p), U_o) <= 1e-8
     assert info.converged == int(all(conv_o))
+
+
+@pytest.mark.parametrize("name", ["c4t_m32_nt16", "c4t_m64_nt32"])
+def test_timeavg_device_arnoldi_matches_host_loop(cuda_lib, monkeypatch, name):
+    """The inner GMRES's Arnoldi steps run as a conditional WHILE graph with the Hessenberg column,
+    the Givens rotations and the stop test on the device (k_krylov.cuh, KryDev); the host loop
+    (PARADIAG_KRYGRAPH=0) does the same arithmetic with the rotations on the CPU.  Both must give
+    the same P̃⁻¹ r to rounding (the rotations' hypot / division may round differently)."""
+    p = CASES[name]
+    rng = np.random.default_rng(37)
+    r = rng.uniform(-1, 1, gshape(p))
+    jt = 3.0 * rng.uniform(-1, 1, (p.ny, p.nx)) ** 2
+    out = []
+    for g in ("1", "0"):
+        monkeypatch.setenv("PARADIAG_KRYGRAPH", g)
+        s = cuda_lib.Solver(p)
+        d = s.empty()
+        assert s.apply_precond_jt(to_dev(r, p), d, to_dev(jt)) == 0
+        out.append(to_host(d, p))
+        s.close()
+    assert rel_err(out[0], out[1]) <= 1e-13
