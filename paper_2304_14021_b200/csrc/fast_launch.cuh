@@ -107,9 +107,11 @@ cudaError_t fast_attrs() {
     PD_ATTR((k_cols4<1>), dttp_cols_smem());
     PD_ATTR((k_cols4<0>), dttp_cols_smem());
   }
+  if constexpr (E >= 8) {
+    PD_ATTR((k_cols_tma_inv<1, fast_col_warps(E), kYsSlots, E>), dtt3_cols_smem<E>() + 1024 + kYsRing);
+    PD_ATTR((k_cols_tma_inv<0, fast_col_warps(E), kYsSlots, E>), dtt3_cols_smem<E>() + 1024 + kYsRing);
+  }
   if constexpr (E == 32) {
-    PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
-    PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32)>), dtt3_cols_smem<32>() + 1024 + kYsRing);
     PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32), 2>), dtt3_cols_smem<32>() + 1024 + kYsRing / 2);
     PD_ATTR((k_cols_tma_inv<0, fast_col_warps(32), 2>), dtt3_cols_smem<32>() + 1024 + kYsRing / 2);
     PD_ATTR((k_cols_tma_inv<1, fast_col_warps(32), 3>), dtt3_cols_smem<32>() + 1024 + kYsRing * 3 / 4);
@@ -232,21 +234,25 @@ void fast_cols_cm(int neumann, int dir, const double* in, double* out, const Lin
 template <int E>
 bool fast_cols_tma_inv(int neumann, const double* in, const LineParams& L, const FastLaunch& F, int64_t lp,
                        const CUtensorMap* tmo) {
-  if constexpr (E != 32) {
+  if constexpr (E < 8) {
     return false;
   } else {
-    constexpr int NW = fast_col_warps(32);
+    constexpr int NW = fast_col_warps(E);
     constexpr int C = NW * (32 / E);
     const int64_t groups = (int64_t)F.nt * ((F.nx + C - 1) / C);
     const unsigned grid = (unsigned)std::min<int64_t>(groups, 148);
-    // ring slots: 4 (default), 2 or 3 (A/B: tune 2^21 / 2^22; a smaller ring leaves more L1 to the
-    // transform's tables)
-    const int ns = (L.tune & (1 << 21)) ? 2 : (L.tune & (1 << 22)) ? 3 : kYsSlots;
-    const size_t sm = dtt3_cols_smem<32>() + 1024 + kYsRing / kYsSlots * ns;
+    // ring slots: 4 (default), 2 or 3 (A/B, M = 2048: tune 2^21 / 2^22; a smaller ring leaves more
+    // L1 to the transform's tables — measured slower, 11.4 / 10.9 vs 10.5 ms)
+    const int ns = E != 32 ? kYsSlots : (L.tune & (1 << 21)) ? 2 : (L.tune & (1 << 22)) ? 3 : kYsSlots;
+    const size_t sm = dtt3_cols_smem<E>() + 1024 + kYsRing / kYsSlots * ns;
 #define PD_TI(NS)                                                                                \
-    if (neumann) k_cols_tma_inv<1, NW, NS><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo); \
-    else k_cols_tma_inv<0, NW, NS><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
-    if (ns == 2) { PD_TI(2) } else if (ns == 3) { PD_TI(3) } else { PD_TI(kYsSlots) }
+    if (neumann) k_cols_tma_inv<1, NW, NS, E><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo); \
+    else k_cols_tma_inv<0, NW, NS, E><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
+    if constexpr (E == 32) {
+      if (ns == 2) { PD_TI(2) } else if (ns == 3) { PD_TI(3) } else { PD_TI(kYsSlots) }
+    } else {
+      PD_TI(kYsSlots)
+    }
 #undef PD_TI
     return true;
   }

@@ -721,22 +721,27 @@ constexpr int kYsRows = 256;
 constexpr int kYsSlots = 4;
 constexpr size_t kYsRing = (size_t)kYsSlots * kYsRows * 8 * sizeof(double);   // 64 KB
 
-template <int NEUMANN, int NW, int NS = kYsSlots>
+// E = 32 / 16 / 8 (M = 2048 / 1024 / 512): tiles of C = 8 / 16 / 32 columns, staging chunks of
+// RC = 256 / 128 / 64 rows (16 KB each), boxes {C, RC, 1}.
+template <int E>
+__host__ __device__ constexpr int ys_rows() { return kYsRows * 8 / (8 * 32 / E); }
+
+template <int NEUMANN, int NW, int NS = kYsSlots, int E = 32>
 __global__ void __launch_bounds__(NW * 32, 1)
 k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2, int64_t lp,
                const __grid_constant__ CUtensorMap tmo) {
-  constexpr int E = 32;
   using D = Dtt3<NEUMANN, E>;
   constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;
   constexpr int C = NW * D::P;
-  static_assert(C == 8, "8-column tiles: 64-byte box rows");
+  static_assert(C * 8 <= 256, "box rows of at most 32 doubles");
+  constexpr int RC = ys_rows<E>();                              // rows per staging chunk
   constexpr int NTH = NW * 32;
   constexpr int RSTEP = NTH / C;
   constexpr int PER = 64 / RSTEP;
   constexpr int KB = (kNel + 63) / 64;
-  constexpr int NCH = (kNel + kYsRows - 1) / kYsRows;
-  static_assert(kYsRows % 64 == 0, "a chunk holds whole 64-row blocks");
-  constexpr int KPC = kYsRows / 64;                             // 64-row blocks per chunk
+  constexpr int NCH = (kNel + RC - 1) / RC;
+  static_assert(RC % 64 == 0, "a chunk holds whole 64-row blocks");
+  constexpr int KPC = RC / 64;                                  // 64-row blocks per chunk
   extern __shared__ double2 smem2[];
   double* base = reinterpret_cast<double*>(smem2);
   double* ring = reinterpret_cast<double*>(
@@ -821,20 +826,20 @@ k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2
     if (G + gridDim.x < ngroups) issue(G + gridDim.x);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch, ++chunk) {
-      double* slot = ring + (size_t)(chunk % NS) * (kYsRows * 8);
+      double* slot = ring + (size_t)(chunk % NS) * (RC * C);
 #pragma unroll
       for (int kk = 0; kk < KPC; ++kk) {
         const int k = ch * KPC + kk;
         if (k < KB) {
 #pragma unroll
-          for (int j = 0; j < PER; ++j) slot[(kk * 64 + e_t + j * RSTEP) * 8 + c_t] = ov[k * PER + j];
+          for (int j = 0; j < PER; ++j) slot[(kk * 64 + e_t + j * RSTEP) * C + c_t] = ov[k * PER + j];
         }
       }
       fence_proxy_async();
       if (threadIdx.x == 0) tma_wait_read_le<NS - 2>();         // slot of chunk + 1 free for the next write
       __syncthreads();
       if (threadIdx.x == 0 && !(L.tune & (1 << 19))) {
-        tma_store_3d(&tmo, x0, ch * kYsRows, (int)n, slot);
+        tma_store_3d(&tmo, x0, ch * RC, (int)n, slot);
         tma_commit();
       }
     }

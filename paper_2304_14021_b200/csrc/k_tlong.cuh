@@ -222,12 +222,12 @@ k_tl_divide(double2* __restrict__ X, TlongParams Q) {
 // input layout of the inverse FFT, so the divided spectrum never leaves registers; Y is read and
 // written once (in place) instead of three round trips through X.
 #ifndef PD_FB_PAIRS
-#define PD_FB_PAIRS 4
+#define PD_FB_PAIRS 2
 #endif
 constexpr int kFbPairs = PD_FB_PAIRS;                 // pencil pairs per group (2 groups per CTA)
 constexpr int kFbThreads = 2 * kFbPairs * 32;
 constexpr int kFbRowC = kFbPairs + 1;                 // staged row pitch (complex)
-constexpr size_t kFbSmem = (size_t)2 * 1024 * kFbRowC * sizeof(double2);   // 160 KB ≥ 8 × kWarpScratch
+constexpr size_t kFbSmem = (size_t)2 * 1024 * kFbRowC * sizeof(double2);   // 96 KB (2 pairs: two CTAs per SM)
 
 template <bool PLAIN>      // PLAIN: θ = 1 and no λ₃ term, divisor d_k + μ
 __global__ void __launch_bounds__(kFbThreads, kFbPairs <= 2 ? 2 : 1)

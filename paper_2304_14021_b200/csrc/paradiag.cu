@@ -575,10 +575,17 @@ int launch_cols_tma_inv(pd_handle* h, const double* in, int kid, const double* o
   L.ldn = h->lpx;
   L.ps_out = (int64_t)h->ny * h->lpx;
   const FastLaunch F = fast_launch(h);
+  const int nm = h->neumann ? 1 : 0;
   prof_begin(h, kid);
-  const bool ok = fast_cols_tma_inv<32>(h->neumann ? 1 : 0, in, L, F, h->lp, &h->wp_map);
+  bool ok = false;
+  switch (L.M) {
+    case 512: ok = fast_cols_tma_inv<8>(nm, in, L, F, h->lp, &h->wp_map); break;
+    case 1024: ok = fast_cols_tma_inv<16>(nm, in, L, F, h->lp, &h->wp_map); break;
+    case 2048: ok = fast_cols_tma_inv<32>(nm, in, L, F, h->lp, &h->wp_map); break;
+    default: break;
+  }
   prof_end(h, kid);
-  if (!ok) return fail(PD_EINVAL, "TMA y-inverse pass: M = 2048 only");
+  if (!ok) return fail(PD_EINVAL, "TMA y-inverse pass: M = 512, 1024 or 2048 only");
   PD_LAUNCHED();
   return PD_OK;
 }
@@ -1313,7 +1320,8 @@ int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes) {
   // TMA time pass workspace (2D, 32 <= nt <= 512, 64 <= m <= 2048): one more iterate-sized array
   if (p->dim == 2 && !tl && p->nt >= 32 && p->nt <= 512 && p->m >= 64 && p->m <= 2048) {
     b += p->nt * (ns + 1) * sizeof(double);
-    // M = 2048: the padded x/y exchange workspace wp (rows rounded up to 8 doubles)
+    // M = 2048 (M = 512 / 1024 with PARADIAG_WP=1): the padded x/y exchange workspace wp (rows
+    // rounded up to 8 doubles)
     if (p->m == 2048) b += (size_t)p->nt * ny * ((nx + 7) & ~7) * sizeof(double);
   }
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
@@ -1704,10 +1712,14 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
       if (cudaMemsetAsync(h->wt, 0, (size_t)nt * h->ps * sizeof(double), h->stream) != cudaSuccess)
         return cleanup(fail(PD_ECUDA, "wt memset"));
       const char* fw = std::getenv("PARADIAG_WP");
-      if (p->m == 2048 && h->dtt_ver == 3 && !(fw && std::atoi(fw) == 0)) {
+      // default for M = 2048 (y⁻¹ 13.4 -> 10.4 ms on c5); M = 512 / 1024 only with PARADIAG_WP=1 (c3:
+      // y⁻¹ 0.231 -> 0.244 ms — its 32-column tiles already store 256-byte row segments)
+      const bool wp_on = fw ? std::atoi(fw) != 0 : p->m == 2048;
+      if ((p->m == 512 || p->m == 1024 || p->m == 2048) && h->dtt_ver == 3 && wp_on) {
         h->lpx = (h->nx + 7) & ~(int64_t)7;
         PD_TRY(dalloc(h, &h->wp, (size_t)nt * h->ny * h->lpx));
-        if (!make_map_3d(&h->wp_map, h->wp, h->nx, h->ny, nt, h->lpx, 8, kYsRows))
+        const unsigned cw = 8u * 2048u / (unsigned)p->m;            // tile columns (8 / 16 / 32)
+        if (!make_map_3d(&h->wp_map, h->wp, h->nx, h->ny, nt, h->lpx, cw, kYsRows * 8 / cw))
           return cleanup(fail(PD_ECUDA, "wp tensor map encode failed"));
       }
     }

@@ -262,13 +262,13 @@ def test_divergence_flag_matches_oracle(cuda_lib, fixed):
     assert it.growth == 3
 
 
-@pytest.mark.parametrize("bc_cfg", ["c5", "c3"])
-def test_padded_workspace_path_bit_identical(cuda_lib, monkeypatch, bc_cfg):
-    """M = 2048 with N_t ≥ 32 runs the x / y passes through the padded workspace wp (16-byte row
+@pytest.mark.parametrize("bc_cfg,m", [("c5", 2048), ("c3", 2048), ("c3", 512), ("c5", 1024), ("c5", 512)])
+def test_padded_workspace_path_bit_identical(cuda_lib, monkeypatch, bc_cfg, m):
+    """M = 512 / 1024 / 2048 with N_t ≥ 32 runs the x / y passes through the padded workspace wp (16-byte row
     loads and stores in the x passes, TMA box stores in the inverse y pass, k_cols_tma_inv).  Only
     the data movement differs from the natural-layout path (PARADIAG_WP=0, pinned to the oracle
     above at M = 2048), so P_α⁻¹ must agree bit for bit, out of place and in place."""
-    p = twin(bc_cfg, m=2048, nt=32)
+    p = twin(bc_cfg, m=m, nt=32)
     r = np.random.default_rng(41).uniform(-1, 1, gshape(p))
     out = []
     for wp in ("1", "0"):
