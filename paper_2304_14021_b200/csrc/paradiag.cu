@@ -1325,7 +1325,8 @@ int paradiag_workspace_bytes(const pd_problem* p, int nranks, size_t* bytes) {
     if (p->m == 2048) b += (size_t)p->nt * ny * ((nx + 7) & ~7) * sizeof(double);
   }
   // (the opt-in pipelined solve, PARADIAG_PIPELINE=1, adds 2 more iterate-sized arrays)
-  if (p->jacobian == PD_JACOBIAN_TIME_AVG) b += (size_t)(kKryM + 2) * total * sizeof(double) + 2 * ns * sizeof(double);
+  // NEXT-4: the GMRES basis (kKryM + 1), b', and the device-side Arnoldi loop's fixed K in / out
+  if (p->jacobian == PD_JACOBIAN_TIME_AVG) b += (size_t)(kKryM + 4) * total * sizeof(double) + 2 * ns * sizeof(double);
   *bytes = b;
   return PD_OK;
 }
