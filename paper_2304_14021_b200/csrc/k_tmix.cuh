@@ -119,14 +119,18 @@ PD_DEV void mix_stage(double2* x, int pitch, int L, int len, const double2* __re
     double2 a[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) a[t] = x[(b + j + t * m) * pitch];
+    double2 w[R];                                    // W^{jq}: one load, powers by products (mix_stage_ct)
+    w[1] = mix_root<SIGN>(tab, j * stride);
+#pragma unroll
+    for (int q = 2; q < R; ++q) w[q] = cmul(w[q - 1], w[1]);
     if (SIGN > 0) {                                  // DIT: undo the twiddles first
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<+1>(tab, j * q * stride));
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
     }
     dft_r<R, SIGN>(a);
     if (SIGN < 0) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<-1>(tab, j * q * stride));
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) x[(b + j + t * m) * pitch] = a[t];
@@ -161,14 +165,22 @@ PD_DEV void mix_stage_ct(double2* x, int pitch, const double2* __restrict__ tab,
       double2 a[R];
 #pragma unroll
       for (int t = 0; t < R; ++t) a[t] = x[(b + j + t * m) * pitch];
-      if (SIGN > 0) {
+      // W^{jq} for q = 1..R-1: one table load, the powers by complex products (q - 1 extra roundings;
+      // the table gathers were the stage loop's long-scoreboard stalls)
+      double2 w[R];
+      if (m > 1) {
+        w[1] = mix_root<SIGN>(tab, j * stride);
 #pragma unroll
-        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<+1>(tab, j * q * stride));
+        for (int q = 2; q < R; ++q) w[q] = cmul(w[q - 1], w[1]);
+      }
+      if (SIGN > 0 && m > 1) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
       }
       dft_r<R, SIGN>(a);
-      if (SIGN < 0) {
+      if (SIGN < 0 && m > 1) {
 #pragma unroll
-        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], mix_root<-1>(tab, j * q * stride));
+        for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
       }
 #pragma unroll
       for (int t = 0; t < R; ++t) x[(b + j + t * m) * pitch] = a[t];
