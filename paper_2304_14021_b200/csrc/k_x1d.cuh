@@ -29,7 +29,8 @@ constexpr int kX1Threads = kX1Warps * 32;
 constexpr int kX1H = 32;                  // half transform size (N_x ≤ 64, or 65 Neumann nodes)
 constexpr int kX1K = 36;                  // B rows (K): j < 32, plus the centre j = 32 of N_x = 65
 constexpr int kX1BP = 40;                 // B tile pitch (doubles): modes i < 32, plus i = 32 (mode 64)
-constexpr int kX1RP = 70;                 // staged row pitch: 2 ghosts | up to 65 | 2 ghosts
+constexpr int kX1RP = 76;                 // staged row pitch: 2 ghosts | up to 65 | 2 ghosts; 76 ≡ 12 (mod 16
+                                          // doubles): the 8 rows × 4 columns of a fragment read hit 16 banks twice each
 constexpr int kX1In = 9 * kX1RP;          // one input buffer: 9 rows (MODE 0: rows n0-1 .. n0+7)
 constexpr size_t kX1Smem = (size_t)(2 * kX1K * kX1BP + kX1Warps * 2 * kX1In) * sizeof(double);
 
