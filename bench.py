@@ -155,13 +155,15 @@ def time_oracle(name, steps, warmup):
     U = iterate.initial_iterate(p, u0)
     for _ in range(warmup):
         U, _ = iterate.iterate_once(p, u0, U)
-    t0 = time.perf_counter()
-    for _ in range(steps):
+    ts = []
+    for _ in range(max(steps, 1)):
+        t0 = time.perf_counter()
         U, _ = iterate.iterate_once(p, u0, U)
-    dt = (time.perf_counter() - t0) / max(steps, 1)
+        ts.append(time.perf_counter() - t0)
+    dt = statistics.median(ts)
     desc = (f"oracle iterate_once (numpy fp64, naive O(N_t^2) DFT, dense DCT-I matmuls) on a "
-            f"{p.ny}x{p.nx} x N_t={p.nt} twin of {name} ({p.dofs} dofs), {steps} iteration(s)"
-            + ("; 1D: banded LU + refinement per bin" if p.dim == 1 else ""))
+            f"{p.ny}x{p.nx} x N_t={p.nt} twin of {name} ({p.dofs} dofs), median of {len(ts)} iteration(s) "
+            f"after {warmup} warm-up" + ("; 1D: banded LU + refinement per bin" if p.dim == 1 else ""))
     return p.dofs / dt, cores, desc, dt
 
 
@@ -656,7 +658,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, desc, dt = time_oracle(args.config, 1, 0)
+        v, cores, desc, dt = time_oracle(args.config, 3, 1)
         cpu = {"value": v, "unit": "dof/s", "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
