@@ -85,6 +85,10 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 2>), fast_time_smem(E));
   PD_ATTR((k_time2d_v2<E, kFastTimeWarps, 3>), fast_time_smem(E));
   if (fast_time_smem(E, 8) <= 227 * 1024) PD_ATTR((k_time2d_v2<E, 8>), fast_time_smem(E, 8));
+  if constexpr (E == 32) {    // the table variant of the row pass (A/B, tune 2^24)
+    PD_ATTR((k_rows3<1, E, kFastRowWarps, 0, 0>), dtt3_rows_smem<E>());
+    PD_ATTR((k_rows3<0, E, kFastRowWarps, 0, 0>), dtt3_rows_smem<E>());
+  }
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 1>), dtt3_rows_smem<E>() + 100 * 1024);
@@ -146,6 +150,8 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
     const bool gen = L.sin.n || L.sout.n;
     if (gen) k_rows3<NEUMANN, E, kFastRowWarps, 2><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     else if (L.upd) k_rows3<NEUMANN, E, kFastRowWarps, 3><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+    else if (E == 32 && (L.tune & (1 << 24)) && !L.amax)   // (A/B) the trig tables read every step
+      k_rows3<NEUMANN, E, kFastRowWarps, 0, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
   } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
@@ -249,7 +255,7 @@ bool fast_cols_tma_inv(int neumann, const double* in, const LineParams& L, const
     if (neumann) k_cols_tma_inv<1, NW, NS, E><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo); \
     else k_cols_tma_inv<0, NW, NS, E><<<grid, NW * 32, sm, F.stream>>>(in, L, F.trig2, lp, *tmo);
     if constexpr (E == 32) {
-      if (ns == 2) { PD_TI(2) } else if (ns == 3) { PD_TI(3) } else { PD_TI(kYsSlots) }
+if (ns == 2) { PD_TI(2) } else if (ns == 3) { PD_TI(3) } else { PD_TI(kYsSlots) }
     } else {
       PD_TI(kYsSlots)
     }

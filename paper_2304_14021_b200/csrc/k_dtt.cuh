@@ -36,7 +36,16 @@ PD_DEV void bulk_prefetch_l2(const void* p, size_t bytes, const void* limit) {
 
 __host__ __device__ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 
-template <int NEUMANN, int E>
+// Trig factors (CT > 0, the default kDttCT = 32): the pre-processing pairs (sin, cos)(π(2n, 2n+1)/M)
+// and the split factors (cos, sin)(2πk/M) are loaded exactly every CT-th step and rotated in
+// registers in between (one complex product per angle and step, ≤ CT − 1 roundings of a unit
+// rotation: a few ulp), so a line reads its three tables once instead of 32 times through L1.
+// Measured on c5 (r02, PARADIAG_TUNE A/B of the table (CT = 0), CT = 8 and CT = 32 variants):
+// x passes 9.26 → 9.08 → 8.91 ms, y 12.49 → 11.58 → 11.54 ms, y⁻¹ 10.29 → 9.33 → 9.30 ms — the
+// line passes are L1-bound (ncu r02za: l1tex 88 % in the row pass, 2.35e9 global-load sectors per
+// launch for 0.54e9 of line data) and the FP64 pipe has room for the rotations (29-39 %).
+constexpr int kDttCT = 32;
+template <int NEUMANN, int E, int CT = kDttCT>
 struct Dtt3 {
   static constexpr int P = 32 / E, M = 64 * E, H = 32 * E, LDX = M + 2;
   static constexpr int LOG2H = 5 + ilog2_c(E);
@@ -56,21 +65,29 @@ struct Dtt3 {
                                double g = 1.0) {
     double2 v[32];
     double x1p[P];
+    double2 rot = make_double2(1.0, 0.0);
+    if (CT) rot = __ldg(L.trig + 64);                                   // (cos, sin)(64π/M): n -> n + 32
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       double acc = 0.0;
       const double* x = xb + p * LDX;
+      double2 sn, cs;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int n = lane + 32 * e, j0 = 2 * n;
         const double2 a = *reinterpret_cast<const double2*>(x + j0);   // x_{2n}, x_{2n+1}
         const double m0 = x[M - j0], m1 = x[M - j0 - 1];
-        const double2 sn = __ldg(L.trigs + n);                          // sin(π(2n, 2n+1)/M)
-        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, sn.x), ymap<NEUMANN>(a.y, m1, sn.y));
-        if (NEUMANN) {
-          const double2 cs = __ldg(L.trigc + n);                        // cos(π(2n, 2n+1)/M)
-          acc = fma(a.x - m0, cs.x, fma(a.y - m1, cs.y, acc));
+        if (!CT || e % (CT > 0 ? CT : 1) == 0) {
+          sn = __ldg(L.trigs + n);                                      // sin(π(2n, 2n+1)/M)
+          if (NEUMANN || CT) cs = __ldg(L.trigc + n);                   // cos(π(2n, 2n+1)/M)
+        } else {                                                        // rotate both angles by 64π/M
+          const double c0 = fma(cs.x, rot.x, -sn.x * rot.y), s0 = fma(sn.x, rot.x, cs.x * rot.y);
+          const double c1 = fma(cs.y, rot.x, -sn.y * rot.y), s1 = fma(sn.y, rot.x, cs.y * rot.y);
+          cs = make_double2(c0, c1);
+          sn = make_double2(s0, s1);
         }
+        v[p * E + e] = make_double2(ymap<NEUMANN>(a.x, m0, sn.x), ymap<NEUMANN>(a.y, m1, sn.y));
+        if (NEUMANN) acc = fma(a.x - m0, cs.x, fma(a.y - m1, cs.y, acc));
       }
       x1p[p] = acc;
     }
@@ -91,6 +108,8 @@ struct Dtt3 {
     const double g2 = 2.0 * g;
     double run = 0.0;
     double2 Z0 = make_double2(0.0, 0.0);
+    double2 t, r2 = make_double2(1.0, 0.0);
+    if (CT) r2 = __ldg(L.trig + 2);                                     // (cos, sin)(2π/M): k -> k + 1
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int k = 32 * b + j;
@@ -98,7 +117,8 @@ struct Dtt3 {
       const double2 Zm = T[tpad(pl * H + ((H - k) & (H - 1)))];
       const double2 Ev = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
       const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
-      const double2 t = __ldg(trig2 + j * E + b);
+      if (!CT || j % (CT > 0 ? CT : 1) == 0) t = __ldg(trig2 + j * E + b);
+      else t = make_double2(fma(t.x, r2.x, -t.y * r2.y), fma(t.y, r2.x, t.x * r2.y));
       const double Yx = Ev.x + t.x * O.x + t.y * O.y;
       const double Yy = Ev.y + t.x * O.y - t.y * O.x;
       double ev, a;
@@ -214,12 +234,12 @@ PD_DEV void update_line(const double* __restrict__ ob, double* __restrict__ U, i
 // V: 0 plain (no block I/O, no ‖·‖∞, no fused update), 1 with the ‖·‖∞ epilogue, 2 general
 // (runtime block maps / fused update / ‖·‖∞), 3 the fused update (tune 16) — the common passes
 // compile without the branches
-template <int NEUMANN, int E, int NW, int V = 2>
+template <int NEUMANN, int E, int NW, int V = 2, int CT = kDttCT>
 __global__ void __launch_bounds__(NW * 32, 2)
 k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
   constexpr bool GEN = V == 2;
   constexpr bool UPD = V == 3 || GEN;             // V = 3: the fused update only
-  using D = Dtt3<NEUMANN, E>;
+  using D = Dtt3<NEUMANN, E, CT>;
   extern __shared__ double2 smem2[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* xb = reinterpret_cast<double*>(smem2) + (size_t)warp * D::BUF;
@@ -561,10 +581,10 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
 // element.  The natural-layout side keeps k_cols3's column-tile staging.
 // DIR 0: in natural [n][y][x] (slice pitch L.ps_in) -> out column-major wt;
 // DIR 1: in column-major wt -> out natural [n][y][x] (slice pitch L.ps_out).  L.upd unused.
-template <int NEUMANN, int E, int NW, int DIR>
+template <int NEUMANN, int E, int NW, int DIR, int CT = kDttCT>
 __global__ void __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1)
 k_cols_cm(const double* in, double* out, LineParams L, const double2* __restrict__ trig2, int64_t lp) {
-  using D = Dtt3<NEUMANN, E>;
+  using D = Dtt3<NEUMANN, E, CT>;
   constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;
   constexpr int C = NW * D::P;
   constexpr int NTH = NW * 32;
@@ -726,11 +746,11 @@ constexpr size_t kYsRing = (size_t)kYsSlots * kYsRows * 8 * sizeof(double);   //
 template <int E>
 __host__ __device__ constexpr int ys_rows() { return kYsRows * 8 / (8 * 32 / E); }
 
-template <int NEUMANN, int NW, int NS = kYsSlots, int E = 32>
+template <int NEUMANN, int NW, int NS = kYsSlots, int E = 32, int CT = kDttCT>
 __global__ void __launch_bounds__(NW * 32, 1)
 k_cols_tma_inv(const double* in, LineParams L, const double2* __restrict__ trig2, int64_t lp,
                const __grid_constant__ CUtensorMap tmo) {
-  using D = Dtt3<NEUMANN, E>;
+  using D = Dtt3<NEUMANN, E, CT>;
   constexpr int kNel = NEUMANN ? D::M + 1 : D::M - 1;
   constexpr int C = NW * D::P;
   static_assert(C * 8 <= 256, "box rows of at most 32 doubles");

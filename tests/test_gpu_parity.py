@@ -282,3 +282,35 @@ def test_padded_workspace_path_bit_identical(cuda_lib, monkeypatch, bc_cfg, m):
         s.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert np.array_equal(out[0][0], out[0][1])
+
+
+@pytest.mark.parametrize("bc_cfg", ["c5", "c3"])
+def test_precond_parity_production_y_passes(cuda_lib, bc_cfg):
+    """M = 2048 with N_t ≥ 32 runs the production line kernels of c5 — k_rows3 into the padded
+    workspace wp, k_cols_cm into the column-major wt, the TMA time pass, k_cols_tma_inv, k_rows3 —
+    with the trig factors rotated in registers between exact table loads (Dtt3 CT = 32): compared
+    element-wise with the oracle, both BCs (DCT-I / DST-I), out of place and in place."""
+    p = twin(bc_cfg, m=2048, nt=32)
+    r = np.random.default_rng(43).uniform(-1, 1, gshape(p))
+    s = cuda_lib.Solver(p)
+    rd = to_dev(r, p)
+    d = s.empty()
+    s.apply_precond(rd, d, 0.0)
+    d_o, _ = precond.apply_precond(p, r, 0.0)
+    assert rel_err(to_host(d, p), d_o) <= 1e-11
+    s.apply_precond(rd, rd, 0.0)
+    assert np.array_equal(to_host(rd, p), to_host(d, p))
+
+
+@pytest.mark.parametrize("name", ["c5_m2048_nt4", "c3_m2048_nt2"])
+def test_precond_parity_table_trig(cuda_lib, monkeypatch, name):
+    """The table variant of the row pass (PARADIAG_TUNE bit 24: trig factors read every step, the
+    A/B baseline of the computed factors) against the oracle at M = 2048, both BCs."""
+    monkeypatch.setenv("PARADIAG_TUNE", str(1 << 24))
+    p = CASES[name]
+    r = _rand_U(p, 12)
+    s = cuda_lib.Solver(p)
+    d = s.empty()
+    s.apply_precond(to_dev(r, p), d, 0.0)
+    d_o, _ = precond.apply_precond(p, r, 0.0)
+    assert rel_err(to_host(d, p), d_o) <= 1e-11
