@@ -63,6 +63,9 @@ inline size_t dttp_rows_smem() { return (size_t)kPairsPerRowCta * DttPair<1>::BU
 inline size_t dttp_cols_smem() { return (size_t)8 * DttPair<1>::BUF * sizeof(double); }
 template <int E>
 size_t dtt3_rows_smem() { return (size_t)kFastRowWarps * Dtt3<1, E>::BUF * sizeof(double); }
+// k_rows3 with bulk row loads (BK = 1): the per-warp mbarriers follow the line buffers
+template <int E>
+size_t dtt3_rows_bulk_smem() { return dtt3_rows_smem<E>() + kFastRowWarps * 8; }
 template <int E>
 size_t dtt3_cols_smem() { return (size_t)fast_col_warps(E) * Dtt3<1, E>::BUF * sizeof(double); }
 
@@ -88,6 +91,7 @@ cudaError_t fast_attrs() {
   if constexpr (E == 32) {    // the table variant of the row pass (A/B, tune 2^24)
     PD_ATTR((k_rows3<1, E, kFastRowWarps, 0, 0>), dtt3_rows_smem<E>());
     PD_ATTR((k_rows3<0, E, kFastRowWarps, 0, 0>), dtt3_rows_smem<E>());
+    PD_ATTR((k_rows3<1, E, kFastRowWarps, 0, kDttCT, 1>), dtt3_rows_bulk_smem<E>());
   }
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 0>), dtt3_rows_smem<E>() + 100 * 1024);
@@ -153,7 +157,10 @@ void fast_line_bc(int axis, const double* in, double* out, const LineParams& L, 
     else if (E == 32 && (L.tune & (1 << 24)) && !L.amax)   // (A/B) the trig tables read every step
       k_rows3<NEUMANN, E, kFastRowWarps, 0, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
     else if (L.amax) k_rows3<NEUMANN, E, kFastRowWarps, 1><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
-    else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
+    else if (NEUMANN && E == 32 && !(L.tune & (1 << 25)) && L.ldi > L.nx && L.ldi % 2 == 0 && ((uintptr_t)in & 15) == 0) {
+      if constexpr (NEUMANN && E == 32)      // rows of wp in by bulk copy (x⁻¹); (A/B) tune 2^25: per-element copies
+        k_rows3<1, E, kFastRowWarps, 0, kDttCT, 1><<<grid, kFastRowWarps * 32, dtt3_rows_bulk_smem<E>(), F.stream>>>(in, out, L, F.trig2);
+    } else k_rows3<NEUMANN, E, kFastRowWarps, 0><<<grid, kFastRowWarps * 32, smem, F.stream>>>(in, out, L, F.trig2);
   } else if (L.tune & 64) {     // 4-warp column CTAs, two per SM (A/B)
     constexpr int C4 = 4 * (32 / E);
     const int64_t groups = (int64_t)F.nt * ((F.nx + C4 - 1) / C4);

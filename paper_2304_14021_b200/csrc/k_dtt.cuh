@@ -234,15 +234,40 @@ PD_DEV void update_line(const double* __restrict__ ob, double* __restrict__ U, i
 // V: 0 plain (no block I/O, no ‖·‖∞, no fused update), 1 with the ‖·‖∞ epilogue, 2 general
 // (runtime block maps / fused update / ‖·‖∞), 3 the fused update (tune 16) — the common passes
 // compile without the branches
-template <int NEUMANN, int E, int NW, int V = 2, int CT = kDttCT>
+// BK = 1 (plain Neumann variant reading rows of the padded workspace wp: 16-byte aligned, even
+// pitch): the warp's lines arrive by one bulk copy each (lane 0 issues, a per-warp mbarrier
+// completes) instead of one 8-byte cp.async per element: c5 x⁻¹ 9.01 -> 8.58 ms.  (The store side
+// through per-lane 512-byte bulk stores of a 16-byte aligned staging layout measured 8.96 -> 9.02 ms
+// on the forward x pass: not kept.)
+// The forward x pass reads the residual at the odd pitch N_x, where every other row starts 8 bytes
+// past a 16-byte boundary: starting those rows' bulk copies one double earlier and reading the line
+// one double in (the mirrored pair becomes the aligned 16-byte read) is bit-identical but measured
+// 8.91 -> 9.51 ms with a second transform instance and 9.05 ms with a warp-uniform branch in the
+// pre-processing loop: not kept.  Nor was a de-interleaved staging layout for the per-element copies
+// (x_{2i} at xb[i], x_{2i+1} behind them, so all four pre-processing reads are unit-stride: 8
+// instead of 12 shared-memory wavefronts per step): bit-identical, 8.90 -> 9.59 ms.
+// Occupancy: the register file is per SM sub-partition (16 K registers), so a ninth warp needs
+// <= 170 registers per thread; ptxas then takes 168 and spills 96-128 B, and the x passes measured
+// 12.6 / 12.0 ms with 9 warps per SM against 8.9 / 8.5 ms with 8 warps at 255 registers.
+template <int NEUMANN, int E, int NW, int V = 2, int CT = kDttCT, int BK = 0>
 __global__ void __launch_bounds__(NW * 32, 2)
 k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__ trig2) {
+  static_assert(BK == 0 || (NEUMANN == 1 && V == 0), "bulk row loads: plain Neumann variant only");
   constexpr bool GEN = V == 2;
   constexpr bool UPD = V == 3 || GEN;             // V = 3: the fused update only
   using D = Dtt3<NEUMANN, E, CT>;
   extern __shared__ double2 smem2[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* xb = reinterpret_cast<double*>(smem2) + (size_t)warp * D::BUF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem2) + (size_t)NW * D::BUF) + warp;
+  unsigned phase = 0;
+  if (BK) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+  }
   double lmax = 0.0;
   unsigned long long ubits = 0ull;
   const int64_t ngroups = (L.nlines + D::P - 1) / D::P;
@@ -265,8 +290,22 @@ k_rows3(const double* in, double* out, LineParams L, const double2* __restrict__
     // fused update: bring this group's U rows towards L2 now, they are read after the transform
     if (UPD && L.upd && lane == 0)
       bulk_prefetch_l2(L.upd + L0 * L.nx, (size_t)nl * L.nx * sizeof(double), L.upd + L.nlines * L.nx);
+    constexpr unsigned kRowBytes = (unsigned)(D::M + 2) * 8;     // x_0..x_M and one pad double of the row
+    if (BK) {                                                  // whole rows of wp by bulk copy
+      fence_proxy_async();                                     // the buffer's generic accesses come first
+      __syncwarp();
+      if (lane == 0) {
+        mbar_expect_tx(bar, (unsigned)nl * kRowBytes);
+        for (int p = 0; p < nl; ++p)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(xb + p * D::LDX)), "l"(src + p * ldi), "r"(kRowBytes), "r"(smem_u32(bar))
+                       : "memory");
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+    }
 #pragma unroll
-    for (int p = 0; p < D::P; ++p) {
+    for (int p = 0; p < (BK ? 0 : D::P); ++p) {
       if (p < nl) {
         double* x = xb + p * D::LDX + (NEUMANN ? 0 : 1);
         if (GEN && L.sin.n) {                              // transpose blocks

@@ -302,6 +302,24 @@ def test_precond_parity_production_y_passes(cuda_lib, bc_cfg):
     assert np.array_equal(to_host(rd, p), to_host(d, p))
 
 
+def test_bulk_row_loads_bit_identical(cuda_lib, monkeypatch):
+    """The inverse x pass of the Neumann M = 2048 path takes its rows of the padded workspace wp by
+    one bulk copy per line (k_rows3 BK = 1, the default); PARADIAG_TUNE bit 25 switches back to the
+    per-element copies.  Only the data movement differs: P_α⁻¹ must agree bit for bit (and the
+    default is compared with the oracle in test_precond_parity_production_y_passes)."""
+    p = twin("c5", m=2048, nt=32)
+    r = np.random.default_rng(47).uniform(-1, 1, gshape(p))
+    out = []
+    for tune in ("0", str(1 << 25)):
+        monkeypatch.setenv("PARADIAG_TUNE", tune)
+        s = cuda_lib.Solver(p)
+        d = s.empty()
+        s.apply_precond(to_dev(r, p), d, 0.0)
+        out.append(to_host(d, p))
+        s.close()
+    assert np.array_equal(out[0], out[1])
+
+
 @pytest.mark.parametrize("name", ["c5_m2048_nt4", "c3_m2048_nt2"])
 def test_precond_parity_table_trig(cuda_lib, monkeypatch, name):
     """The table variant of the row pass (PARADIAG_TUNE bit 24: trig factors read every step, the

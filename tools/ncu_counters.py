@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 # ncu kernel name (prefix) -> library kernel name; k_rows3 runs twice per iteration (forward, inverse)
-MAP = [("k_residual_tile", "residual"), ("k_cols_cm<1, 32, 8, 0>", "dtt_y_fwd"), ("k_cols_cm<1, 32, 8, 1>", "dtt_y_inv"),
+MAP = [("k_residual_tile", "residual"), ("k_cols_cm<1, 32, 8, 0", "dtt_y_fwd"), ("k_cols_cm<1, 32, 8, 1", "dtt_y_inv"),
        ("k_cols_tma_inv", "dtt_y_inv"),
        ("k_time2d_v4", "time_solve_2d"), ("k_update", "update"), ("k_rows3", ("dtt_x_fwd", "dtt_x_inv")),
        ("k_cols3", ("dtt_y_fwd", "dtt_y_inv")), ("k_time2d_v2", "time_solve_2d")]
@@ -24,7 +24,10 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "
 
 
 def main(path, out):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):          # the raw page already exported on the GPU box (large reports stay there)
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")

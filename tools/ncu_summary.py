@@ -21,7 +21,10 @@ STALL = re.compile(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active.ra
 
 
 def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):          # the raw page already exported on the GPU box (large reports stay there)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
