@@ -27,6 +27,9 @@ struct ResidualParams {
   const double* dU;
   double* unew;
   unsigned long long* umax;
+  // k_residual_tile<.., PADR = true> (opt-in A/B): r is written at row pitch ldr and slice pitch
+  // nsr (the padded exchange workspace wp, so the forward x pass can take its rows by bulk copy)
+  int64_t ldr, nsr;
 };
 
 // Reflect an out-of-range Neumann index back onto the node grid (ghost u_{-1} = u_1).
@@ -338,7 +341,7 @@ static_assert(kResIX * kResGroups == kResThreads, "one thread per inner column a
 // VAR: 0 general (runtime CH / slab-halo checks), 1 linear kind on a single handle, 3 linear kind on
 // a slab (halo rows, no CH branch), 2 CH kind on a
 // single handle — the single-handle variants are compiled without those branches
-template <int MODE, bool UPD = false, int VAR = 0>
+template <int MODE, bool UPD = false, int VAR = 0, bool PADR = false>
 __global__ void __launch_bounds__(kResThreads)
 k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, double* __restrict__ r,
                 ResidualParams P, double* __restrict__ jpart) {
@@ -435,6 +438,8 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
                                     : 0.0;
     }
   }
+  // PADR: this thread's first output of slice 0 (row pitch ldr, slice pitch nsr)
+  double* const rpad = r + (size_t)(y0 + ty0) * (size_t)(PADR ? P.ldr : 0) + gx;
   double jloc = 0.0;
   // θ < 1 / PinT-II need A U_{n-1} / L U_{n-1}: march one extra (output-free) slice n0-1 first;
   // the quantity of every slice is then carried to the next in registers like U_{n-1}
@@ -466,7 +471,7 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
     }
     __syncthreads();
     // ---- outer stencil + time difference down the output strip
-    double* rn = r + (size_t)max(n, 0) * ns;
+    double* rn = PADR ? rpad + (size_t)max(n, 0) * (size_t)P.nsr : r + (size_t)max(n, 0) * ns;
     if (tx < kResTX) {
       const double* I = sI + (ty0 + 1) * kResIP + (tx + 1);
       const double* cu = cur + (ty0 + 2) * kResUP + (tx + 2);
@@ -493,7 +498,8 @@ k_residual_tile(const double* __restrict__ u0, const double* __restrict__ U, dou
           if (thet) prevA[j] = Au;
         }
         if (n >= n0 && gx < P.nx && gy < P.ny) {
-          rn[(size_t)gy * P.nx + gx] = outv;
+          if (PADR) rn[(size_t)j * (size_t)P.ldr] = outv;
+          else rn[(size_t)gy * P.nx + gx] = outv;
           if (UPD) {
             P.unew[(size_t)n * ns + (size_t)gy * P.nx + gx] = uo;
             ubits = max(ubits, (unsigned long long)__double_as_longlong(uo) & 0x7fffffffffffffffull);

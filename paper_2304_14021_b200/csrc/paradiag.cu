@@ -387,6 +387,7 @@ ResidualParams residual_params(pd_handle* h) {
   R.inv_h2 = h->inv_h2; R.inv_dt = h->inv_dt; R.b2 = h->b2; R.e2 = h->e2;
   R.y0g = 0; R.nyg = h->ny; R.hlo = nullptr; R.hhi = nullptr; R.theta = h->P.theta;
   R.dU = nullptr; R.unew = nullptr; R.umax = &h->st->umax_bits;
+  R.ldr = h->nx; R.nsr = h->ns;
   return R;
 }
 
@@ -416,10 +417,12 @@ int launch_x1d(pd_handle* h, int mode, const double* u0, const double* in, doubl
   return PD_OK;
 }
 
+// ldr != 0 (residual_to_wp): r is the padded workspace wp, row pitch ldr, slice pitch ny·ldr
 int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, const double* dU = nullptr,
-                    double* unew = nullptr) {
+                    double* unew = nullptr, int64_t ldr = 0) {
   ResidualParams R = residual_params(h);
   R.dU = dU; R.unew = unew;
+  if (ldr) { R.ldr = ldr; R.nsr = (int64_t)h->ny * ldr; }
   const int kid = dU ? K_RESUPD : K_RESIDUAL;
   prof_begin(h, kid);
   size_t nparts = 0;     // CH: J̄ partial sums written by this launch (summed in a fixed order)
@@ -438,6 +441,8 @@ int launch_residual(pd_handle* h, const double* u0, const double* U, double* r, 
         k_residual_tile<2, false, 2><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (h->P.theta != 1.0)
         k_residual_tile<1, false, 1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
+      else if (!is_ch(h->P.kind) && ldr)
+        k_residual_tile<0, false, 1, true><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else if (!is_ch(h->P.kind))       // linear, single handle (launch_residual has no slab halos)
         k_residual_tile<0, false, 1><<<grd, kResThreads, kResSmem, h->stream>>>(u0, U, r, R, h->jpart);
       else                              // CH PinT-I, single handle
@@ -675,10 +680,23 @@ bool can_fuse_update(const pd_handle* h) {
          h->P.m <= 2048;
 }
 
+// (A/B, opt-in: tune 2^26) 2D linear kinds with Neumann lines on the padded-workspace path (c5): the
+// residual writes r into wp at its 64-byte aligned row pitch, so the forward x pass takes its rows
+// by bulk copy like the inverse one (k_rows3 BK = 1) and runs in place.  Bit-identical; measured on
+// c5: x 8.92 -> 8.49 ms but the residual 7.54 -> 8.33 ms (reading U at pitch 2049 while writing r
+// at pitch 2056, with either form of the store addressing), 64.3 -> 64.7 ms per iteration: off.
+bool residual_to_wp(pd_handle* h) {
+  return h->P.dim == 2 && !is_ch(h->P.kind) && h->P.theta == 1.0 && h->neumann && h->P.m == 2048 && h->wt && h->wp &&
+         h->dtt_ver == 3 && h->fast && !h->tlong && (h->tune & (1 << 26)) && !(h->tune & (65536 | 16 | 32)) &&
+         h->P.jacobian != PD_JACOBIAN_TIME_AVG;
+}
+
 // δ = P_α⁻¹ r; with U_fused != NULL (can_fuse_update) the last pass adds δ to U_fused instead of
 // storing δ (‖δ‖∞ and ‖U‖∞ reduced on the way).
 // want_dmax = false: the caller's update folds ‖δ‖∞ (2D: the last x pass runs its plain variant).
-int precond(pd_handle* h, const double* r, double* delta, double* U_fused = nullptr, bool want_dmax = true) {
+// r_in_wp: r already lies in wp at its padded pitch (residual_to_wp), the forward x pass runs in place.
+int precond(pd_handle* h, const double* r, double* delta, double* U_fused = nullptr, bool want_dmax = true,
+            bool r_in_wp = false) {
   unsigned long long* dmax = &h->st->dmax_bits;
   if (h->P.dim == 2) {
     int rc;
@@ -689,7 +707,10 @@ int precond(pd_handle* h, const double* r, double* delta, double* U_fused = null
     const bool use_wt = h->wt && h->dtt_ver == 3 && !(h->tune & 65536);   // tune 65536 (A/B): the in-place v2 time pass
     const bool use_wp = use_wt && h->wp;          // x, y passes exchange data through wp
     double* xo = use_wp ? h->wp : delta;           // x-pass output / x⁻¹-pass input
-    if ((rc = launch_lines(h, r, xo, 0, nullptr, K_XFWD, nullptr, nullptr, 0, 0, 0, use_wp ? h->lpx : 0))) return rc;
+    if (r_in_wp && !use_wp) return fail(PD_EINVAL, "residual in wp without the padded-workspace path");
+    if ((rc = launch_lines(h, r_in_wp ? h->wp : r, xo, 0, nullptr, K_XFWD, nullptr, nullptr, 0, 0, r_in_wp ? h->lpx : 0,
+                           use_wp ? h->lpx : 0)))
+      return rc;
     // (measured and not kept: TMA loads of the natural side through a 4-chunk staging ring, whole
     // tile 13.9 ms or half of it prefetched during the transform 14.4 ms, and TMA box stores of the
     // wt lines through the same ring 16.1 ms, against 12.3 ms for per-element cp.async + coalesced
@@ -1045,6 +1066,10 @@ int enqueue_iteration(pd_handle* h, const double* u0, double* U) {
     if ((rc = launch_x1d(h, 0, u0, U, h->work, K_XRES))) return rc;
     if ((rc = tlong_time(h, h->work, h->work))) return rc;
     if ((rc = launch_x1d(h, 3, nullptr, h->work, U, K_XUPD))) return rc;
+  } else if (residual_to_wp(h)) {   // r straight into wp: the forward x pass bulk-loads its rows, in place
+    if ((rc = launch_residual(h, u0, U, h->wp, nullptr, nullptr, h->lpx))) return rc;
+    if ((rc = precond(h, h->wp, h->work, nullptr, false, true))) return rc;
+    if ((rc = launch_update(h, U, h->work, true))) return rc;
   } else if ((rc = launch_residual(h, u0, U, h->work))) {
     return rc;
   } else if (can_fuse_update(h)) {
@@ -1687,6 +1712,7 @@ int init_impl(const pd_problem* p, int device, void* cuda_stream, pd_handle** ou
     }
     PD_TRY(allow_smem(k_residual_tile<0>, kResSmem));
     PD_TRY(allow_smem((k_residual_tile<0, false, 1>), kResSmem));
+    PD_TRY(allow_smem((k_residual_tile<0, false, 1, true>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<0, false, 2>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<0, false, 3>), kResSmem));
     PD_TRY(allow_smem((k_residual_tile<1, false, 1>), kResSmem));

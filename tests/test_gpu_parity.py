@@ -320,6 +320,27 @@ def test_bulk_row_loads_bit_identical(cuda_lib, monkeypatch):
     assert np.array_equal(out[0], out[1])
 
 
+def test_residual_into_padded_workspace_bit_identical(cuda_lib, monkeypatch):
+    """PARADIAG_TUNE bit 26 (opt-in A/B): Neumann M = 2048 linear iterations write the residual
+    straight into the padded workspace wp (k_residual_tile PADR), so the forward x pass bulk-loads
+    its rows and runs in place.  Same arithmetic, other addresses: two iterations must agree bit for
+    bit with the default path (r in the work array), with the same ‖δ‖∞."""
+    p = twin("c5", m=2048, nt=32)
+    u0 = make_u0(p)
+    U0 = np.random.default_rng(53).uniform(-1, 1, gshape(p))
+    out = []
+    for tune in ("0", str(1 << 26)):
+        monkeypatch.setenv("PARADIAG_TUNE", tune)
+        s = cuda_lib.Solver(p)
+        U = to_dev(U0, p)
+        info = None
+        for _ in range(2):
+            info = s.iterate(to_dev(u0), U, info)
+        out.append((to_host(U, p), info.delta_max))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("name", ["c5_m2048_nt4", "c3_m2048_nt2"])
 def test_precond_parity_table_trig(cuda_lib, monkeypatch, name):
     """The table variant of the row pass (PARADIAG_TUNE bit 24: trig factors read every step, the
