@@ -2,6 +2,7 @@
 // k_fast.cuh time pass), one instantiation per E = transform length / 32 in its own translation
 // unit (fast_e<E>.cu) so the library builds in parallel.  paradiag.cu sees only the declarations.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -101,6 +102,14 @@ cudaError_t fast_attrs() {
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 2>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<1, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
   PD_ATTR((k_rows3<0, E, kFastRowWarps, 3>), dtt3_rows_smem<E>() + 100 * 1024);
+  if constexpr (E == 32) {   // (A/B) PARADIAG_CARVE: preferred shared-memory carve-out (percent) of the cp.async line passes
+    if (const char* cv = getenv("PARADIAG_CARVE")) {
+      const int pc = atoi(cv);
+      cudaFuncSetAttribute(k_cols_cm<1, E, fast_col_warps(E), 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+      cudaFuncSetAttribute(k_rows3<1, E, kFastRowWarps, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+      cudaFuncSetAttribute(k_rows3<1, E, kFastRowWarps, 0, kDttCT, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+    }
+  }
   PD_ATTR((k_cols_cm<1, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols_cm<0, E, fast_col_warps(E), 0>), dtt3_cols_smem<E>());
   PD_ATTR((k_cols_cm<1, E, fast_col_warps(E), 1>), dtt3_cols_smem<E>());

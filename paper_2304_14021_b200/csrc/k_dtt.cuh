@@ -618,6 +618,13 @@ k_cols3(const double* in, double* out, LineParams L, const double2* __restrict__
 // (coalesced, like a row pass) instead of a 64-byte-wide column tile — the forward pass stores its
 // lines with store_line, the inverse pass loads them with one 8-byte cp.async per lane and
 // element.  The natural-layout side keeps k_cols3's column-tile staging.
+// Measured and not kept (round 2, after the trig factors left the tables): a forward variant with 13
+// line slots (216 KB) that issues columns 0-4 of the next tile into the 5 free slots right after the
+// tile barrier, so only 3/8 of a tile's loads stay exposed between two transforms: parity-green,
+// 11.5 -> 18.0 ms on c5.  The per-element cp.async.ca loads land through L1, and a CTA that takes the
+// 228 KB shared-memory carve-out leaves 28 KB of it: the lines in flight, not the tables, are what
+// the earlier prefetch / ring variants of this pass lost with their L1 (bulk and TMA copies bypass
+// it, which is why the inverse pass and the time pass can afford their rings).
 // DIR 0: in natural [n][y][x] (slice pitch L.ps_in) -> out column-major wt;
 // DIR 1: in column-major wt -> out natural [n][y][x] (slice pitch L.ps_out).  L.upd unused.
 template <int NEUMANN, int E, int NW, int DIR, int CT = kDttCT>
